@@ -1,0 +1,342 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run in the build container (the reference is importable read-only there):
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz. The GPU box never runs this (it has no
+/root/reference); tests only read the committed .npz files. Every case is
+built from the reference's own seeded builders (make_rng / make_hyena_config /
+testing.random_*), so the inputs are bit-reproducible.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from convhybrid import blockconv as bc  # noqa: E402
+from convhybrid import cpsim, hyena  # noqa: E402
+from convhybrid import fft as fftmod  # noqa: E402
+from convhybrid.core import (  # noqa: E402
+    ExplicitFilter,
+    GroupSpec,
+    ImplicitFilter,
+    RegularizedFilter,
+    SeqTensor,
+    direct_causal_conv,
+    materialize_filter,
+    uniform_groups,
+)
+from convhybrid.rand import make_rng  # noqa: E402
+from convhybrid.testing import random_explicit_groups, random_mixed_groups, random_seq  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def bank_arrays(prefix: str, g: GroupSpec) -> dict:
+    """Serialize a GroupSpec (any filter kind, one kind per bank) to flat arrays."""
+    out = {f"{prefix}.channels": g.channels, f"{prefix}.group_size": g.group_size}
+    f0 = g.filters[0]
+    kinds = {type(f) for f in g.filters}
+    if len(kinds) > 1:
+        out[f"{prefix}.kind"] = "mixed"
+        out[f"{prefix}.taps"] = g.materialized()
+        return out
+    if isinstance(f0, ExplicitFilter):
+        out[f"{prefix}.kind"] = "explicit"
+        out[f"{prefix}.taps"] = np.stack([f.taps for f in g.filters])
+    elif isinstance(f0, RegularizedFilter):
+        out[f"{prefix}.kind"] = "regularized"
+        out[f"{prefix}.taps_hat"] = np.stack([f.taps_hat for f in g.filters])
+        out[f"{prefix}.rate"] = np.array([f.decay_rate for f in g.filters])
+        out[f"{prefix}.base"] = np.array([f.base for f in g.filters])
+    else:
+        out[f"{prefix}.kind"] = "implicit"
+        out[f"{prefix}.residues"] = np.stack([f.residues for f in g.filters])
+        out[f"{prefix}.poles"] = np.stack([f.poles for f in g.filters])
+        out[f"{prefix}.length"] = f0.length
+    out[f"{prefix}.materialized"] = g.materialized()
+    return out
+
+
+def cfg_arrays(prefix: str, cfg: hyena.HyenaConfig) -> dict:
+    out = {f"{prefix}.variant": cfg.variant, f"{prefix}.width": cfg.width,
+           f"{prefix}.block_size": cfg.block_size, f"{prefix}.backend": cfg.backend}
+    for name in ("w_q", "w_k", "w_v", "w_out"):
+        out[f"{prefix}.{name}"] = hyena.projection_dense(getattr(cfg, name))
+    for name in ("q_feat", "k_feat", "v_feat", "inner"):
+        out.update(bank_arrays(f"{prefix}.{name}", getattr(cfg, name)))
+    return out
+
+
+def save(name: str, cases: dict) -> None:
+    path = os.path.join(OUT, f"{name}.npz")
+    np.savez_compressed(path, **{k: np.asarray(v) for k, v in cases.items()})
+    print(f"wrote {path} ({len(cases)} arrays)")
+
+
+def gen_direct() -> None:
+    c = {}
+    # reference hand values (pkg/tests/test_core.py:124-137)
+    c["hand0.x"] = [[1.0, 2.0, 3.0, 4.0]]
+    c["hand0.taps"] = [[1.0, 1.0]]
+    c["hand0.y"] = direct_causal_conv(SeqTensor(c["hand0.x"]), uniform_groups(1, [1.0, 1.0])).data
+    c["hand1.x"] = [[1.0, 2.0, 3.0, 4.0]]
+    c["hand1.taps"] = [[0.0, 1.0]]
+    c["hand1.y"] = direct_causal_conv(SeqTensor(c["hand1.x"]), uniform_groups(1, [0.0, 1.0])).data
+    c["hand2.x"] = [[1.0, 1.0]]
+    c["hand2.taps"] = [[1.0, 2.0, 3.0, 4.0]]
+    c["hand2.y"] = direct_causal_conv(SeqTensor(c["hand2.x"]), uniform_groups(1, [1.0, 2.0, 3.0, 4.0])).data
+    for i in range(3):
+        c[f"hand{i}.gs"] = 1
+    rng = make_rng(500)
+    shapes = [(3, 1, 40, 5), (4, 2, 50, 6), (2, 1, 3, 9), (6, 3, 30, 4), (8, 8, 64, 14),
+              (5, 1, 33, 1), (16, 1, 300, 7), (4, 2, 257, 40), (2, 1, 1000, 129), (3, 3, 4099, 7)]
+    n = 0
+    for dtype in ("f64", "f32"):
+        for d, gs, length, lh in shapes:
+            g = random_explicit_groups(rng, d, gs, lh)
+            x = random_seq(rng, d, length, dtype=dtype)
+            y = direct_causal_conv(x, g)
+            c[f"rand{n}.x"] = x.data
+            c[f"rand{n}.taps"] = g.materialized()
+            c[f"rand{n}.gs"] = gs
+            c[f"rand{n}.y"] = y.data
+            n += 1
+    c["n_rand"] = n
+    save("direct_conv", c)
+
+
+def gen_blockconv() -> None:
+    c = {}
+    rng = make_rng(510)
+    # paper H0/H1 worked example (pkg/tests/test_blockconv.py:25-42)
+    h = rng.standard_normal(4)
+    f = bc.build_factors(h, 3)
+    c["factors.h"] = h
+    c["factors.blocks"] = f.blocks
+    # two-stage (gated and ungated), both dtypes
+    n = 0
+    for dtype in ("f64", "f32"):
+        for d, dg, length, lh, lb, gated in ((1, 1, 48, 3, 4, False), (4, 4, 96, 17, 16, False),
+                                              (6, 2, 65, 8, 8, True), (4, 2, 40, 5, 8, True),
+                                              (8, 1, 1000, 129, 128, True), (3, 1, 300, 128, 128, True),
+                                              (2, 2, 2051, 100, 128, False), (5, 1, 130, 7, 16, True)):
+            g = random_explicit_groups(rng, d, dg, lh)
+            v = random_seq(rng, d, length, dtype)
+            q = random_seq(rng, d, length, dtype) if gated else None
+            k = random_seq(rng, d, length, dtype) if gated else None
+            y = bc.two_stage_forward(v, g, lb, q=q, k=k)
+            c[f"ts{n}.v"] = v.data
+            if gated:
+                c[f"ts{n}.q"] = q.data
+                c[f"ts{n}.k"] = k.data
+            c[f"ts{n}.taps"] = g.materialized()
+            c[f"ts{n}.gs"] = dg
+            c[f"ts{n}.lb"] = lb
+            c[f"ts{n}.y"] = y.data
+            n += 1
+    c["n_ts"] = n
+    # mixed filter kinds through two-stage (regularized decay in the path)
+    g = random_mixed_groups(rng, 6, 2, 9)
+    v = random_seq(rng, 6, 77)
+    c["mixed.v"] = v.data
+    c["mixed.taps"] = g.materialized()
+    c["mixed.gs"] = 2
+    c["mixed.y"] = bc.two_stage_forward(v, g, 8).data
+    # block_conv (pkg/tests/test_blockconv.py:70-83 shapes)
+    n = 0
+    for d, dg, length, lh, lb in ((1, 1, 32, 4, 8), (4, 2, 100, 9, 16), (8, 4, 257, 40, 16),
+                                  (2, 1, 64, 64, 8), (4, 1, 600, 300, 128)):
+        g = random_explicit_groups(rng, d, dg, lh)
+        x = random_seq(rng, d, length)
+        c[f"bk{n}.x"] = x.data
+        c[f"bk{n}.taps"] = g.materialized()
+        c[f"bk{n}.gs"] = dg
+        c[f"bk{n}.lb"] = lb
+        c[f"bk{n}.y"] = bc.block_conv(x, g, lb).data
+        n += 1
+    c["n_bk"] = n
+    # chunk-parallel
+    taps = rng.standard_normal(9) / 3.0
+    x = random_seq(rng, 5, 70)
+    c["cp.x"] = x.data
+    c["cp.taps"] = taps
+    c["cp.y"] = bc.chunk_parallel_forward(x, taps, 8).data
+    c["flops"] = bc.two_stage_flops(1024, 64, 128)
+    save("blockconv", c)
+
+
+def gen_fft() -> None:
+    c = {}
+    rng = make_rng(520)
+    n = 0
+    for d, length, lh in ((1, 16, 16), (3, 100, 100), (2, 64, 10), (4, 257, 257), (2, 1024, 1024),
+                          (1, 5, 3)):
+        x = rng.standard_normal((d, length))
+        taps = rng.standard_normal((d, lh)) / np.sqrt(lh)
+        c[f"fc{n}.x"] = x
+        c[f"fc{n}.taps"] = taps
+        c[f"fc{n}.y"] = fftmod.fft_conv(x, taps)
+        n += 1
+    c["n_fc"] = n
+    z = rng.standard_normal(32) + 1j * rng.standard_normal(32)
+    c["fft.x"] = z
+    c["fft.y"] = fftmod.fft(z)
+    c["bitrev8"] = fftmod.bit_reversal_indices(8)
+    save("fft", c)
+
+
+def gen_filters() -> None:
+    c = {}
+    rng = make_rng(530)
+    th = rng.standard_normal(10)
+    c["reg.taps_hat"] = th
+    c["reg.rate"] = 0.7
+    c["reg.base"] = 2.0
+    c["reg.y"] = materialize_filter(RegularizedFilter(th, 0.7, 2.0))
+    res = rng.standard_normal(5)
+    poles = np.array([-1.0, -0.5, 0.0, 0.99, 1.0])
+    c["imp.residues"] = res
+    c["imp.poles"] = poles
+    c["imp.length"] = 300
+    c["imp.y"] = materialize_filter(ImplicitFilter(res, poles, 300))
+    save("filters", c)
+
+
+def gen_hyena() -> None:
+    c = {}
+    n = 0
+    specs = [
+        # (variant, width, L, group_size, inner_len, block_size, backend, dtype)
+        ("SE", 8, 64, 1, None, 16, "blocked", "f32"),
+        ("SE", 8, 96, 2, 9, 8, "direct", "f64"),
+        ("SE", 8, 96, 2, 9, 8, "fft", "f64"),
+        ("SE", 16, 200, 1, 14, 16, "blocked", "f32"),
+        ("MR", 8, 256, 1, 128, 128, "blocked", "f32"),
+        ("MR", 8, 300, 2, 128, 128, "blocked", "f64"),
+        ("MR", 4, 64, 1, 24, 8, "blocked", "f64"),  # spill > 1 -> block_conv route
+        ("MR", 8, 130, 1, 64, 16, "direct", "f32"),
+        ("LI", 8, 64, 1, None, 16, "fft", "f32"),
+        ("LI", 8, 256, 2, None, 16, "fft", "f64"),
+        ("LI", 4, 48, 1, None, 16, "direct", "f64"),
+    ]
+    for variant, width, length, gs, inner_len, lb, backend, dtype in specs:
+        rng = make_rng(600 + n)
+        cfg = hyena.make_hyena_config(variant, width, rng, seq_len=length, group_size=gs,
+                                      inner_len=inner_len, block_size=lb, backend=backend)
+        x = random_seq(make_rng(700 + n), width, length, dtype)
+        y = hyena.hyena_forward(x, cfg)
+        c.update(cfg_arrays(f"h{n}.cfg", cfg))
+        c[f"h{n}.seed"] = 600 + n
+        c[f"h{n}.x"] = x.data
+        c[f"h{n}.y"] = y.data
+        c[f"h{n}.args"] = np.array([variant, str(width), str(length), str(gs), str(inner_len), str(lb),
+                                    backend, dtype])
+        n += 1
+    c["n_h"] = n
+    # identity collapse (pkg/tests/test_hyena.py:21-25)
+    x = random_seq(make_rng(60), 3, 24)
+    c["ident.x"] = x.data
+    c["ident.y"] = hyena.hyena_forward(x, hyena.identity_config(width=3)).data
+    save("hyena", c)
+
+
+def gen_layout() -> None:
+    c = {}
+    width, length = 8, 64
+    rng = make_rng(800)
+    layers = (
+        hyena.make_hyena_config("SE", width, rng, seq_len=length, block_size=16),
+        hyena.make_hyena_config("MR", width, rng, seq_len=length, inner_len=32, block_size=32),
+        hyena.make_hyena_config("LI", width, rng, seq_len=length, backend="fft"),
+    )
+    spec = hyena.LayoutSpec(("SE", "MR", "LI"), 1, layers)
+    for residual in (False, True):
+        for dtype in ("f32", "f64"):
+            stack = hyena.build_layout(spec, residual=residual)
+            x = random_seq(make_rng(801), width, length, dtype)
+            c[f"{int(residual)}.{dtype}.x"] = x.data
+            c[f"{int(residual)}.{dtype}.y"] = hyena.layout_forward(x, stack).data
+    for i, cfg in enumerate(layers):
+        c.update(cfg_arrays(f"layer{i}", cfg))
+    c["n_layers"] = len(layers)
+    save("layout", c)
+
+
+def gen_cpsim() -> None:
+    c = {}
+    n = 0
+    for scheme, n_ranks, d, dg, length, lh, n_pipe, layout in (
+        ("p2p", 4, 8, 2, 256, 7, 1, "sequential"),
+        ("p2p_ov", 4, 8, 4, 128, 9, 1, "sequential"),
+        ("p2p", 2, 4, 1, 64, 1, 1, "sequential"),
+        ("a2a", 4, 16, 1, 256, 9, 1, "sequential"),
+        ("a2a", 4, 16, 1, 256, 9, 1, "zigzag"),
+        ("a2a_pipe", 4, 16, 1, 128, 7, 2, "sequential"),
+        ("a2a", 2, 8, 2, 64, 64, 1, "sequential"),
+    ):
+        rng = make_rng(900 + n)
+        groups = random_explicit_groups(rng, d, dg, lh)
+        x = random_seq(rng, d, length)
+        grp = cpsim.SimGroup(n_ranks)
+        xs = cpsim.shard(x, n_ranks, layout)
+        if scheme == "p2p":
+            ys = cpsim.p2p_conv(xs, groups, grp)
+            name = "p2p_conv"
+        elif scheme == "p2p_ov":
+            ys = cpsim.p2p_conv_overlapped(xs, groups, grp)
+            name = "p2p_conv_overlapped"
+        elif scheme == "a2a":
+            ys = cpsim.a2a_conv(xs, groups, grp)
+            name = "a2a_conv"
+        else:
+            ys = cpsim.a2a_conv_pipelined(xs, groups, grp, n_pipe)
+            name = "a2a_conv_pipelined"
+        c[f"cp{n}.args"] = np.array([scheme, str(n_ranks), str(d), str(dg), str(length), str(lh),
+                                     str(n_pipe), layout, name])
+        c[f"cp{n}.x"] = x.data
+        c[f"cp{n}.taps"] = groups.materialized()
+        c[f"cp{n}.y"] = cpsim.gather(ys).data
+        for r in range(n_ranks):
+            c[f"cp{n}.shard{r}"] = ys.shards[r]
+        c[f"cp{n}.elements"] = grp.total_elements(name)
+        c[f"cp{n}.messages"] = grp.total_messages(name)
+        c[f"cp{n}.rounds"] = grp.scheme_rounds.get(name, 0)
+        c[f"cp{n}.filter_elements"] = np.array([grp.filter_elements[r] for r in range(n_ranks)])
+        n += 1
+    c["n_cp"] = n
+    save("cpsim", c)
+
+
+def gen_builders() -> None:
+    """Raw make_hyena_config draws, to pin the product's seeded builders."""
+    c = {}
+    for i, (variant, kw) in enumerate((("SE", {}), ("MR", {"group_size": 2}),
+                                       ("LI", {"seq_len": 32, "n_poles": 4}))):
+        cfg = hyena.make_hyena_config(variant, 4, make_rng(1000 + i), **kw)
+        c.update(cfg_arrays(f"b{i}", cfg))
+    layout = hyena.make_layout(("SE", "MR"), 2, 4, make_rng(1010), seq_len=16)
+    for i, cfg in enumerate(layout.layers):
+        c.update(cfg_arrays(f"lay{i}", cfg))
+    save("builders", c)
+
+
+if __name__ == "__main__":
+    gen_direct()
+    gen_blockconv()
+    gen_fft()
+    gen_filters()
+    gen_hyena()
+    gen_layout()
+    gen_cpsim()
+    gen_builders()
