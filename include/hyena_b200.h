@@ -1,0 +1,114 @@
+/*
+ * hyena_b200.h — C-ABI of the B200-native StripedHyena 2 convolution hot path.
+ *
+ * Every entry point takes caller-owned DEVICE pointers (plain pointers and
+ * sizes, no torch types), enqueues work on the caller's cudaStream_t (passed
+ * as void*), never synchronises, never allocates, and returns an int status
+ * (HY_OK = 0). hy_last_error() returns a thread-local message for the last
+ * failure. Layout of every activation is (B, C, L) contiguous, time innermost:
+ * element (b, c, t) lives at ((b * C) + c) * L + t. This is the reference's
+ * (channels, length) SeqTensor layout (core.py:25-45) with a batch dimension.
+ *
+ * Filter taps are per GROUP: taps[g * lh + j] multiplies the input j steps in
+ * the past for every channel c with c / group_size == g (core.py:161-204).
+ * Taps are fp32 for HY_F32 / HY_BF16 activations and fp64 for HY_F64.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/convhybrid/):
+ *   hy_causal_conv_fwd      core.py:212-226      direct_causal_conv (any filter length)
+ *                           hyena.py:122-126     the featurizer conv inside _featurize
+ *                           blockconv.py:103-121 block_conv (same numbers, K spill factors)
+ *   hy_gated_conv_fwd       blockconv.py:182-220 two_stage_forward(v, groups, lb, q, k) for
+ *                                                fp32/fp64 (CUDA-core FIR, any filter length)
+ *   hy_two_stage_fwd        blockconv.py:160-220 two_stage_forward / _two_stage_core on tcgen05
+ *                           blockconv.py:267-293 chunk_parallel_forward (shared taps, gs = C)
+ *                           core.py:144-146      RegularizedFilter decay, fused in-kernel
+ *   hy_hyena_mixer_fwd      hyena.py:162-186     _featurize(q,k,v) conv + inner conv + gates,
+ *                                                fused (the projections stay cuBLAS GEMMs)
+ *   hy_fft_conv_fwd         fft.py:128-145       fft_conv, fused with the k*v / q gates as used
+ *                           hyena.py:183-186     by the LI operator (backend="fft")
+ *   hy_halo_correction_fwd  cpsim.py:498-510     p2p_conv_overlapped's correction conv
+ */
+#ifndef HYENA_B200_H
+#define HYENA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HY_API __attribute__((visibility("default")))
+#else
+#define HY_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hy_status {
+  HY_OK = 0,
+  HY_ERR_INVALID = 1,     /* bad shape / argument: the Python layer raises ValueError */
+  HY_ERR_INELIGIBLE = 2,  /* filter needs > 1 spill factor: TwoStageIneligibleError */
+  HY_ERR_UNSUPPORTED = 3, /* dtype / size not handled by this kernel */
+  HY_ERR_CUDA = 4         /* launch / runtime failure */
+};
+
+enum hy_dtype { HY_F32 = 0, HY_BF16 = 1, HY_F64 = 2 };
+
+/* ABI version (major * 100 + minor) and last-error text (thread-local). */
+HY_API int hy_version(void);
+HY_API const char* hy_last_error(void);
+
+/* Causal FIR, any filter length:
+ *   y[b,c,t] = sum_{j < lh, j <= t} taps[c/gs, j] * x[b,c,t-j]
+ * CUDA cores, 128-bit coalesced loads, fp32 accumulation (fp64 for HY_F64). */
+HY_API int hy_causal_conv_fwd(const void* x, void* y, const void* taps,
+                       int B, int C, int L, int lh, int group_size, int dtype, void* stream);
+
+/* Gated FIR: y = q * conv(k * v); q and/or k may be NULL (gate omitted). */
+HY_API int hy_gated_conv_fwd(const void* q, const void* k, const void* v, void* y, const void* taps,
+                      int B, int C, int L, int lh, int group_size, int dtype, void* stream);
+
+/* Two-stage blocked conv on tcgen05 (bf16 operands, fp32 TMEM accumulation):
+ *   u = k * v;  Y_n = T0 U_n + T1 U_{n-1} (128-step chunks);  y = q * Y
+ * taps_hat: fp32 (n_groups, lh); decay: fp32 (n_groups) holding rate*log2(base),
+ * or NULL for explicit taps, giving h[t] = taps_hat[t] * exp2(-decay * t).
+ * Requires dtype == HY_BF16, lh <= 129, L % 8 == 0, 16-byte aligned pointers. */
+HY_API int hy_two_stage_fwd(const void* q, const void* k, const void* v, void* y,
+                     const float* taps_hat, const float* decay,
+                     int B, int C, int L, int lh, int group_size, int dtype, void* stream);
+
+/* Fused Hyena mixer (everything between the projections):
+ *   proj: (B, 3C, L) = [W_q^T x ; W_k^T x ; W_v^T x] per batch element
+ *   q,k,v = featurizer FIRs (feat_taps: (3, C, lhf) per CHANNEL, zero padded)
+ *   y = q * inner(k * v)     (inner taps per group, optional decay as above)
+ * SE (lh <= 14): CUDA-core kernel, fp32 or bf16. MR (bf16, lh <= 129): tcgen05.
+ * HY_F64 and longer filters return HY_ERR_UNSUPPORTED (the host composes kernels). */
+HY_API int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,
+                       const void* inner_taps, const float* inner_decay, int lh, int group_size,
+                       int B, int C, int L, int dtype, void* stream);
+
+/* SE mixer only (CUDA cores, fp32 / bf16, lh and lhf <= 16), same arguments. */
+HY_API int hy_se_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,
+                           const void* inner_taps, const float* inner_decay, int lh, int group_size,
+                           int B, int C, int L, int dtype, void* stream);
+
+/* FFT causal conv fused with gates: y = q * (h conv (k * v)) truncated to L,
+ * h given as per-group taps (n_groups, lh) with lh <= L; q/k may be NULL.
+ * fp32 complex FFT of size next_pow2(L + lh - 1). ws: device workspace of
+ * hy_fft_conv_workspace_size() bytes. */
+HY_API size_t hy_fft_conv_workspace_size(int B, int C, int L, int lh, int group_size, int dtype);
+HY_API int hy_fft_conv_fwd(const void* q, const void* k, const void* v, void* y, const void* taps,
+                    int B, int C, int L, int lh, int group_size, int dtype,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* Overlapped-p2p correction: y[:, t] += sum_{j > t} taps[j] * halo[:, H + t - j]
+ * for t < H = lh - 1, where halo (B, C, H) holds the predecessor's last H steps. */
+HY_API int hy_halo_correction_fwd(const void* halo, void* y, const void* taps,
+                           int B, int C, int L, int lh, int group_size, int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HYENA_B200_H */

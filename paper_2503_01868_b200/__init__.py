@@ -1,0 +1,53 @@
+"""B200-native StripedHyena 2 convolution operators (arXiv 2503.01868), drop-in for the
+reference `convhybrid` operator API (Hyena-SE / MR / LI forward, multi-hybrid layouts,
+context-parallel conv schemes). Compute runs in hand-written sm_100a kernels behind the
+C-ABI of include/hyena_b200.h; there is no CPU fallback.
+"""
+
+from . import fft
+from .blockconv import (
+    MultiplyCounter,
+    ToeplitzFactors,
+    TwoStageIneligibleError,
+    assemble_toeplitz,
+    block_conv,
+    build_factors,
+    chunk_parallel_forward,
+    spill_count,
+    two_stage_flops,
+    two_stage_forward,
+    two_stage_forward_saved,
+)
+from .core import (
+    ExplicitFilter,
+    GroupSpec,
+    ImplicitFilter,
+    RegularizedFilter,
+    SeqTensor,
+    direct_causal_conv,
+    filter_length,
+    full_toeplitz,
+    materialize_filter,
+    uniform_groups,
+)
+from .fft import fft_conv, next_pow2
+from .hyena import (
+    HyenaConfig,
+    HyenaOperator,
+    LayoutSpec,
+    OperatorStack,
+    build_layout,
+    hyena_forward,
+    hyena_forward_saved,
+    identity_config,
+    layout_forward,
+    layout_forward_device,
+    layout_forward_saved,
+    make_hyena_config,
+    make_inner_bank,
+    make_layout,
+    update_param,
+)
+from .rand import make_rng
+
+__version__ = "0.1.0"

@@ -1,0 +1,475 @@
+"""Gated convolution operators (Hyena-SE / MR / LI) and multi-hybrid stacks on B200.
+
+Mirrors /root/reference/pkg/src/convhybrid/hyena.py: HyenaConfig, hyena_forward,
+LayoutSpec / OperatorStack / build_layout / layout_forward and the seeded
+builders keep their names, arguments, validation and errors. The forward runs
+on the device:
+
+    proj  = W_qkv^T x                 cuBLAS GEMM, (B, 3D, L)    (hyena.py:124 x3, fused)
+    mixed = q * inner(k * v)          one fused sm_100a kernel    (hyena.py:125, 170-186)
+    y     = W_out^T mixed             cuBLAS GEMM                 (hyena.py:188)
+
+`HyenaOperator` is the torch-native entry ((B, D, L) device tensors, parameters
+packed once on the device); `hyena_forward` stages a SeqTensor through it.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+from typing import Union
+
+import numpy as np
+import torch
+
+from . import ops
+from .blockconv import spill_count
+from .core import (
+    ExplicitFilter,
+    GroupSpec,
+    ImplicitFilter,
+    RegularizedFilter,
+    SeqTensor,
+    device,
+    from_device,
+    to_device,
+)
+
+VARIANTS = ("SE", "MR", "LI")
+BACKENDS = ("direct", "blocked", "fft")
+MAX_SHORT_FILTER = 14
+
+Projection = Union[np.ndarray, tuple]
+
+
+def _as_projection(p, width: int, name: str) -> Projection:
+    if isinstance(p, tuple):
+        if len(p) != 2:
+            raise ValueError(f"factored projection {name} must be a (left, right) pair")
+        left = np.asarray(p[0], dtype=np.float64)
+        right = np.asarray(p[1], dtype=np.float64)
+        if left.ndim != 2 or right.ndim != 2 or left.shape[0] != width or right.shape[1] != width \
+                or left.shape[1] != right.shape[0]:
+            raise ValueError(f"factored projection {name} needs shapes (d, r), (r, d) with d={width}")
+        return (left, right)
+    arr = np.asarray(p, dtype=np.float64)
+    if arr.shape != (width, width):
+        raise ValueError(f"projection {name} must be ({width}, {width}), got {arr.shape}")
+    return arr
+
+
+def projection_dense(p: Projection) -> np.ndarray:
+    """(hyena.py:64-65); factored projections are densified once at packing time."""
+    return p[0] @ p[1] if isinstance(p, tuple) else p
+
+
+def _check_feat(groups: GroupSpec, width: int, name: str) -> None:
+    if groups.channels != width:
+        raise ValueError(f"{name} covers {groups.channels} channels, operator width is {width}")
+    for f in groups.filters:
+        if not isinstance(f, ExplicitFilter):
+            raise ValueError(f"{name} filters must be explicit short taps")
+    if groups.filter_len > MAX_SHORT_FILTER:
+        raise ValueError(f"{name} filter length {groups.filter_len} exceeds short-filter cap {MAX_SHORT_FILTER}")
+
+
+_INNER_KIND = {"SE": ExplicitFilter, "MR": RegularizedFilter, "LI": ImplicitFilter}
+
+
+@dataclass(frozen=True, eq=False)
+class HyenaConfig:
+    """One operator instance (hyena.py:81-119)."""
+
+    variant: str
+    width: int
+    w_q: Projection
+    w_k: Projection
+    w_v: Projection
+    w_out: Projection
+    q_feat: GroupSpec
+    k_feat: GroupSpec
+    v_feat: GroupSpec
+    inner: GroupSpec
+    block_size: int = 16
+    backend: str = "blocked"
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}, got {self.variant!r}")
+        if self.backend not in BACKENDS:
+            raise ValueError(f"backend must be one of {BACKENDS}, got {self.backend!r}")
+        if self.width < 1:
+            raise ValueError("width must be >= 1")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        for name in ("w_q", "w_k", "w_v", "w_out"):
+            object.__setattr__(self, name, _as_projection(getattr(self, name), self.width, name))
+        for name in ("q_feat", "k_feat", "v_feat"):
+            _check_feat(getattr(self, name), self.width, name)
+        if self.inner.channels != self.width:
+            raise ValueError(f"inner filters cover {self.inner.channels} channels, width is {self.width}")
+        kind = _INNER_KIND[self.variant]
+        for f in self.inner.filters:
+            if not isinstance(f, kind):
+                raise ValueError(f"variant {self.variant} requires {kind.__name__} inner filters, "
+                                 f"got {type(f).__name__}")
+        if self.variant == "SE" and self.inner.filter_len > MAX_SHORT_FILTER:
+            raise ValueError(f"SE inner filter length {self.inner.filter_len} exceeds {MAX_SHORT_FILTER}")
+
+
+# ---------------------------------------------------------------- device operator
+
+
+def _implicit_taps_device(inner: GroupSpec, dev, dtype) -> torch.Tensor:
+    """h_t = sum_n R_n lambda_n^t (core.py:147-151) evaluated on the device in fp64."""
+    res = torch.from_numpy(np.stack([f.residues for f in inner.filters])).to(dev)
+    poles = torch.from_numpy(np.stack([f.poles for f in inner.filters])).to(dev)
+    L = inner.filter_len
+    out = torch.empty((inner.n_groups, L), dtype=torch.float64, device=dev)
+    step = 8192
+    for s in range(0, L, step):
+        t = torch.arange(s, min(L, s + step), dtype=torch.float64, device=dev)
+        # poles**t with 0**0 = 1, as numpy
+        pw = torch.pow(poles[:, None, :], t[None, :, None])
+        out[:, s:s + t.numel()] = (pw * res[:, None, :]).sum(-1)
+    return out.to(dtype)
+
+
+class HyenaOperator:
+    """Device-resident parameters of one HyenaConfig and the torch-native forward.
+
+    forward(x) takes a contiguous CUDA tensor (B, D, L) (or (D, L)) of the
+    operator's dtype (float32, bfloat16 or float64) and returns y of the same
+    shape: two cuBLAS GEMMs around one fused mixer kernel.
+    """
+
+    def __init__(self, cfg: HyenaConfig, dtype: torch.dtype = torch.bfloat16, dev=None):
+        self.cfg = cfg
+        self.dtype = dtype
+        self.dev = dev or device()
+        D = cfg.width
+        w = [projection_dense(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v")]
+        self.w_qkv_t = torch.from_numpy(np.concatenate([m.T for m in w], axis=0)).to(self.dev, dtype).contiguous()
+        self.w_out_t = torch.from_numpy(np.ascontiguousarray(projection_dense(cfg.w_out).T)).to(self.dev, dtype)
+        tdt = ops.tap_dtype(dtype)
+        self.lhf = max(cfg.q_feat.filter_len, cfg.k_feat.filter_len, cfg.v_feat.filter_len)
+        feat = np.zeros((3, D, self.lhf))
+        for i, bank in enumerate((cfg.q_feat, cfg.k_feat, cfg.v_feat)):
+            feat[i, :, :bank.filter_len] = bank.taps_per_channel()
+        self.feat_taps = torch.from_numpy(feat).to(self.dev, tdt).contiguous()
+        inner = cfg.inner
+        self.gs = inner.group_size
+        self.lh = inner.filter_len
+        self.decay = None
+        if isinstance(inner.filters[0], ImplicitFilter):
+            self.inner_taps = _implicit_taps_device(inner, self.dev, tdt)
+        elif isinstance(inner.filters[0], RegularizedFilter) and dtype != torch.float64:
+            # taps_hat + per-group rate*log2(base): the decay is applied inside the kernels
+            self.inner_taps = torch.from_numpy(np.stack([f.taps_hat for f in inner.filters])).to(self.dev, tdt)
+            self.decay = torch.tensor([f.decay_rate * np.log2(f.base) for f in inner.filters],
+                                      dtype=torch.float32, device=self.dev)
+        else:
+            self.inner_taps = torch.from_numpy(inner.materialized()).to(self.dev, tdt)
+        self._mat_taps = None
+
+    @property
+    def materialized_inner(self) -> torch.Tensor:
+        if self.decay is None:
+            return self.inner_taps
+        if self._mat_taps is None:
+            t = torch.arange(self.lh, device=self.dev, dtype=torch.float32)
+            self._mat_taps = (self.inner_taps * torch.exp2(-self.decay[:, None] * t[None, :])).contiguous()
+        return self._mat_taps
+
+    def mixer(self, proj: torch.Tensor) -> torch.Tensor:
+        """q * inner(k * v) from the (B, 3D, L) projections."""
+        D = self.cfg.width
+        fused_ok = (self.dtype == torch.bfloat16 and self.lh <= 129) or \
+                   (self.dtype in (torch.float32, torch.bfloat16) and self.lh <= 16)
+        if fused_ok:
+            return ops.hyena_mixer(proj, self.feat_taps, self.inner_taps, self.gs, decay=self.decay)
+        # unfused: featurizers over all 3D rows in one launch, then the gated inner conv
+        B, _, L = proj.shape
+        feats = ops.causal_conv(proj, self.feat_taps.reshape(3 * D, self.lhf), 1)
+        q, k, v = (feats[:, i * D:(i + 1) * D].contiguous() for i in range(3))
+        if self.lh > 129 or self.cfg.variant == "LI":
+            return ops.long_conv(v, self.materialized_inner, self.gs, q=q, k=k)
+        return ops.gated_conv(v, self.materialized_inner, self.gs, q=q, k=k)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        squeeze = x.dim() == 2
+        x3 = x.unsqueeze(0) if squeeze else x
+        if x3.shape[1] != self.cfg.width:
+            raise ValueError(f"input has {x3.shape[1]} channels, operator width is {self.cfg.width}")
+        if self.cfg.variant == "LI" and self.lh != x3.shape[2]:
+            raise ValueError(
+                f"LI inner filter length {self.lh} must equal the sequence length {x3.shape[2]}")
+        if x3.dtype != self.dtype:
+            raise ValueError(f"operator packed for {self.dtype}, got {x3.dtype}")
+        proj = torch.matmul(self.w_qkv_t, x3)
+        mixed = self.mixer(proj)
+        y = torch.matmul(self.w_out_t, mixed)
+        return y[0] if squeeze else y
+
+    __call__ = forward
+
+
+_OPS: dict = {}
+
+
+def operator_for(cfg: HyenaConfig, dtype: torch.dtype) -> HyenaOperator:
+    """Cached device packing of a config (evicted when the config is garbage collected)."""
+    key = (id(cfg), dtype)
+    hit = _OPS.get(key)
+    if hit is not None and hit[0]() is cfg:
+        return hit[1]
+    op = HyenaOperator(cfg, dtype)
+    _OPS[key] = (weakref.ref(cfg, lambda _r, k=key: _OPS.pop(k, None)), op)
+    return op
+
+
+def _fp32_exact():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+
+
+def hyena_forward(x: SeqTensor, cfg: HyenaConfig) -> SeqTensor:
+    """Eq. 1, y = W_out^T (q * conv_inner(k * v)) (hyena.py:157-190), on the GPU."""
+    _check_input(x, cfg)
+    _fp32_exact()
+    xd = to_device(x)
+    y = operator_for(cfg, xd.dtype).forward(xd)
+    return from_device(y, x.dtype)
+
+
+def _check_input(x: SeqTensor, cfg: HyenaConfig) -> None:
+    if x.channels != cfg.width:
+        raise ValueError(f"input has {x.channels} channels, operator width is {cfg.width}")
+    if cfg.variant == "LI" and cfg.inner.filter_len != x.length:
+        raise ValueError(
+            f"LI inner filter length {cfg.inner.filter_len} must equal the sequence length {x.length}")
+
+
+@dataclass
+class HyenaSaved:
+    """Forward intermediates (hyena.py:138-154), host copies."""
+
+    cfg: HyenaConfig
+    x: np.ndarray
+    proj_q: np.ndarray
+    proj_k: np.ndarray
+    proj_v: np.ndarray
+    q: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+    gated: np.ndarray
+    conv_out: np.ndarray
+    mixed: np.ndarray
+    ts_saved: object
+    dtype: str
+
+
+def hyena_forward_saved(x: SeqTensor, cfg: HyenaConfig):
+    """Forward half of hyena.py:162-190 returning (y, HyenaSaved) with the intermediates."""
+    _check_input(x, cfg)
+    _fp32_exact()
+    xd = to_device(x)
+    op = operator_for(cfg, xd.dtype)
+    D = cfg.width
+    proj = torch.matmul(op.w_qkv_t, xd)
+    feats = ops.causal_conv(proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
+    q, k, v = (feats[i * D:(i + 1) * D].contiguous() for i in range(3))
+    gated = k * v
+    conv_out = ops.long_conv(gated, op.materialized_inner, op.gs) if op.lh > 129 else \
+        ops.gated_conv(gated, op.materialized_inner, op.gs)
+    mixed = q * conv_out
+    y = torch.matmul(op.w_out_t, mixed)
+    h = lambda t: t.detach().cpu().numpy().astype(np.float64)  # noqa: E731
+    saved = HyenaSaved(cfg, h(xd), h(proj[:D]), h(proj[D:2 * D]), h(proj[2 * D:]), h(q), h(k), h(v), h(gated),
+                       h(conv_out), h(mixed), None, x.dtype)
+    return from_device(y, x.dtype), saved
+
+
+# ---------------------------------------------------------------- layouts (hyena.py:350-417)
+
+
+@dataclass(frozen=True, eq=False)
+class LayoutSpec:
+    """Variant pattern repeated `depth` times with one config per layer."""
+
+    pattern: tuple
+    depth: int
+    layers: tuple
+
+    def __post_init__(self):
+        pattern = tuple(self.pattern)
+        layers = tuple(self.layers)
+        if not pattern:
+            raise ValueError("pattern must be nonempty")
+        for v in pattern:
+            if v not in VARIANTS:
+                raise ValueError(f"unknown variant {v!r} in pattern")
+        if self.depth < 1:
+            raise ValueError("depth must be >= 1")
+        if len(layers) != len(pattern) * self.depth:
+            raise ValueError(f"need {len(pattern) * self.depth} layer configs "
+                             f"(pattern {len(pattern)} x depth {self.depth}), got {len(layers)}")
+        for i, cfg in enumerate(layers):
+            want = pattern[i % len(pattern)]
+            if cfg.variant != want:
+                raise ValueError(f"layer {i} has variant {cfg.variant}, pattern expects {want}")
+        object.__setattr__(self, "pattern", pattern)
+        object.__setattr__(self, "layers", layers)
+
+
+@dataclass(frozen=True, eq=False)
+class OperatorStack:
+    layers: tuple
+    residual: bool = False
+
+
+def build_layout(spec: LayoutSpec, residual: bool = False) -> OperatorStack:
+    widths = {cfg.width for cfg in spec.layers}
+    if len(widths) != 1:
+        raise ValueError(f"layer widths differ: {sorted(widths)}")
+    return OperatorStack(tuple(spec.layers), residual=residual)
+
+
+def layout_forward_device(x: torch.Tensor, stack: OperatorStack) -> torch.Tensor:
+    """Torch-native stack forward: activations stay on the device between layers."""
+    cur = x
+    for cfg in stack.layers:
+        out = operator_for(cfg, x.dtype).forward(cur)
+        cur = cur + out if stack.residual else out
+    return cur
+
+
+def layout_forward(x: SeqTensor, stack: OperatorStack) -> SeqTensor:
+    """Sequential composition with optional residual (hyena.py:394-406)."""
+    for cfg in stack.layers:
+        _check_input(x, cfg)
+    _fp32_exact()
+    return from_device(layout_forward_device(to_device(x), stack), x.dtype)
+
+
+def layout_forward_saved(x: SeqTensor, stack: OperatorStack):
+    saveds = []
+    cur = x
+    for cfg in stack.layers:
+        out, saved = hyena_forward_saved(cur, cfg)
+        saveds.append(saved)
+        cur = SeqTensor(cur.data + out.data, dtype=x.dtype) if stack.residual else out
+    return cur, saveds
+
+
+# ---------------------------------------------------------------- seeded builders (hyena.py:423-533)
+
+DEFAULT_FEATURIZER_LEN = 7
+DEFAULT_SE_LEN = 7
+DEFAULT_MR_LEN = 128
+DEFAULT_LI_POLES = 8
+DECAY_SWEEP = (0.01, 2.0)
+
+
+def _rand_taps(rng: np.random.Generator, lh: int) -> np.ndarray:
+    return rng.standard_normal(lh) / np.sqrt(lh)
+
+
+def _explicit_bank(rng, width: int, group_size: int, lh: int) -> GroupSpec:
+    n = width // group_size
+    return GroupSpec(width, group_size, tuple(ExplicitFilter(_rand_taps(rng, lh)) for _ in range(n)))
+
+
+def make_inner_bank(variant: str, width: int, group_size: int, rng: np.random.Generator,
+                    filter_len: int | None = None, seq_len: int | None = None,
+                    n_poles: int = DEFAULT_LI_POLES, decay_base: float = 2.0) -> GroupSpec:
+    """Inner bank with the reference's draw order and MR decay sweep (hyena.py:439-469)."""
+    n = width // group_size
+    if variant == "SE":
+        return _explicit_bank(rng, width, group_size, DEFAULT_SE_LEN if filter_len is None else filter_len)
+    if variant == "MR":
+        lh = DEFAULT_MR_LEN if filter_len is None else filter_len
+        rates = np.linspace(DECAY_SWEEP[0], DECAY_SWEEP[1], n)
+        return GroupSpec(width, group_size, tuple(
+            RegularizedFilter(_rand_taps(rng, lh), float(rates[g]), decay_base) for g in range(n)))
+    if variant == "LI":
+        if seq_len is None:
+            raise ValueError("LI inner filters need the sequence length")
+        filters = []
+        for _ in range(n):
+            poles = rng.uniform(-0.95, 0.95, size=n_poles)
+            residues = rng.standard_normal(n_poles) / n_poles
+            filters.append(ImplicitFilter(residues, poles, seq_len))
+        return GroupSpec(width, group_size, tuple(filters))
+    raise ValueError(f"variant must be one of {VARIANTS}, got {variant!r}")
+
+
+def make_hyena_config(variant: str, width: int, rng: np.random.Generator, seq_len: int | None = None,
+                      group_size: int = 1, featurizer_len: int = DEFAULT_FEATURIZER_LEN,
+                      inner_len: int | None = None, block_size: int = 16, backend: str = "blocked",
+                      n_poles: int = DEFAULT_LI_POLES) -> HyenaConfig:
+    """Seeded config with the reference's exact draw order (hyena.py:472-497)."""
+    scale = 1.0 / np.sqrt(width)
+    projs = [rng.standard_normal((width, width)) * scale for _ in range(4)]
+    return HyenaConfig(
+        variant=variant, width=width,
+        w_q=projs[0], w_k=projs[1], w_v=projs[2], w_out=projs[3],
+        q_feat=_explicit_bank(rng, width, group_size, featurizer_len),
+        k_feat=_explicit_bank(rng, width, group_size, featurizer_len),
+        v_feat=_explicit_bank(rng, width, group_size, featurizer_len),
+        inner=make_inner_bank(variant, width, group_size, rng, filter_len=inner_len, seq_len=seq_len,
+                              n_poles=n_poles),
+        block_size=block_size, backend=backend)
+
+
+def make_layout(pattern, depth: int, width: int, rng: np.random.Generator, seq_len: int | None = None,
+                **cfg_kw) -> LayoutSpec:
+    """(hyena.py:500-513)."""
+    pattern = tuple(pattern)
+    layers = tuple(make_hyena_config(pattern[i % len(pattern)], width, rng, seq_len=seq_len, **cfg_kw)
+                   for i in range(len(pattern) * depth))
+    return LayoutSpec(pattern, depth, layers)
+
+
+def identity_config(variant: str = "SE", width: int = 1, inner: GroupSpec | None = None,
+                    backend: str = "direct", block_size: int = 16) -> HyenaConfig:
+    """Identity projections and unit featurizers (hyena.py:516-533)."""
+    eye = np.eye(width)
+    unit = GroupSpec(width, width, (ExplicitFilter(np.array([1.0])),))
+    return HyenaConfig(variant=variant, width=width, w_q=eye, w_k=eye.copy(), w_v=eye.copy(),
+                       w_out=eye.copy(), q_feat=unit, k_feat=unit, v_feat=unit,
+                       inner=unit if inner is None else inner, block_size=block_size, backend=backend)
+
+
+def update_param(cfg: HyenaConfig, path: tuple, value: np.ndarray) -> HyenaConfig:
+    """Functional single-leaf update (hyena.py:331-344); returns a new config."""
+    from dataclasses import replace
+    if path[0].startswith("w_"):
+        proj = getattr(cfg, path[0])
+        if len(path) == 2:
+            proj = (value, proj[1]) if path[1] == "left" else (proj[0], value)
+        else:
+            proj = value
+        return replace(cfg, **{path[0]: proj})
+    role, idx, leaf = path
+    groups: GroupSpec = getattr(cfg, role)
+    filters = list(groups.filters)
+    f = filters[idx]
+    if isinstance(f, ExplicitFilter):
+        filters[idx] = ExplicitFilter(value)
+    elif isinstance(f, RegularizedFilter):
+        filters[idx] = RegularizedFilter(value, f.decay_rate, f.base)
+    elif leaf == "residues":
+        filters[idx] = ImplicitFilter(value, f.poles, f.length)
+    else:
+        filters[idx] = ImplicitFilter(f.residues, value, f.length)
+    return replace(cfg, **{role: GroupSpec(groups.channels, groups.group_size, tuple(filters))})
+
+
+__all__ = [
+    "VARIANTS", "BACKENDS", "MAX_SHORT_FILTER", "HyenaConfig", "HyenaOperator", "HyenaSaved",
+    "LayoutSpec", "OperatorStack", "build_layout", "hyena_forward", "hyena_forward_saved",
+    "identity_config", "layout_forward", "layout_forward_device", "layout_forward_saved",
+    "make_hyena_config", "make_inner_bank", "make_layout", "operator_for", "projection_dense",
+    "spill_count", "update_param",
+]

@@ -1,0 +1,183 @@
+"""Torch-native device entry points over the C-ABI (no host copies, no fallback).
+
+Every function takes CUDA tensors in the (B, C, L) layout (a 2-D (C, L) tensor
+is treated as B = 1), launches one of the sm_100a kernels on the current torch
+stream and returns a new CUDA tensor. Filter taps are per group, (G, lh),
+float32 for fp32/bf16 activations and float64 for fp64 ones.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.HY_F32, torch.bfloat16: _lib.HY_BF16, torch.float64: _lib.HY_F64}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _as3(x: torch.Tensor) -> torch.Tensor:
+    if x.dim() == 2:
+        return x.unsqueeze(0)
+    if x.dim() != 3:
+        raise ValueError(f"expected (B, C, L) or (C, L), got shape {tuple(x.shape)}")
+    return x
+
+
+def _check_device(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("paper_2503_01868_b200 ops need CUDA tensors (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+
+
+def _dtype_code(x: torch.Tensor) -> int:
+    try:
+        return _DT[x.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {x.dtype}; use float32, bfloat16 or float64") from None
+
+
+def tap_dtype(act_dtype: torch.dtype) -> torch.dtype:
+    return torch.float64 if act_dtype == torch.float64 else torch.float32
+
+
+def _taps(taps: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    want = tap_dtype(x.dtype)
+    if taps.dtype != want or not taps.is_contiguous() or taps.device != x.device:
+        taps = taps.to(device=x.device, dtype=want).contiguous()
+    return taps
+
+
+def causal_conv(x: torch.Tensor, taps: torch.Tensor, group_size: int = 1) -> torch.Tensor:
+    """y = h conv x per channel (core.py:212-226), any filter length. x: (B,C,L) or (C,L)."""
+    squeeze = x.dim() == 2
+    x3 = _as3(x)
+    _check_device(x3)
+    taps = _taps(taps, x3)
+    B, C, L = x3.shape
+    lh = taps.shape[-1]
+    y = torch.empty_like(x3)
+    lib = _lib.load()
+    _lib.check(lib.hy_causal_conv_fwd(x3.data_ptr(), y.data_ptr(), taps.data_ptr(), B, C, L, lh,
+                                      group_size, _dtype_code(x3), _stream()), "causal_conv")
+    return y[0] if squeeze else y
+
+
+def gated_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None) -> torch.Tensor:
+    """y = q * conv(k * v) on CUDA cores (blockconv.py:182-220 semantics, any lh)."""
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    for name, g in (("q", q3), ("k", k3)):
+        if g is not None and (g.shape != v3.shape or g.dtype != v3.dtype):
+            raise ValueError(f"gate {name} shape/dtype {tuple(g.shape)}/{g.dtype} does not match input "
+                             f"{tuple(v3.shape)}/{v3.dtype}")
+    taps = _taps(taps, v3)
+    B, C, L = v3.shape
+    y = torch.empty_like(v3)
+    lib = _lib.load()
+    _lib.check(lib.hy_gated_conv_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), taps.data_ptr(), B, C,
+                                     L, taps.shape[-1], group_size, _dtype_code(v3), _stream()),
+               "gated_conv")
+    return y[0] if squeeze else y
+
+
+def two_stage(v: torch.Tensor, taps_hat: torch.Tensor, group_size: int = 1, q=None, k=None,
+              decay=None) -> torch.Tensor:
+    """tcgen05 two-stage conv, bf16 (blockconv.py:160-220): y = q * (T0 U_n + T1 U_{n-1}).
+
+    taps_hat: (G, lh) fp32 with lh <= 129; decay: (G,) fp32 = rate*log2(base) or None.
+    """
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    if v3.dtype != torch.bfloat16:
+        raise ValueError("two_stage (tcgen05) takes bfloat16 activations; use gated_conv for fp32/fp64")
+    for name, g in (("q", q3), ("k", k3)):
+        if g is not None and (g.shape != v3.shape or g.dtype != v3.dtype):
+            raise ValueError(f"gate {name} shape {tuple(g.shape)} does not match input {tuple(v3.shape)}")
+    taps_hat = taps_hat.to(device=v3.device, dtype=torch.float32).contiguous()
+    if decay is not None:
+        decay = decay.to(device=v3.device, dtype=torch.float32).contiguous()
+    B, C, L = v3.shape
+    y = torch.empty_like(v3)
+    lib = _lib.load()
+    _lib.check(lib.hy_two_stage_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), taps_hat.data_ptr(),
+                                    _ptr(decay), B, C, L, taps_hat.shape[-1], group_size, _lib.HY_BF16,
+                                    _stream()), "two_stage")
+    return y[0] if squeeze else y
+
+
+def hyena_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, inner_taps: torch.Tensor, group_size: int,
+                decay=None, out=None, se_only: bool = False) -> torch.Tensor:
+    """Fused featurizers + gates + inner conv (hyena.py:162-186) from the (B, 3C, L) projections.
+
+    feat_taps: (3, C, lhf) per-channel [q, k, v] featurizer taps (fp32);
+    inner_taps: (G, lh) fp32; decay: (G,) fp32 or None.
+    """
+    _check_device(proj)
+    B, C3, L = proj.shape
+    if C3 % 3 != 0:
+        raise ValueError("proj must be (B, 3C, L)")
+    C = C3 // 3
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    it = inner_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    if decay is not None:
+        decay = decay.to(device=proj.device, dtype=torch.float32).contiguous()
+    if ft.shape[:2] != (3, C):
+        raise ValueError(f"feat_taps must be (3, {C}, lhf), got {tuple(ft.shape)}")
+    y = out if out is not None else torch.empty((B, C, L), device=proj.device, dtype=proj.dtype)
+    lib = _lib.load()
+    fn = lib.hy_se_mixer_fwd if se_only else lib.hy_hyena_mixer_fwd
+    _lib.check(fn(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), ft.shape[-1], it.data_ptr(), _ptr(decay),
+                  it.shape[-1], group_size, B, C, L, _dtype_code(proj), _stream()), "hyena_mixer")
+    return y
+
+
+def halo_correction(halo: torch.Tensor, y: torch.Tensor, taps: torch.Tensor, group_size: int = 1) -> None:
+    """In place: y[..., t] += sum_{j>t} h[j] halo[..., H+t-j] for t < H (cpsim.py:498-510)."""
+    h3, y3 = _as3(halo), _as3(y)
+    _check_device(h3, y3)
+    taps = _taps(taps, y3)
+    B, C, L = y3.shape
+    lib = _lib.load()
+    _lib.check(lib.hy_halo_correction_fwd(h3.data_ptr(), y3.data_ptr(), taps.data_ptr(), B, C, L,
+                                          taps.shape[-1], group_size, _dtype_code(y3), _stream()),
+               "halo_correction")
+
+
+def fft_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None) -> torch.Tensor:
+    """y = q * (h conv (k * v)) through the FFT kernel (fft.py:128-145, hyena.py:183-186)."""
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    taps = _taps(taps, v3)
+    B, C, L = v3.shape
+    lh = taps.shape[-1]
+    lib = _lib.load()
+    code = _dtype_code(v3)
+    ws_bytes = lib.hy_fft_conv_workspace_size(B, C, L, lh, group_size, code)
+    ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=v3.device)
+    y = torch.empty_like(v3)
+    _lib.check(lib.hy_fft_conv_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), taps.data_ptr(), B, C, L,
+                                   lh, group_size, code, ws.data_ptr(), int(ws_bytes), _stream()), "fft_conv")
+    return y[0] if squeeze else y
+
+
+def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None) -> torch.Tensor:
+    """Gated causal conv for long filters: the FFT kernel where it covers the case, else the FIR kernel."""
+    try:
+        return fft_conv(v, taps, group_size, q=q, k=k)
+    except NotImplementedError:
+        return gated_conv(v, taps, group_size, q=q, k=k)

@@ -1,0 +1,115 @@
+"""GPU parity of the Hyena operator and layouts against the reference golden vectors
+and the oracle (fp32 1e-5, fp64 1e-12-ish, bf16 1e-2 on bf16-representable inputs)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2503_01868_b200 as hy
+
+from .helpers import load, oracle_cfg, product_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_hyena_forward_golden():
+    z = load("hyena")
+    for i in range(int(z["n_h"])):
+        cfg = product_cfg(z, f"h{i}.cfg")
+        x = hy.SeqTensor(z[f"h{i}.x"])
+        got = hy.hyena_forward(x, cfg)
+        assert got.dtype == x.dtype
+        tol = 1e-5 if x.dtype == "f32" else 1e-10
+        err = oracle.rel_err(got.data, z[f"h{i}.y"])
+        assert err < tol, (i, list(z[f"h{i}.args"]), err)
+
+
+def test_identity_collapse_and_known_answers():
+    z = load("hyena")
+    x = hy.SeqTensor(z["ident.x"])
+    y = hy.hyena_forward(x, hy.identity_config(width=3))
+    assert np.max(np.abs(y.data - z["ident.y"])) < 1e-12  # y = x * (x * x)
+    # zero w_q -> y == 0
+    cfg = hy.update_param(hy.identity_config(width=2), ("w_q",), np.zeros((2, 2)))
+    y = hy.hyena_forward(hy.SeqTensor(np.random.default_rng(1).standard_normal((2, 16))), cfg)
+    assert np.max(np.abs(y.data)) == 0.0
+    # one-step delay inner filter: y = x * shift(x*x)
+    rng = hy.make_rng(62)
+    xd = rng.standard_normal((2, 12))
+    inner = hy.GroupSpec(2, 2, (hy.ExplicitFilter(np.array([0.0, 1.0])),))
+    y = hy.hyena_forward(hy.SeqTensor(xd), hy.identity_config(width=2, inner=inner))
+    sq = xd * xd
+    shifted = np.zeros_like(sq)
+    shifted[:, 1:] = sq[:, :-1]
+    assert np.max(np.abs(y.data - xd * shifted)) < 1e-14
+    # MR decay applied: delta input returns the materialized regularized taps
+    spec = hy.RegularizedFilter(np.ones(4), decay_rate=1.0, base=2.0)
+    cfg = hy.identity_config("MR", width=1, inner=hy.GroupSpec(1, 1, (spec,)))
+    y = hy.hyena_forward(hy.SeqTensor(np.array([[1.0, 0.0, 0.0, 0.0]])), cfg)
+    assert np.max(np.abs(y.data - hy.materialize_filter(spec)[None, :])) < 1e-15
+
+
+def test_backends_agree():
+    rng = hy.make_rng(68)
+    x = hy.SeqTensor(rng.standard_normal((8, 96)))
+    base = hy.make_hyena_config("SE", 8, rng, group_size=2, inner_len=9, block_size=8, backend="direct")
+    want = hy.hyena_forward(x, base).data
+    for backend in ("blocked", "fft"):
+        cfg = hy.HyenaConfig(**{**base.__dict__, "backend": backend})
+        assert np.max(np.abs(hy.hyena_forward(x, cfg).data - want)) < 1e-10
+
+
+def test_layout_golden():
+    z = load("layout")
+    layers = tuple(product_cfg(z, f"layer{i}") for i in range(int(z["n_layers"])))
+    spec = hy.LayoutSpec(("SE", "MR", "LI"), 1, layers)
+    for residual in (0, 1):
+        for dtype in ("f32", "f64"):
+            stack = hy.build_layout(spec, residual=bool(residual))
+            x = hy.SeqTensor(z[f"{residual}.{dtype}.x"])
+            got = hy.layout_forward(x, stack)
+            tol = 1e-5 if dtype == "f32" else 1e-10
+            assert oracle.rel_err(got.data, z[f"{residual}.{dtype}.y"]) < tol, (residual, dtype)
+
+
+@pytest.mark.parametrize("variant,B,D,L,kw", [
+    ("MR", 2, 64, 8192, {"inner_len": 128, "block_size": 128}),
+    ("SE", 1, 128, 4096, {}),
+    ("MR", 1, 32, 4096, {"inner_len": 128, "block_size": 128, "group_size": 4}),
+])
+def test_operator_bf16_vs_oracle(variant, B, D, L, kw):
+    """bf16 operator (cuBLAS projections + fused tcgen05 mixer) vs the fp64 oracle on
+    bf16-representable parameters and inputs."""
+    cfg = hy.make_hyena_config(variant, D, hy.make_rng(0), seq_len=L, **kw)
+    rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+    def rbank(g):
+        fs = []
+        for f in g.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fs.append(hy.ExplicitFilter(bf16_round(f.taps)))
+            else:
+                fs.append(hy.RegularizedFilter(bf16_round(f.taps_hat), f.decay_rate, f.base))
+        return hy.GroupSpec(g.channels, g.group_size, tuple(fs))
+    cfg = hy.HyenaConfig(**{**cfg.__dict__, **rnd, **{n: rbank(getattr(cfg, n))
+                                                      for n in ("q_feat", "k_feat", "v_feat", "inner")}})
+    x = bf16_round(np.stack([hy.make_rng(1, stream=b).standard_normal((D, L)) for b in range(B)]))
+    op = hy.HyenaOperator(cfg, torch.bfloat16)
+    y = op.forward(torch.from_numpy(x).to("cuda", torch.bfloat16)).float().cpu().numpy()
+    ocfg = {"variant": cfg.variant, "width": D, "block_size": cfg.block_size, "backend": cfg.backend,
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        g = getattr(cfg, n)
+        ocfg[n] = {"channels": g.channels, "group_size": g.group_size,
+                   "filters": [("explicit", f.taps) if isinstance(f, hy.ExplicitFilter)
+                               else ("regularized", f.taps_hat, f.decay_rate, f.base) for f in g.filters]}
+    for b in range(B):
+        want = oracle.hyena_forward(x[b], ocfg)
+        err = oracle.rel_err(y[b], want)
+        assert err < 1e-2, (b, err)

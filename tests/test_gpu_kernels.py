@@ -1,0 +1,245 @@
+"""GPU parity of the sm_100a kernels against the oracle and the reference golden vectors.
+
+Tolerances (rel_err = ||a-b||_inf / max(||b||_inf, 1), testing.py:57-62):
+  fp64 path: 1e-12; fp32 path: 1e-5 (north star); bf16 path: 1e-2 against the
+  fp64 oracle run on bf16-representable inputs and parameters (north star).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2503_01868_b200 as hy
+from paper_2503_01868_b200 import ops
+
+from .helpers import explicit_bank_from_taps, load, product_groups_from_taps
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+# ---------------------------------------------------------------- direct conv
+
+
+def test_direct_conv_golden():
+    z = load("direct_conv")
+    for i in range(3):
+        x = hy.SeqTensor(np.asarray(z[f"hand{i}.x"], dtype=np.float64))
+        got = hy.direct_causal_conv(x, product_groups_from_taps(z[f"hand{i}.taps"], 1))
+        assert np.array_equal(got.data, z[f"hand{i}.y"]), i
+    for i in range(int(z["n_rand"])):
+        x = hy.SeqTensor(z[f"rand{i}.x"])
+        got = hy.direct_causal_conv(x, product_groups_from_taps(z[f"rand{i}.taps"], int(z[f"rand{i}.gs"])))
+        assert got.dtype == x.dtype
+        assert oracle.rel_err(got.data, z[f"rand{i}.y"]) < TOL[x.dtype], i
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("shape", [(1, 1, 1, 1), (3, 2, 1023, 7), (2, 5, 1025, 33), (1, 4, 3000, 300),
+                                   (2, 3, 8, 20), (4, 2, 4097, 14)])
+def test_causal_conv_batched_vs_oracle(dtype, shape):
+    B, C, L, lh = shape
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal((B, C, L))
+    taps = rng.standard_normal((C, lh)) / np.sqrt(lh)
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    y = ops.causal_conv(dev(x, tdt), dev(taps, tdt), 1).cpu().numpy()
+    for b in range(B):
+        want = oracle.direct_causal_conv(x[b], explicit_bank_from_taps(taps, 1))
+        assert oracle.rel_err(y[b], want) < TOL[dtype]
+
+
+def test_causal_conv_bf16_unaligned_length():
+    rng = np.random.default_rng(5)
+    x = bf16_round(rng.standard_normal((2, 3, 1001)))
+    taps = bf16_round(rng.standard_normal((3, 9)) / 3)
+    y = ops.causal_conv(dev(x, torch.bfloat16), dev(taps), 1).float().cpu().numpy()
+    for b in range(2):
+        want = oracle.direct_causal_conv(x[b], explicit_bank_from_taps(taps, 1))
+        assert oracle.rel_err(y[b], want) < TOL["bf16"]
+
+
+def test_direct_conv_properties():
+    rng = hy.make_rng(11)
+    taps = rng.standard_normal((3, 5))
+    groups = product_groups_from_taps(taps, 1)
+    x = rng.standard_normal((3, 40))
+    bumped = x.copy()
+    bumped[:, 25] += 1.0
+    a = hy.direct_causal_conv(hy.SeqTensor(x), groups).data[:, :25]
+    b = hy.direct_causal_conv(hy.SeqTensor(bumped), groups).data[:, :25]
+    assert np.array_equal(a, b)  # causality
+    x2 = rng.standard_normal((3, 40))
+    lhs = hy.direct_causal_conv(hy.SeqTensor(3.0 * x - 0.5 * x2), groups).data
+    rhs = 3.0 * hy.direct_causal_conv(hy.SeqTensor(x), groups).data - 0.5 * hy.direct_causal_conv(
+        hy.SeqTensor(x2), groups).data
+    assert np.max(np.abs(lhs - rhs)) < 1e-12  # linearity
+    # grouping == replication
+    t4 = rng.standard_normal(4)
+    x6 = rng.standard_normal((6, 30))
+    by_group = hy.GroupSpec(6, 3, (hy.ExplicitFilter(t4),) * 2)
+    repl = hy.GroupSpec(6, 1, (hy.ExplicitFilter(t4),) * 6)
+    assert np.array_equal(hy.direct_causal_conv(hy.SeqTensor(x6), by_group).data,
+                          hy.direct_causal_conv(hy.SeqTensor(x6), repl).data)
+
+
+# ---------------------------------------------------------------- blocked API
+
+
+def test_two_stage_block_chunk_golden():
+    z = load("blockconv")
+    for i in range(int(z["n_ts"])):
+        v = hy.SeqTensor(z[f"ts{i}.v"])
+        q = hy.SeqTensor(z[f"ts{i}.q"]) if f"ts{i}.q" in z else None
+        k = hy.SeqTensor(z[f"ts{i}.k"]) if f"ts{i}.k" in z else None
+        groups = product_groups_from_taps(z[f"ts{i}.taps"], int(z[f"ts{i}.gs"]))
+        got = hy.two_stage_forward(v, groups, int(z[f"ts{i}.lb"]), q=q, k=k)
+        assert oracle.rel_err(got.data, z[f"ts{i}.y"]) < TOL[v.dtype], i
+    v = hy.SeqTensor(z["mixed.v"])
+    got = hy.two_stage_forward(v, product_groups_from_taps(z["mixed.taps"], int(z["mixed.gs"])), 8)
+    assert oracle.rel_err(got.data, z["mixed.y"]) < 1e-12
+    for i in range(int(z["n_bk"])):
+        got = hy.block_conv(hy.SeqTensor(z[f"bk{i}.x"]), product_groups_from_taps(z[f"bk{i}.taps"], int(z[f"bk{i}.gs"])),
+                            int(z[f"bk{i}.lb"]))
+        assert oracle.rel_err(got.data, z[f"bk{i}.y"]) < 1e-12, i
+    got = hy.chunk_parallel_forward(hy.SeqTensor(z["cp.x"]), z["cp.taps"], 8)
+    assert oracle.rel_err(got.data, z["cp.y"]) < 1e-12
+
+
+def test_multiply_counter_both_factors():
+    rng = hy.make_rng(49)
+    counter = hy.MultiplyCounter()
+    x = hy.SeqTensor(rng.standard_normal((4, 64)))
+    groups = hy.GroupSpec(4, 2, tuple(hy.ExplicitFilter(rng.standard_normal(9)) for _ in range(2)))
+    hy.two_stage_forward(x, groups, 8, counter=counter)
+    assert counter.multiplies == 2 * 8 * 8 * 4 * 8
+
+
+# ---------------------------------------------------------------- tcgen05 two-stage (bf16)
+
+
+@pytest.mark.parametrize("B,C,L,lh,gs,gated", [
+    (1, 2, 4096, 128, 1, True),
+    (2, 3, 8192, 129, 1, True),
+    (1, 4, 1024, 7, 2, True),
+    (3, 2, 5000, 100, 1, False),
+    (1, 2, 128, 128, 1, True),
+    (2, 4, 12296, 64, 4, True),
+    (1, 1, 8, 3, 1, True),
+])
+def test_two_stage_tcgen05_vs_oracle(B, C, L, lh, gs, gated):
+    rng = np.random.default_rng(B * 1000 + C * 100 + L + lh)
+    G = C // gs
+    taps = bf16_round(rng.standard_normal((G, lh)) / np.sqrt(lh))
+    v = bf16_round(rng.standard_normal((B, C, L)))
+    q = bf16_round(rng.standard_normal((B, C, L))) if gated else None
+    k = bf16_round(rng.standard_normal((B, C, L))) if gated else None
+    y = ops.two_stage(dev(v, torch.bfloat16), dev(taps), gs,
+                      q=None if q is None else dev(q, torch.bfloat16),
+                      k=None if k is None else dev(k, torch.bfloat16)).float().cpu().numpy()
+    bank = explicit_bank_from_taps(taps, gs)
+    for b in range(B):
+        want = oracle.two_stage_forward(v[b], bank, 128, q=None if q is None else q[b],
+                                        k=None if k is None else k[b])
+        err = oracle.rel_err(y[b], want)
+        assert err < TOL["bf16"], (b, err)
+
+
+def test_two_stage_tcgen05_decay_fused():
+    rng = np.random.default_rng(7)
+    C, L, lh = 4, 4096, 128
+    taps_hat = bf16_round(rng.standard_normal((C, lh)) / np.sqrt(lh))
+    rates = np.linspace(0.01, 2.0, C)
+    v, q, k = (bf16_round(rng.standard_normal((1, C, L))) for _ in range(3))
+    y = ops.two_stage(dev(v, torch.bfloat16), dev(taps_hat), 1, q=dev(q, torch.bfloat16), k=dev(k, torch.bfloat16),
+                      decay=dev(rates * np.log2(2.0))).float().cpu().numpy()
+    bank = {"channels": C, "group_size": 1,
+            "filters": [("regularized", taps_hat[c], float(rates[c]), 2.0) for c in range(C)]}
+    want = oracle.two_stage_forward(v[0], bank, 128, q=q[0], k=k[0])
+    assert oracle.rel_err(y[0], want) < TOL["bf16"]
+
+
+def test_two_stage_tcgen05_known_answers():
+    # delta filter: y = q * k * v exactly in bf16 arithmetic (one nonzero tap)
+    rng = np.random.default_rng(3)
+    C, L = 2, 4096
+    taps = np.zeros((C, 128))
+    taps[:, 0] = 1.0
+    v = bf16_round(rng.standard_normal((1, C, L)))
+    y = ops.two_stage(dev(v, torch.bfloat16), dev(taps), 1).float().cpu().numpy()
+    assert np.array_equal(y, v)
+    # pure delay by 128 (exercises T1 only): y[t] = v[t-128]
+    taps = np.zeros((C, 129))
+    taps[:, 128] = 1.0
+    y = ops.two_stage(dev(v, torch.bfloat16), dev(taps), 1).float().cpu().numpy()
+    want = np.zeros_like(v)
+    want[..., 128:] = v[..., :-128]
+    assert np.array_equal(y, want)
+    with pytest.raises(hy.TwoStageIneligibleError):
+        ops.two_stage(dev(v, torch.bfloat16), dev(np.ones((C, 130))), 1)
+
+
+# ---------------------------------------------------------------- fused mixers
+
+
+def _mixer_oracle(proj, feat, inner_bank):
+    """q * conv_inner(k * v) from raw projections (hyena.py:170-186), fp64."""
+    B, C3, L = proj.shape
+    C = C3 // 3
+    out = np.empty((B, C, L))
+    for b in range(B):
+        q, k, v = (oracle.direct_causal_conv(proj[b, i * C:(i + 1) * C], explicit_bank_from_taps(feat[i], 1))
+                   for i in range(3))
+        out[b] = q * oracle.direct_causal_conv(k * v, inner_bank)
+    return out
+
+
+@pytest.mark.parametrize("B,C,L,lhf,lh,gs", [(2, 4, 8192, 7, 128, 1), (1, 3, 4104, 14, 129, 1),
+                                            (1, 4, 4096, 3, 7, 2), (2, 2, 136, 7, 100, 1)])
+def test_mr_mixer_tcgen05_vs_oracle(B, C, L, lhf, lh, gs):
+    rng = np.random.default_rng(L + lh)
+    proj = bf16_round(rng.standard_normal((B, 3 * C, L)))
+    feat = bf16_round(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    taps = bf16_round(rng.standard_normal((C // gs, lh)) / np.sqrt(lh))
+    y = ops.hyena_mixer(dev(proj, torch.bfloat16), dev(feat), dev(taps), gs).float().cpu().numpy()
+    want = _mixer_oracle(proj, feat, explicit_bank_from_taps(taps, gs))
+    assert oracle.rel_err(y, want) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("B,C,L,lhf,lh,gs", [(1, 4, 4096, 7, 7, 1), (2, 3, 1000, 14, 14, 3), (1, 2, 2049, 3, 16, 1)])
+def test_se_mixer_vs_oracle(dtype, B, C, L, lhf, lh, gs):
+    rng = np.random.default_rng(L + lh + lhf)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    rnd = (lambda a: a) if dtype == "f32" else bf16_round
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    taps = rnd(rng.standard_normal((C // gs, lh)) / np.sqrt(lh))
+    y = ops.hyena_mixer(dev(proj, tdt), dev(feat), dev(taps), gs, se_only=True).float().cpu().numpy()
+    want = _mixer_oracle(np.asarray(dev(proj, tdt).double().cpu()), feat, explicit_bank_from_taps(taps, gs))
+    assert oracle.rel_err(y, want) < TOL[dtype]
+
+
+def test_halo_correction_matches_overlap_scheme():
+    rng = np.random.default_rng(9)
+    C, L, lh = 3, 64, 9
+    taps = rng.standard_normal((C, lh))
+    halo = rng.standard_normal((C, lh - 1))
+    local = rng.standard_normal((C, L))
+    bank = explicit_bank_from_taps(taps, 1)
+    want = oracle.direct_causal_conv(np.concatenate([halo, local], axis=1), bank)[:, lh - 1:]
+    y = ops.causal_conv(dev(local, torch.float64), dev(taps, torch.float64), 1)
+    ops.halo_correction(dev(halo, torch.float64), y, dev(taps, torch.float64), 1)
+    assert oracle.rel_err(y.cpu().numpy(), want) < 1e-12
