@@ -24,6 +24,8 @@
 #include "internal.h"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 namespace hy {
 namespace ts {
 
@@ -39,10 +41,15 @@ constexpr int KV_LEN = (NCH + 1) * LB + HALO;  // staged k / v: prev chunk + til
 constexpr int Q_LEN = NCH * LB + HALO;
 constexpr int MAX_LHF = 16;
 
-constexpr int N_CONV_WARPS = 8, N_EPI_WARPS = 4;
-constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2, W_EPI0 = W_CONV0 + N_CONV_WARPS;
-constexpr int THREADS = (W_EPI0 + N_EPI_WARPS) * 32;
-constexpr int CONV_THREADS = N_CONV_WARPS * 32, EPI_THREADS = N_EPI_WARPS * 32;
+constexpr int N_EPI_WARPS = 4;
+constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
+constexpr int EPI_THREADS = N_EPI_WARPS * 32;
+template <int CW>
+struct Roles {
+  static constexpr int W_EPI0 = W_CONV0 + CW;
+  static constexpr int THREADS = (W_EPI0 + N_EPI_WARPS) * 32;
+  static constexpr int CONV_THREADS = CW * 32;
+};
 constexpr uint32_t BAR_CONV = 1, BAR_EPI = 2;
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
@@ -125,31 +132,55 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int j, int rows) {
   return (j >> 3) * (rows * 128) + row * 128 + (((j & 7) ^ (row & 7)) << 4);
 }
 
-// Featurize 8 consecutive outputs from a 24-wide raw window (r[16 + e] = x(t + e)).
-template <int LHF>
-__device__ __forceinline__ void fir8(const float* r, const float* h, float* out) {
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// Unpack two bf16 vectors elementwise into float2 pairs: out[i] = (a[i], b[i]).
+__device__ __forceinline__ void unpack8_pair(int4 ra, int4 rb, float2* out) {
+  const uint32_t* a = reinterpret_cast<const uint32_t*>(&ra);
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(&rb);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    float acc = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < LHF; ++jj) acc = fmaf(h[jj], r[16 + e - jj], acc);
-    out[e] = acc;
+  for (int i = 0; i < 4; ++i) {
+    out[2 * i] = make_float2(__uint_as_float(a[i] << 16), __uint_as_float(b[i] << 16));
+    out[2 * i + 1] = make_float2(__uint_as_float(a[i] & 0xFFFF0000u), __uint_as_float(b[i] & 0xFFFF0000u));
   }
 }
 
-// Load a window of 24 raw values ending at idx+8 (3 aligned 16-byte vectors).
+// Two FIRs at once on f32x2 lanes: acc[e] = sum_jj h[jj] * r[16 + e - jj] (r: 24-wide pair window).
 template <int LHF>
-__device__ __forceinline__ void load_raw(const bf16* buf, int idx, float* r) {
-  if (LHF > 9) unpack8(*reinterpret_cast<const int4*>(buf + idx - 16), r);
-  if (LHF > 1) unpack8(*reinterpret_cast<const int4*>(buf + idx - 8), r + 8);
-  unpack8(*reinterpret_cast<const int4*>(buf + idx), r + 16);
+__device__ __forceinline__ void fir8x2(const float2* r, const float2* h, float2* acc) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int jj = 0; jj < LHF; ++jj) a = ffma2(h[jj], r[16 + e - jj], a);
+    acc[e] = a;
+  }
 }
 
-template <bool FEAT, bool GK, bool GQ, int LHF>
-__global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+// Load a pair window of 24 (a, b) values ending at idx+8 from two staging buffers.
+template <int LHF>
+__device__ __forceinline__ void load_raw_pair(const bf16* ba, const bf16* bb, int ia, int ib, float2* r) {
+  if (LHF > 9)
+    unpack8_pair(*reinterpret_cast<const int4*>(ba + ia - 16), *reinterpret_cast<const int4*>(bb + ib - 16), r);
+  if (LHF > 1)
+    unpack8_pair(*reinterpret_cast<const int4*>(ba + ia - 8), *reinterpret_cast<const int4*>(bb + ib - 8), r + 8);
+  unpack8_pair(*reinterpret_cast<const int4*>(ba + ia), *reinterpret_cast<const int4*>(bb + ib), r + 16);
+}
+
+template <bool FEAT, bool GK, bool GQ, int LHF, int CW>
+__global__ void __launch_bounds__(Roles<CW>::THREADS, 1) two_stage_kernel(const Params p) {
+  constexpr int W_EPI0 = Roles<CW>::W_EPI0;
+  constexpr int CONV_THREADS = Roles<CW>::CONV_THREADS;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // keep the pointer in the shared window (offset arithmetic, not an integer round trip)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* full = bars;                 // [STAGES] producer -> converter
   uint64_t* empty = bars + STAGES;       // [STAGES] converter -> producer
@@ -171,9 +202,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], 1 + EPI_THREADS);
+      mbar_init(&uempty[i], 1 + N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_THREADS);
+      mbar_init(&tempty[i], N_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -258,9 +289,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   } else if (warp < W_EPI0) {
     // ------------------------------------------------------------ converters
     const int ctid = threadIdx.x - W_CONV0 * 32;
-    float hk[LHF], hv[LHF], hq[LHF];
+    float2 hkv[LHF], hqq[LHF];  // (k, v) and (q, q) featurizer taps on f32x2 lanes
 #pragma unroll
-    for (int i = 0; i < LHF; ++i) hk[i] = hv[i] = hq[i] = (i == 0 ? 1.f : 0.f);
+    for (int i = 0; i < LHF; ++i) hkv[i] = hqq[i] = make_float2(i == 0 ? 1.f : 0.f, i == 0 ? 1.f : 0.f);
     int cur_g = -1, cur_c = -1;
     int it = 0;
     for (int tile = tb; tile < te; ++tile, ++it) {
@@ -299,9 +330,11 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
 #pragma unroll
         for (int i = 0; i < LHF; ++i) {
           const bool ok = i < p.lhf;
-          hq[i] = ok ? p.feat_taps[(static_cast<size_t>(0) * p.C + t.c) * p.lhf + i] : 0.f;
-          hk[i] = ok ? p.feat_taps[(static_cast<size_t>(1) * p.C + t.c) * p.lhf + i] : 0.f;
-          hv[i] = ok ? p.feat_taps[(static_cast<size_t>(2) * p.C + t.c) * p.lhf + i] : 0.f;
+          const float hq = ok ? p.feat_taps[(static_cast<size_t>(0) * p.C + t.c) * p.lhf + i] : 0.f;
+          const float hk = ok ? p.feat_taps[(static_cast<size_t>(1) * p.C + t.c) * p.lhf + i] : 0.f;
+          const float hv = ok ? p.feat_taps[(static_cast<size_t>(2) * p.C + t.c) * p.lhf + i] : 0.f;
+          hkv[i] = make_float2(hk, hv);
+          hqq[i] = make_float2(hq, hq);
         }
         cur_c = t.c;
       }
@@ -316,13 +349,11 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         const int idx = (n + 1) * LB + HALO + 8 * j;
         float uv[8];
         if (FEAT) {
-          float r[24], fk[8];
-          load_raw<LHF>(kbuf, idx, r);
-          fir8<LHF>(r, hk, fk);
-          load_raw<LHF>(vbuf, idx, r);
-          fir8<LHF>(r, hv, uv);
+          float2 r[24], acc[8];
+          load_raw_pair<LHF>(kbuf, vbuf, idx, idx, r);
+          fir8x2<LHF>(r, hkv, acc);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) uv[e] *= fk[e];
+          for (int e = 0; e < 8; ++e) uv[e] = acc[e].x * acc[e].y;
         } else {
           unpack8(*reinterpret_cast<const int4*>(vbuf + idx), uv);
           if (GK) {
@@ -338,18 +369,25 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       }
       if (GQ) {
         float* fq = reinterpret_cast<float*>(smem + OFF_FQ + u * FQ_BYTES);
-        for (int i = ctid; i < NCH * 16; i += CONV_THREADS) {
-          const int idx = HALO + 8 * i;  // i = n*16 + j  ->  time n*128 + 8j
-          float o[8];
+        constexpr int NQ = NCH * 16, HQ = NQ / 2;  // q units, processed in pairs (i, i + HQ)
+        for (int i = ctid; i < HQ; i += CONV_THREADS) {
+          // unit i -> time 8i (= chunk n*128 + 8j with i = n*16 + j)
+          const int ia = HALO + 8 * i, ib = HALO + 8 * (i + HQ);
+          float2 o[8];
           if (FEAT) {
-            float r[24];
-            load_raw<LHF>(qbuf, idx, r);
-            fir8<LHF>(r, hq, o);
+            float2 r[24];
+            load_raw_pair<LHF>(qbuf, qbuf, ia, ib, r);
+            fir8x2<LHF>(r, hqq, o);
           } else {
-            unpack8(*reinterpret_cast<const int4*>(qbuf + idx), o);
+            float2 r[8];
+            unpack8_pair(*reinterpret_cast<const int4*>(qbuf + ia), *reinterpret_cast<const int4*>(qbuf + ib), r);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = r[e];
           }
-          *reinterpret_cast<float4*>(fq + 8 * i) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(fq + 8 * i + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          *reinterpret_cast<float4*>(fq + 8 * i) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
+          *reinterpret_cast<float4*>(fq + 8 * i + 4) = make_float4(o[4].x, o[5].x, o[6].x, o[7].x);
+          *reinterpret_cast<float4*>(fq + 8 * (i + HQ)) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
+          *reinterpret_cast<float4*>(fq + 8 * (i + HQ) + 4) = make_float4(o[4].y, o[5].y, o[6].y, o[7].y);
         }
       }
       fence_proxy_async();
@@ -373,7 +411,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       float acc[NCH];
       tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + a * NCH, acc);
       tc_fence_before();
-      mbar_arrive(&tempty[a]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
       if (etid == 0 && it >= 2) bulk_wait_read<1>();
       named_bar_sync(BAR_EPI, EPI_THREADS);
       bf16* yb = reinterpret_cast<bf16*>(smem + OFF_Y + a * Y_BYTES);
@@ -384,7 +423,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         if (GQ) val *= fq[n * LB + tout];
         yb[n * LB + tout] = __float2bfloat16_rn(val);
       }
-      mbar_arrive(&uempty[a]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&uempty[a]);
       fence_proxy_async();
       named_bar_sync(BAR_EPI, EPI_THREADS);
       if (etid == 0) {
@@ -403,9 +443,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   if (warp == W_MMA) tmem_dealloc<2 * NCH>(tmem_base);
 }
 
-template <bool FEAT, bool GK, bool GQ, int LHF>
-static int launch(const Params& p, cudaStream_t st) {
-  auto kern = two_stage_kernel<FEAT, GK, GQ, LHF>;
+template <bool FEAT, bool GK, bool GQ, int LHF, int CW>
+static int launch_cw(const Params& p, cudaStream_t st) {
+  auto kern = two_stage_kernel<FEAT, GK, GQ, LHF, CW>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -416,8 +456,23 @@ static int launch(const Params& p, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = p.total_tiles < sms ? p.total_tiles : sms;
-  kern<<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  kern<<<grid, Roles<CW>::THREADS, SMEM_BYTES, st>>>(p);
   return check_launch("two_stage_kernel");
+}
+
+// Converter warp count: 8 (default) or 12 (HY_TS_CONV_WARPS=12), for tuning.
+static int conv_warps() {
+  static int cw = [] {
+    const char* e = getenv("HY_TS_CONV_WARPS");
+    return (e && atoi(e) == 12) ? 12 : 8;
+  }();
+  return cw;
+}
+
+template <bool FEAT, bool GK, bool GQ, int LHF>
+static int launch(const Params& p, cudaStream_t st) {
+  if (conv_warps() == 12) return launch_cw<FEAT, GK, GQ, LHF, 12>(p, st);
+  return launch_cw<FEAT, GK, GQ, LHF, 8>(p, st);
 }
 
 int check_shapes(int B, int C, int L, int lh, int gs) {

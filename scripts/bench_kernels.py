@@ -1,0 +1,83 @@
+"""Kernel micro-benchmarks (device-resident inputs, CUDA events, after warm-up).
+
+Prints one JSON line per kernel: duration, algorithmic bytes, achieved GB/s and
+fraction of the measured HBM peak. Used for tuning; bench.py is the contract.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2503_01868_b200 import ops  # noqa: E402
+
+
+def peak_hbm():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except OSError:
+        return 6650.0
+
+
+def timeit(fn, iters=20, warmup=5):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def report(name, ms, nbytes, **extra):
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    print(json.dumps({"kernel": name, "ms": round(ms, 4), "bytes": nbytes, "GB/s": round(gbs, 1),
+                      "frac_hbm": round(gbs / peak_hbm(), 3), **extra}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="all")
+    args = ap.parse_args()
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(0)
+    # MR mixer at C2: proj (4, 3*4096, 8192) bf16 -> y (4, 4096, 8192)
+    if args.which in ("all", "mr"):
+        B, D, L = 4, 4096, 8192
+        proj = torch.randn((B, 3 * D, L), device=dev, dtype=torch.bfloat16, generator=g)
+        feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
+        taps = torch.randn((D, 128), device=dev, generator=g) / 11
+        decay = torch.linspace(0.01, 2.0, D, device=dev)
+        ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, decay=decay))
+        report("mr_mixer_tcgen05", ms, 8 * D * B * L, B=B, D=D, L=L)
+        v = proj[:, :D].contiguous()
+        k = proj[:, D:2 * D].contiguous()
+        q = proj[:, 2 * D:].contiguous()
+        ms = timeit(lambda: ops.two_stage(v, taps, 1, q=q, k=k, decay=decay))
+        report("two_stage_tcgen05_gated", ms, 8 * D * B * L, B=B, D=D, L=L)
+        del proj, v, k, q
+    if args.which in ("all", "se"):
+        B, D, L = 1, 4096, 4096
+        for dt, name in ((torch.float32, "se_mixer_f32"), (torch.bfloat16, "se_mixer_bf16")):
+            proj = torch.randn((B, 3 * D, L), device=dev, dtype=dt, generator=g)
+            feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
+            taps = torch.randn((D, 7), device=dev, generator=g) / 3
+            ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, se_only=True))
+            report(name, ms, 4 * D * B * L * proj.element_size(), B=B, D=D, L=L)
+            x = proj.reshape(B * 3, D, L)
+            ms = timeit(lambda: ops.causal_conv(x, feat.reshape(3 * D, 7), 1))
+            report(name.replace("se_mixer", "featurizer"), ms, 2 * x.numel() * x.element_size(), rows=3 * D, L=L)
+
+
+if __name__ == "__main__":
+    main()

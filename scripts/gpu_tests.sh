@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/smi.txt 2>&1
+timeout 180 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+tail -3 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -40 gpurun_out/pytest_gpu.log

@@ -52,8 +52,9 @@ def test_identity_collapse_and_known_answers():
     # MR decay applied: delta input returns the materialized regularized taps
     spec = hy.RegularizedFilter(np.ones(4), decay_rate=1.0, base=2.0)
     cfg = hy.identity_config("MR", width=1, inner=hy.GroupSpec(1, 1, (spec,)))
-    y = hy.hyena_forward(hy.SeqTensor(np.array([[1.0, 0.0, 0.0, 0.0]])), cfg)
-    assert np.max(np.abs(y.data - hy.materialize_filter(spec)[None, :])) < 1e-15
+    xd = np.array([[1.0, 0.0, 0.0, 0.0]])
+    y = hy.hyena_forward(hy.SeqTensor(xd), cfg)
+    assert np.max(np.abs(y.data - xd * hy.materialize_filter(spec)[None, :])) < 1e-15
 
 
 def test_backends_agree():
