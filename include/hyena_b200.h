@@ -107,6 +107,10 @@ HY_API int hy_fft_conv_fwd(const void* q, const void* k, const void* v, void* y,
 HY_API int hy_halo_correction_fwd(const void* halo, void* y, const void* taps,
                            int B, int C, int L, int lh, int group_size, int dtype, void* stream);
 
+/* Debug / tuning: CTA-0 per-tile timeline (clock64) of the last two-stage launch made
+ * with HY_TS_TRACE=1 in the environment; n <= 4096 values, 8 events per tile. */
+HY_API int hy_debug_two_stage_trace(unsigned long long* host_out, int n);
+
 #ifdef __cplusplus
 }
 #endif

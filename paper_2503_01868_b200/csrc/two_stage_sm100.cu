@@ -1,30 +1,44 @@
 // Two-stage blocked causal convolution on 5th-gen tensor cores (sm_100a).
 //
 // Restates blockconv.py:160-220 (two_stage_forward / _two_stage_core) and, in
-// the fused form, hyena.py:162-186 (featurizers + gates) for bf16:
+// the fused form, hyena.py:162-186 (featurizers + gates), bf16 in / fp32 accumulate:
 //
-//     u = k * v                       (k, v optionally featurized in-kernel)
-//     Y_n = T0 . U_n + T1 . U_{n-1}   (128-step chunks, T0/T1 = Toeplitz factors)
-//     y = q * Y                       (q optionally featurized in-kernel)
+//     k, v, q = featurizer FIRs of the raw rows     (tcgen05, overlapping windows)
+//     u = k * v                                      (CUDA cores, TMEM -> SMEM)
+//     Y_n = T0 . U_n + T1 . U_{n-1}                  (tcgen05, 128-step chunks)
+//     y = q * Y                                      (CUDA cores, TMEM -> HBM)
 //
-// Mapping (per channel c, tile = NCH consecutive chunks of one sequence (b, c)):
-//   MMA M = 128 output steps within a chunk, N = NCH chunks, K = 128 input steps.
-//   A = T0 / T1 (built in SMEM from taps_hat with the decay applied, SW128 K-major),
-//   B = U / U_prev (built in SMEM by the converter warps from staged k, v),
-//   D = fp32 accumulator in TMEM (double buffered).
+// Main GEMM per tile (one sequence (b, c), NCH = 32 consecutive 128-step chunks):
+//   D[t_out][chunk] = T0[t_out][:] . U[chunk][:] + T1[t_out][:] . U_prev[chunk][:]
+//   M = 128, N = 32, K = 128; A = T0/T1 built in SMEM from taps_hat with the
+//   regularisation decay exp2(-rate*log2(base)*t) applied in-kernel (SW128 K-major),
+//   B = U / U_prev written by the converter warps (SW128 K-major), D in TMEM.
 //
-// Warp roles (448 threads, 1 CTA per SM, persistent over a contiguous tile range):
-//   warp 0      producer : 1-D bulk copies (cp.async.bulk, UBLKCP) of the raw k / v / q
-//                          windows of a tile into a STAGES-deep SMEM ring
-//   warp 1      MMA      : TMEM alloc; one lane issues 16 tcgen05.mma per tile
-//   warps 2-9   converter: Toeplitz factors on group change; featurizer FIRs;
-//                          u = k*v -> bf16 swizzled operand U and U_prev; featurized q
-//   warps 10-13 epilogue : tcgen05.ld accumulator -> y = q * acc -> SMEM -> bulk store
+// Featurizer GEMMs (short FIR of <= 16 taps, on the raw staged rows): the staged
+// row p is read as overlapping 8-step windows, A[m][k] = p[8m + k] — the
+// no-swizzle K-major canonical layout with LBO = 16 B and SBO = 128 B — so that
+//   D[m][n] = sum_k A[m][k] F[n][k] = feat(8m + 8*KS + n),  F[n][k] = h[8*KS + n - k],
+// M = 128 windows (1024 outputs) per MMA, N = 16 (8 used), K = 16*KS. Each TMEM
+// lane then holds 8 consecutive featurized samples: exactly one 16-byte unit of
+// the U operand.
+//
+// Warp roles (608 threads, 1 CTA per SM, persistent over a contiguous tile range):
+//   warps 0-7   converter: TMEM feat -> u = k*v -> bf16 swizzled U / U_prev and
+//                          featurized q -> SMEM
+//   warps 8-11  epilogue : TMEM acc -> y = q * acc -> 64-byte coalesced stores
+//   warps 12-15 T builder: Toeplitz factors T0 / T1 of the next filter group, each
+//                          rebuilt as soon as the last MMA reading the old one retires
+//                          (tcgen05.commit after that tile's T0 / T1 MMAs)
+//   warp 16     feat MMA : one lane issues the featurizer MMAs of each tile, then frees
+//                          the stage (tcgen05.commit -> empty barrier)
+//   warp 17     MMA      : TMEM alloc (512 cols); one lane issues the 16 main MMAs per tile
+//   warp 18     producer : 1-D bulk copies (cp.async.bulk) of raw k/v/q windows into a
+//                          4-deep SMEM ring + the per-channel featurizer matrices F
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
-
-#include <cstdlib>
 
 namespace hy {
 namespace ts {
@@ -32,48 +46,56 @@ namespace ts {
 using bf16 = __nv_bfloat16;
 using namespace sm100;
 
-constexpr int LB = 128;            // chunk length (= MMA M = MMA K)
-constexpr int NCH = 32;            // chunks per tile (= MMA N)
+constexpr int LB = 128;            // chunk length (= main MMA M = K)
+constexpr int NCH = 32;            // chunks per tile (= main MMA N)
 constexpr int TILE_T = NCH * LB;   // time steps per tile
 constexpr int HALO = 16;           // featurizer history staged before each window
-constexpr int STAGES = 3;
 constexpr int KV_LEN = (NCH + 1) * LB + HALO;  // staged k / v: prev chunk + tile + halo
 constexpr int Q_LEN = NCH * LB + HALO;
+constexpr int KV_WIN = (NCH + 1) * LB / 8;     // 528 featurizer windows for k / v
+constexpr int KV_MB = (KV_WIN + 127) / 128;    // 5 M-blocks
+constexpr int Q_WIN = NCH * LB / 8;            // 512 windows for q
+constexpr int Q_MB = Q_WIN / 128;              // 4 M-blocks
 constexpr int MAX_LHF = 16;
 
-constexpr int N_EPI_WARPS = 4;
-constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
-constexpr int EPI_THREADS = N_EPI_WARPS * 32;
-template <int CW>
-struct Roles {
-  static constexpr int W_EPI0 = W_CONV0 + CW;
-  static constexpr int THREADS = (W_EPI0 + N_EPI_WARPS) * 32;
-  static constexpr int CONV_THREADS = CW * 32;
-};
-constexpr uint32_t BAR_CONV = 1, BAR_EPI = 2;
+// The warp scheduler favours higher warp ids, so the latency-critical single-lane
+// roles (producer, MMA issuers) take the top ids and the bulk CUDA-core roles the bottom.
+constexpr int N_CONV_WARPS = 8, N_EPI_WARPS = 4, N_TB_WARPS = 4;
+constexpr int W_CONV0 = 0, W_EPI0 = W_CONV0 + N_CONV_WARPS, W_TB0 = W_EPI0 + N_EPI_WARPS;
+constexpr int W_FMMA = W_TB0 + N_TB_WARPS, W_MMA = W_FMMA + 1, W_PROD = W_MMA + 1;
+constexpr int THREADS = (W_PROD + 1) * 32;
+constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
+constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
+
+// TMEM columns (512 allocated): main accumulators [2] x 32, featurizer buffers [2] x 224
+constexpr uint32_t TM_ACC = 0, TM_FEAT = 2 * NCH, TM_FEAT_STRIDE = 224;
+constexpr uint32_t TM_K = 0, TM_V = 16 * KV_MB, TM_Q = 32 * KV_MB;
+static_assert(TM_Q + 16 * Q_MB <= TM_FEAT_STRIDE, "feat TMEM layout");
+static_assert(TM_FEAT + 2 * TM_FEAT_STRIDE <= 512, "TMEM budget");
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
-constexpr int T_BYTES = LB * LB * 2;           // one factor, bf16
-constexpr int U_BYTES = NCH * LB * 2;          // one operand buffer
-constexpr int FQ_BYTES = NCH * LB * 4;         // featurized q, fp32
-constexpr int Y_BYTES = NCH * LB * 2;
 constexpr int KV_BYTES = round_up(KV_LEN * 2, 128);
 constexpr int Q_BYTES = round_up(Q_LEN * 2, 128);
-constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;
-constexpr int OFF_T0 = 0;
-constexpr int OFF_T1 = OFF_T0 + T_BYTES;
-constexpr int OFF_U = OFF_T1 + T_BYTES;        // U[2]
-constexpr int OFF_UP = OFF_U + 2 * U_BYTES;    // U_prev[2]
-constexpr int OFF_FQ = OFF_UP + 2 * U_BYTES;   // featq[2]
-constexpr int OFF_Y = OFF_FQ + 2 * FQ_BYTES;   // ybuf[2]
-constexpr int OFF_ST = OFF_Y + 2 * Y_BYTES;    // stage ring
-constexpr int OFF_HP = OFF_ST + STAGES * STAGE_BYTES;  // padded taps, bf16 [512]
-constexpr int OFF_BAR = OFF_HP + 1024;
-constexpr int N_BARS = 2 * STAGES + 8;
-constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-static_assert((U_BYTES % 1024) == 0 && (OFF_U % 1024) == 0 && (OFF_UP % 1024) == 0, "SW128 alignment");
+constexpr int F_BYTES = 512;  // one 16x16 bf16 featurizer matrix (no-swizzle K-major)
+template <int KS>
+struct Layout {
+  static constexpr int STAGES = KS == 1 ? 4 : 3;
+  static constexpr int F_SET = 3 * KS * F_BYTES;  // q, k, v featurizer matrices
+  static constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES + F_SET;
+  static constexpr int OFF_ST = 0;  // stages first: window over-reads stay inside SMEM
+  static constexpr int OFF_T0 = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);
+  static constexpr int OFF_T1 = OFF_T0 + LB * LB * 2;
+  static constexpr int OFF_U = OFF_T1 + LB * LB * 2;        // U[2]
+  static constexpr int OFF_UP = OFF_U + 2 * NCH * LB * 2;   // U_prev[2]
+  static constexpr int OFF_FQ = OFF_UP + 2 * NCH * LB * 2;  // featurized q, bf16 [2]
+  static constexpr int OFF_HP = OFF_FQ + 2 * NCH * LB * 2;  // padded taps, bf16 [512]
+  static constexpr int OFF_FC = OFF_HP + 1024;               // F of the producer's channel
+  static constexpr int OFF_BAR = OFF_FC + F_SET;
+  static constexpr int N_BARS = 2 * STAGES + 20;
+  static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
 
 struct Params {
   const bf16* q;      // non-fused: gates / input, rows (b*C + c)*L
@@ -86,20 +108,42 @@ struct Params {
   const float* feat_taps;  // fused: (3, C, lhf), per channel
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
+  int trace;
 };
 
-struct Tile {
-  int c, b, t0;
-};
-__device__ __forceinline__ Tile decode(int tile, const Params& p) {
-  Tile t;
-  const int j = tile % p.tiles_per_seq;
-  const int r = tile / p.tiles_per_seq;
-  t.b = r % p.B;
-  t.c = r / p.B;
-  t.t0 = j * TILE_T;
-  return t;
+// Optional timeline trace (debug/tuning): CTA 0 records clock64 per tile and event.
+constexpr int TRACE_TILES = 256, TRACE_EV = 16;
+__device__ unsigned long long g_trace[TRACE_TILES * TRACE_EV];
+__device__ __forceinline__ void trace(const Params& p, int it, int ev) {
+  if (p.trace && blockIdx.x == 0 && it < TRACE_TILES) g_trace[it * TRACE_EV + ev] = clock64();
 }
+
+// Tiles are ordered (channel, batch, time-tile) with the time tile fastest; each role
+// walks its contiguous range with an incremental iterator (one division at start).
+struct Tile {
+  int c, b, j, t0;
+  __device__ __noinline__ void init(int tile, const Params& p) {
+    j = tile % p.tiles_per_seq;
+    const int r = tile / p.tiles_per_seq;
+    b = r % p.B;
+    c = r / p.B;
+    t0 = j * TILE_T;
+  }
+  __device__ __forceinline__ void next(const Params& p) {
+    if (++j == p.tiles_per_seq) {
+      j = 0;
+      if (++b == p.B) {
+        b = 0;
+        ++c;
+      }
+    }
+    t0 = j * TILE_T;
+  }
+  // last tile of its channel: the next tile (if any) belongs to channel c + 1
+  __device__ __forceinline__ bool last_of_channel(const Params& p) const {
+    return j == p.tiles_per_seq - 1 && b == p.B - 1;
+  }
+};
 
 template <bool FEAT>
 __device__ __forceinline__ const bf16* row_ptr(const Params& p, int which, int b, int c) {
@@ -109,15 +153,6 @@ __device__ __forceinline__ const bf16* row_ptr(const Params& p, int which, int b
   return base + (static_cast<size_t>(b) * p.C + c) * p.L;
 }
 
-__device__ __forceinline__ void unpack8(int4 raw, float* out) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 f = __bfloat1622float2(h[i]);
-    out[2 * i] = f.x;
-    out[2 * i + 1] = f.y;
-  }
-}
 __device__ __forceinline__ int4 pack8(const float* in) {
   int4 raw;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
@@ -132,83 +167,69 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int j, int rows) {
   return (j >> 3) * (rows * 128) + row * 128 + (((j & 7) ^ (row & 7)) << 4);
 }
 
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(d)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&d);
+// No-swizzle K-major descriptor with explicit leading / stride byte offsets.
+__device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (static_cast<uint64_t>((saddr >> 4) & 0x3FFF)) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+         (static_cast<uint64_t>(sbo >> 4) << 32) | (static_cast<uint64_t>(1) << 46);
 }
 
-// Unpack two bf16 vectors elementwise into float2 pairs: out[i] = (a[i], b[i]).
-__device__ __forceinline__ void unpack8_pair(int4 ra, int4 rb, float2* out) {
-  const uint32_t* a = reinterpret_cast<const uint32_t*>(&ra);
-  const uint32_t* b = reinterpret_cast<const uint32_t*>(&rb);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    out[2 * i] = make_float2(__uint_as_float(a[i] << 16), __uint_as_float(b[i] << 16));
-    out[2 * i + 1] = make_float2(__uint_as_float(a[i] & 0xFFFF0000u), __uint_as_float(b[i] & 0xFFFF0000u));
-  }
+// 32 lanes x 8 consecutive fp32 columns.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Two FIRs at once on f32x2 lanes: acc[e] = sum_jj h[jj] * r[16 + e - jj] (r: 24-wide pair window).
-template <int LHF>
-__device__ __forceinline__ void fir8x2(const float2* r, const float2* h, float2* acc) {
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    float2 a = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int jj = 0; jj < LHF; ++jj) a = ffma2(h[jj], r[16 + e - jj], a);
-    acc[e] = a;
-  }
-}
-
-// Load a pair window of 24 (a, b) values ending at idx+8 from two staging buffers.
-template <int LHF>
-__device__ __forceinline__ void load_raw_pair(const bf16* ba, const bf16* bb, int ia, int ib, float2* r) {
-  if (LHF > 9)
-    unpack8_pair(*reinterpret_cast<const int4*>(ba + ia - 16), *reinterpret_cast<const int4*>(bb + ib - 16), r);
-  if (LHF > 1)
-    unpack8_pair(*reinterpret_cast<const int4*>(ba + ia - 8), *reinterpret_cast<const int4*>(bb + ib - 8), r + 8);
-  unpack8_pair(*reinterpret_cast<const int4*>(ba + ia), *reinterpret_cast<const int4*>(bb + ib), r + 16);
-}
-
-template <bool FEAT, bool GK, bool GQ, int LHF, int CW>
-__global__ void __launch_bounds__(Roles<CW>::THREADS, 1) two_stage_kernel(const Params p) {
-  constexpr int W_EPI0 = Roles<CW>::W_EPI0;
-  constexpr int CONV_THREADS = Roles<CW>::CONV_THREADS;
+// KS: K-steps of 16 in the featurizer GEMM (1 for lhf <= 9, 2 for lhf <= 16).
+template <bool FEAT, bool GK, bool GQ, int KS>
+__global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
+  using LY = Layout<KS>;
+  constexpr int STAGES = LY::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // keep the pointer in the shared window (offset arithmetic, not an integer round trip)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;                 // [STAGES] producer -> converter
-  uint64_t* empty = bars + STAGES;       // [STAGES] converter -> producer
-  uint64_t* ufull = bars + 2 * STAGES;   // [2] converter -> MMA
-  uint64_t* uempty = ufull + 2;          // [2] MMA commit + epilogue -> converter
-  uint64_t* tfull = ufull + 4;           // [2] MMA commit -> epilogue
-  uint64_t* tempty = ufull + 6;          // [2] epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
-  bf16* hpad = reinterpret_cast<bf16*>(smem + OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LY::OFF_BAR);
+  uint64_t* full = bars;                 // [STAGES] producer -> MMA
+  uint64_t* empty = bars + STAGES;       // [STAGES] MMA commit (featurizer done) -> producer
+  uint64_t* ffull = bars + 2 * STAGES;   // [2] MMA commit -> converter (featurized in TMEM)
+  uint64_t* fempty = ffull + 2;          // [2] converter -> MMA (feat TMEM drained)
+  uint64_t* ufull = ffull + 4;           // [2] converter -> MMA
+  uint64_t* uempty = ffull + 6;          // [2] MMA commit (U / U_prev read) -> converter
+  uint64_t* tfull = ffull + 8;           // [2] MMA commit -> epilogue
+  uint64_t* tempty = ffull + 10;         // [2] epilogue warps -> MMA
+  uint64_t* tfree = ffull + 12;          // [2] MMA commit: last reader of T0 / T1 done
+  uint64_t* tready = ffull + 14;         // [2] T builder -> MMA: T0 / T1 of the next group
+  uint64_t* qfull = ffull + 16;          // [2] converter -> epilogue: featurized q in SMEM
+  uint64_t* qempty = ffull + 18;         // [2] epilogue warps -> converter
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
+  bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tb = static_cast<int>((static_cast<long long>(blockIdx.x) * p.total_tiles) / gridDim.x);
   const int te = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * p.total_tiles) / gridDim.x);
+  const int ntiles = te - tb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&ffull[i], 1);
+      mbar_init(&fempty[i], 1);
       mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], 1 + N_EPI_WARPS);
+      mbar_init(&uempty[i], 1);
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
+      mbar_init(&tfree[i], 1);
+      mbar_init(&tready[i], 1);
     }
     fence_mbar_init();
   }
-  if (warp == W_MMA) tmem_alloc<2 * NCH>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -216,20 +237,44 @@ __global__ void __launch_bounds__(Roles<CW>::THREADS, 1) two_stage_kernel(const 
 
   if (warp == W_PROD) {
     // ------------------------------------------------------------ producer
-    int it = 0;
-    for (int tile = tb; tile < te; ++tile, ++it) {
+    int stage_c[STAGES];
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) stage_c[s] = -1;
+    // featurizer taps (lane = tap index) of the current channel, and of the next channel
+    // already in flight: the global loads are issued one channel ahead of their use
+    float hl_cur[3], hl_nxt[3];
+    int cur_c = -1;
+    auto load_taps = [&](int c, float (&hl)[3]) {
+#pragma unroll
+      for (int tensor = 0; tensor < 3; ++tensor) {
+        if (FEAT)
+          hl[tensor] = lane < p.lhf ? p.feat_taps[(static_cast<size_t>(tensor) * p.C + c) * p.lhf + lane] : 0.f;
+        else
+          hl[tensor] = lane == 0 ? 1.f : 0.f;
+      }
+    };
+    Tile t;
+    t.init(tb, p);
+    if (ntiles > 0) load_taps(FEAT ? t.c : 0, hl_nxt);
+    const int c_end = ntiles > 0 ? (te - 1) / (p.tiles_per_seq * p.B) : -1;  // last channel in range
+    for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int s = it % STAGES;
+      if (lane == 0) trace(p, it, 12);
       mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-      const Tile t = decode(tile, p);
-      bf16* kbuf = reinterpret_cast<bf16*>(smem + OFF_ST + s * STAGE_BYTES);
-      bf16* vbuf = kbuf + KV_BYTES / 2;
-      bf16* qbuf = vbuf + KV_BYTES / 2;
+      if (lane == 0) trace(p, it, 0);
+      if (lane == 0) trace(p, it, 7);
+      unsigned char* st = smem + LY::OFF_ST + s * LY::STAGE_BYTES;
+      bf16* kbuf = reinterpret_cast<bf16*>(st);
+      bf16* vbuf = reinterpret_cast<bf16*>(st + KV_BYTES);
+      bf16* qbuf = reinterpret_cast<bf16*>(st + 2 * KV_BYTES);
+      bf16* fmat = reinterpret_cast<bf16*>(st + 2 * KV_BYTES + Q_BYTES);  // [3 tensors][KS][256]
       const int kws = t.t0 - LB - HALO, kwe = t.t0 + TILE_T;
       const int kvs = max(kws, 0), kve = min(kwe, p.L);
       const int qws = t.t0 - HALO, qwe = t.t0 + TILE_T;
       const int qvs = max(qws, 0), qve = min(qwe, p.L);
       // zero the parts of the windows outside [0, L) (whole 8-element units)
       const int4 z = make_int4(0, 0, 0, 0);
+      bool wrote = kvs != kws || kve != kwe || qvs != qws || qve != qwe;  // generic SMEM writes?
       for (int i = lane * 8; i < kvs - kws; i += 256) {
         *reinterpret_cast<int4*>(vbuf + i) = z;
         if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
@@ -242,213 +287,317 @@ __global__ void __launch_bounds__(Roles<CW>::THREADS, 1) two_stage_kernel(const 
         for (int i = lane * 8; i < qvs - qws; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
         for (int i = (qve - qws) + lane * 8; i < Q_LEN; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
       }
-      fence_proxy_async();
+      // featurizer matrices F[n][k] = h[8*KS + n - k] (n < 8), no-swizzle K-major:
+      // element (n, k) of K-step ks at (n%8)*16 + (n/8)*256 + (k%8)*2 + (k/8)*128 bytes.
+      // Taps come in with one load per lane (lane = tap index) and move by shuffles.
+      if (lane == 0) trace(p, it, 8);
+      const int want_c = FEAT ? t.c : 0;
+      if (want_c != cur_c) {
+        cur_c = want_c;
+#pragma unroll
+        for (int tensor = 0; tensor < 3; ++tensor) hl_cur[tensor] = hl_nxt[tensor];
+        if (FEAT && t.c < c_end) load_taps(t.c + 1, hl_nxt);
+        // F[n][k] = h[8*KS + n - k] (n < 8), no-swizzle K-major: element (n, k) of K-step
+        // ks at (n%8)*16 + (n/8)*256 + (k%8)*2 + (k/8)*128 bytes; taps move by shuffles.
+        bf16* fc = reinterpret_cast<bf16*>(smem + LY::OFF_FC);
+#pragma unroll
+        for (int tensor = 0; tensor < 3; ++tensor) {
+#pragma unroll 1
+          for (int r = 0; r < KS * 8; ++r) {
+            const int e = r * 32 + lane;  // 8*KS rounds of 32 lanes cover KS * 256 entries
+            const int ks = e / 256, n = (e / 16) % 16, kk = e % 16;
+            const int tap = 8 * KS + n - (16 * ks + kk);
+            const float hv = __shfl_sync(0xffffffffu, hl_cur[tensor], tap & 31);
+            const float h = (n < 8 && tap >= 0 && tap < MAX_LHF) ? hv : 0.f;
+            const int off = (n & 7) * 8 + (n >> 3) * 128 + (kk & 7) + (kk >> 3) * 64;
+            fc[(tensor * KS + ks) * 256 + off] = __float2bfloat16_rn(h);
+          }
+        }
+        __syncwarp();
+      }
+      if (stage_c[s] != want_c) {
+        // copy the channel's F set (built once per channel below) into the stage
+        const int4* src = reinterpret_cast<const int4*>(smem + LY::OFF_FC);
+        int4* dst = reinterpret_cast<int4*>(fmat);
+#pragma unroll
+        for (int i = lane; i < LY::F_SET / 16; i += 32) dst[i] = src[i];
+        stage_c[s] = want_c;
+        wrote = true;
+      }
+      if (lane == 0) trace(p, it, 9);
+      if (wrote) fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) trace(p, it, 10);
+      if (elect_one()) {
         const uint32_t kvb = static_cast<uint32_t>(kve - kvs) * 2, qb = static_cast<uint32_t>(qve - qvs) * 2;
         mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0));
         bulk_g2s(vbuf + (kvs - kws), row_ptr<FEAT>(p, 2, t.b, t.c) + kvs, kvb, &full[s]);
         if (GK) bulk_g2s(kbuf + (kvs - kws), row_ptr<FEAT>(p, 1, t.b, t.c) + kvs, kvb, &full[s]);
         if (GQ) bulk_g2s(qbuf + (qvs - qws), row_ptr<FEAT>(p, 0, t.b, t.c) + qvs, qb, &full[s]);
-      } else {
-        mbar_arrive(&full[s]);
+        trace(p, it, 11);
       }
     }
-  } else if (warp == W_MMA) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32<LB, NCH>();
-      const uint32_t t0a = smem_u32(smem + OFF_T0), t1a = smem_u32(smem + OFF_T1);
-      int it = 0;
-      for (int tile = tb; tile < te; ++tile, ++it) {
-        const int u = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
-        mbar_wait(&ufull[u], ph);
-        mbar_wait(&tempty[u], ph ^ 1);
+  } else if (warp == W_FMMA) {
+    // ------------------------------------------------------------ featurizer MMA issuer
+    // (the whole warp walks the loop so operands stay warp-uniform; one lane issues)
+    {
+      constexpr uint32_t idesc_feat = idesc_bf16_f32<128, 16>();
+      for (int it = 0; it < ntiles; ++it) {
+        const int s = it % STAGES, f = it & 1;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        if (lane == 0) trace(p, it, 14);
+        mbar_wait(&fempty[f], ((it >> 1) & 1) ^ 1);
+        if (lane == 0) trace(p, it, 15);
         tc_fence_after();
-        const uint32_t d = tmem_base + u * NCH;
-        const uint32_t ua = smem_u32(smem + OFF_U + u * U_BYTES);
-        const uint32_t upa = smem_u32(smem + OFF_UP + u * U_BYTES);
+        const uint32_t st = smem_u32(smem + LY::OFF_ST + s * LY::STAGE_BYTES);
+        const uint32_t fm = st + 2 * KV_BYTES + Q_BYTES;
+        const uint32_t dfe = tmem_base + TM_FEAT + f * TM_FEAT_STRIDE;
+        const uint32_t w0 = 2 * (HALO - 8 * KS);  // byte offset of window 0
 #pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          mma_bf16(d, desc_sw128(t0a + ao), desc_sw128(ua + bo), idesc, ks > 0 ? 1u : 0u);
-        }
+        for (int tensor = 0; tensor < 3; ++tensor) {
+          if (tensor == 0 && !GQ) continue;
+          if (tensor == 1 && !GK) continue;
+          const uint32_t buf = tensor == 0 ? st + 2 * KV_BYTES : st + (tensor == 1 ? 0 : KV_BYTES);
+          const int nmb = tensor == 0 ? Q_MB : KV_MB;
+          const uint32_t dcol = tensor == 0 ? TM_Q : tensor == 1 ? TM_K : TM_V;
+          for (int b = 0; b < nmb; ++b) {
 #pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          mma_bf16(d, desc_sw128(t1a + ao), desc_sw128(upa + bo), idesc, 1u);
+            for (int ks = 0; ks < KS; ++ks) {
+              const uint64_t ad = desc_noswz(buf + w0 + b * 2048 + ks * 32, 16, 128);
+              const uint64_t bd = desc_noswz(fm + (tensor * KS + ks) * F_BYTES, 128, 256);
+              if (elect_one()) mma_bf16(dfe + dcol + b * 16, ad, bd, idesc_feat, ks > 0 ? 1u : 0u);
+              __syncwarp();
+            }
+          }
         }
-        mma_commit(&uempty[u]);
-        mma_commit(&tfull[u]);
+        if (elect_one()) {
+          mma_commit(&empty[s]);
+          mma_commit(&ffull[f]);
+          trace(p, it, 13);
+        }
+        __syncwarp();
       }
     }
     __syncwarp();
-  } else if (warp < W_EPI0) {
-    // ------------------------------------------------------------ converters
-    const int ctid = threadIdx.x - W_CONV0 * 32;
-    float2 hkv[LHF], hqq[LHF];  // (k, v) and (q, q) featurizer taps on f32x2 lanes
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------------ main MMA issuer
+    {
+      constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
+      const uint32_t t0a = smem_u32(smem + LY::OFF_T0), t1a = smem_u32(smem + LY::OFF_T1);
+      int gi = -1, g_prev = -1;
+      Tile t;
+      t.init(tb, p);
+      for (int j = 0; j < ntiles; ++j, t.next(p)) {
+        const int u = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        const int g = t.c / p.gs;
+        const bool first = g != g_prev;
+        const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
+        if (first) ++gi;
+        g_prev = g;
+        mbar_wait(&ufull[u], ph);
+        mbar_wait(&tempty[u], ph ^ 1);
+        if (lane == 0) trace(p, j, 4);
+        if (first) mbar_wait(&tready[0], gi & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + TM_ACC + u * NCH;
+        const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
+        const uint32_t upa = smem_u32(smem + LY::OFF_UP + u * NCH * LB * 2);
 #pragma unroll
-    for (int i = 0; i < LHF; ++i) hkv[i] = hqq[i] = make_float2(i == 0 ? 1.f : 0.f, i == 0 ? 1.f : 0.f);
-    int cur_g = -1, cur_c = -1;
-    int it = 0;
-    for (int tile = tb; tile < te; ++tile, ++it) {
-      const int s = it % STAGES;
-      const int u = it & 1;
-      const Tile t = decode(tile, p);
-      const int g = t.c / p.gs;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      mbar_wait(&uempty[u], ((it >> 1) & 1) ^ 1);
-      if (g != cur_g) {
-        // all MMAs reading the old factors must be done before they are overwritten
-        if (it > 0) mbar_wait(&tfull[u ^ 1], ((it - 1) >> 1) & 1);
-        for (int i = ctid; i < 512; i += CONV_THREADS) {
-          const int tt = i - 128;
-          float h = 0.f;
-          if (tt >= 0 && tt < p.lh) {
-            h = p.taps_hat[static_cast<size_t>(g) * p.lh + tt];
-            if (p.decay) h *= exp2f(-p.decay[g] * static_cast<float>(tt));
-          }
-          hpad[i] = __float2bfloat16_rn(h);
+        for (int ks = 0; ks < LB / 16; ++ks) {
+          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
+          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+          if (elect_one()) mma_bf16(d, desc_sw128(t0a + ao), desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+          __syncwarp();
         }
-        named_bar_sync(BAR_CONV, CONV_THREADS);
-        // T_f[m][k] = h[f*128 + m - k]: unit (f, m, j) holds k = 8j .. 8j+7
-        for (int i = ctid; i < 2 * LB * 16; i += CONV_THREADS) {
-          const int f = i / (LB * 16), m = (i / 16) % LB, j = i % 16;
-          const bf16* src = hpad + 128 + f * 128 + m - 8 * j;
-          int4 raw;
-          bf16* e = reinterpret_cast<bf16*>(&raw);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) e[q] = src[-q];
-          *reinterpret_cast<int4*>(smem + (f ? OFF_T1 : OFF_T0) + sw128_off(m, j, LB)) = raw;
+        if (last && elect_one()) mma_commit(&tfree[0]);
+        __syncwarp();
+        if (first) {
+          mbar_wait(&tready[1], gi & 1);
+          tc_fence_after();
         }
-        cur_g = g;
-      }
-      if (FEAT && t.c != cur_c) {
 #pragma unroll
-        for (int i = 0; i < LHF; ++i) {
-          const bool ok = i < p.lhf;
-          const float hq = ok ? p.feat_taps[(static_cast<size_t>(0) * p.C + t.c) * p.lhf + i] : 0.f;
-          const float hk = ok ? p.feat_taps[(static_cast<size_t>(1) * p.C + t.c) * p.lhf + i] : 0.f;
-          const float hv = ok ? p.feat_taps[(static_cast<size_t>(2) * p.C + t.c) * p.lhf + i] : 0.f;
-          hkv[i] = make_float2(hk, hv);
-          hqq[i] = make_float2(hq, hq);
+        for (int ks = 0; ks < LB / 16; ++ks) {
+          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
+          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+          if (elect_one()) mma_bf16(d, desc_sw128(t1a + ao), desc_sw128(upa + bo), idesc_main, 1u);
+          __syncwarp();
         }
-        cur_c = t.c;
-      }
-      const bf16* kbuf = reinterpret_cast<const bf16*>(smem + OFF_ST + s * STAGE_BYTES);
-      const bf16* vbuf = kbuf + KV_BYTES / 2;
-      const bf16* qbuf = vbuf + KV_BYTES / 2;
-      unsigned char* ub = smem + OFF_U + u * U_BYTES;
-      unsigned char* upb = smem + OFF_UP + u * U_BYTES;
-      // u = k * v for chunks n = -1 .. NCH-1 (chunk -1 only feeds U_prev row 0)
-      for (int i = ctid; i < (NCH + 1) * 16; i += CONV_THREADS) {
-        const int n = i / 16 - 1, j = i % 16;
-        const int idx = (n + 1) * LB + HALO + 8 * j;
-        float uv[8];
-        if (FEAT) {
-          float2 r[24], acc[8];
-          load_raw_pair<LHF>(kbuf, vbuf, idx, idx, r);
-          fir8x2<LHF>(r, hkv, acc);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) uv[e] = acc[e].x * acc[e].y;
-        } else {
-          unpack8(*reinterpret_cast<const int4*>(vbuf + idx), uv);
-          if (GK) {
-            float kv[8];
-            unpack8(*reinterpret_cast<const int4*>(kbuf + idx), kv);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) uv[e] *= kv[e];
-          }
+        if (elect_one()) {
+          if (last) mma_commit(&tfree[1]);
+          mma_commit(&uempty[u]);
+          mma_commit(&tfull[u]);
         }
-        const int4 packed = pack8(uv);
-        if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
-        if (n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
-      }
-      if (GQ) {
-        float* fq = reinterpret_cast<float*>(smem + OFF_FQ + u * FQ_BYTES);
-        constexpr int NQ = NCH * 16, HQ = NQ / 2;  // q units, processed in pairs (i, i + HQ)
-        for (int i = ctid; i < HQ; i += CONV_THREADS) {
-          // unit i -> time 8i (= chunk n*128 + 8j with i = n*16 + j)
-          const int ia = HALO + 8 * i, ib = HALO + 8 * (i + HQ);
-          float2 o[8];
-          if (FEAT) {
-            float2 r[24];
-            load_raw_pair<LHF>(qbuf, qbuf, ia, ib, r);
-            fir8x2<LHF>(r, hqq, o);
-          } else {
-            float2 r[8];
-            unpack8_pair(*reinterpret_cast<const int4*>(qbuf + ia), *reinterpret_cast<const int4*>(qbuf + ib), r);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = r[e];
-          }
-          *reinterpret_cast<float4*>(fq + 8 * i) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
-          *reinterpret_cast<float4*>(fq + 8 * i + 4) = make_float4(o[4].x, o[5].x, o[6].x, o[7].x);
-          *reinterpret_cast<float4*>(fq + 8 * (i + HQ)) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
-          *reinterpret_cast<float4*>(fq + 8 * (i + HQ) + 4) = make_float4(o[4].y, o[5].y, o[6].y, o[7].y);
-        }
-      }
-      fence_proxy_async();
-      named_bar_sync(BAR_CONV, CONV_THREADS);
-      if (ctid == 0) {
-        mbar_arrive(&ufull[u]);
-        mbar_arrive(&empty[s]);
+        __syncwarp();
       }
     }
-  } else {
+    __syncwarp();
+  } else if (warp >= W_CONV0 && warp < W_EPI0) {
+    // ------------------------------------------------------------ converters
+    const int ctid = threadIdx.x - W_CONV0 * 32;
+    const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - W_CONV0) >> 2;       // two warps per quarter split the M-blocks
+    const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    for (int it = 0; it < ntiles; ++it) {
+      const int f = it & 1, u = it & 1;
+      mbar_wait(&ffull[f], (it >> 1) & 1);
+      if (ctid == 0) trace(p, it, 1);
+      mbar_wait(&uempty[u], ((it >> 1) & 1) ^ 1);
+      if (ctid == 0) trace(p, it, 2);
+      tc_fence_after();
+      const uint32_t tf = tmem_base + lane_addr + TM_FEAT + f * TM_FEAT_STRIDE;
+      unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
+      unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
+      // u = k * v: window m holds times t0 - 128 + 8m .. +7  ->  chunk m/16 - 1, unit m%16
+      for (int b = half; b < KV_MB; b += 2) {
+        const int m0 = b * 128 + quarter * 32;
+        if (m0 >= KV_WIN) continue;  // warp-uniform
+        uint32_t rv[8], rk[8];
+        tmem_ld8(tf + TM_V + b * 16, rv);
+        if (GK) tmem_ld8(tf + TM_K + b * 16, rk);
+        tmem_wait_ld();
+        const int m = m0 + lane;
+        if (m < KV_WIN) {
+          float uv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            uv[e] = GK ? __uint_as_float(rv[e]) * __uint_as_float(rk[e]) : __uint_as_float(rv[e]);
+          const int4 packed = pack8(uv);
+          const int n = m / 16 - 1, j = m % 16;
+          if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
+          if (n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
+        }
+      }
+      // U is complete: hand it to the MMA before the featurized q is written
+      fence_proxy_async();
+      named_bar_sync(BAR_CONV, CONV_THREADS);
+      if (ctid == 0) mbar_arrive(&ufull[u]);
+      if (GQ) {
+        mbar_wait(&qempty[u], ((it >> 1) & 1) ^ 1);
+        bf16* fq = reinterpret_cast<bf16*>(smem + LY::OFF_FQ + u * NCH * LB * 2);
+        for (int b = half; b < Q_MB; b += 2) {
+          uint32_t rq[8];
+          tmem_ld8(tf + TM_Q + b * 16, rq);
+          tmem_wait_ld();
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(rq[e]);
+          const int m = b * 128 + quarter * 32 + lane;  // times t0 + 8m .. +7
+          *reinterpret_cast<int4*>(fq + 8 * m) = pack8(o);
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(BAR_CONV, CONV_THREADS);
+      if (ctid == 0) {
+        trace(p, it, 3);
+        mbar_arrive(&fempty[f]);
+        mbar_arrive(&qfull[u]);
+      }
+    }
+  } else if (warp >= W_EPI0 && warp < W_TB0) {
     // ------------------------------------------------------------ epilogue
-    const int etid = threadIdx.x - W_EPI0 * 32;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int tout = quarter * 32 + lane;
-    int it = 0;
-    for (int tile = tb; tile < te; ++tile, ++it) {
+    Tile t;
+    t.init(tb, p);
+    for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int a = it & 1;
-      const Tile t = decode(tile, p);
       mbar_wait(&tfull[a], (it >> 1) & 1);
+      if (quarter == 0 && lane == 0) trace(p, it, 5);
       tc_fence_after();
       float acc[NCH];
-      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + a * NCH, acc);
+      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + TM_ACC + a * NCH, acc);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
-      if (etid == 0 && it >= 2) bulk_wait_read<1>();
-      named_bar_sync(BAR_EPI, EPI_THREADS);
-      bf16* yb = reinterpret_cast<bf16*>(smem + OFF_Y + a * Y_BYTES);
-      const float* fq = reinterpret_cast<const float*>(smem + OFF_FQ + a * FQ_BYTES);
+      if (GQ) mbar_wait(&qfull[a], (it >> 1) & 1);
+      const bf16* fq = reinterpret_cast<const bf16*>(smem + LY::OFF_FQ + a * NCH * LB * 2);
+      bf16* yrow = p.y + (static_cast<size_t>(t.b) * p.C + t.c) * p.L + t.t0;
+      const int nt = min(TILE_T, p.L - t.t0);
 #pragma unroll
       for (int n = 0; n < NCH; ++n) {
+        const int tt = n * LB + tout;
         float val = acc[n];
-        if (GQ) val *= fq[n * LB + tout];
-        yb[n * LB + tout] = __float2bfloat16_rn(val);
+        if (GQ) val *= __bfloat162float(fq[tt]);
+        if (tt < nt) yrow[tt] = __float2bfloat16_rn(val);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&uempty[a]);
-      fence_proxy_async();
-      named_bar_sync(BAR_EPI, EPI_THREADS);
-      if (etid == 0) {
-        const int nt = min(TILE_T, p.L - t.t0);
-        bf16* dst = p.y + (static_cast<size_t>(t.b) * p.C + t.c) * p.L + t.t0;
-        bulk_s2g(dst, yb, static_cast<uint32_t>(nt) * 2);
-        bulk_commit();
-      }
+      if (lane == 0) mbar_arrive(&qempty[a]);
+      if (quarter == 0 && lane == 0) trace(p, it, 6);
     }
-    if (etid == 0) bulk_wait<0>();
+  } else if (warp >= W_TB0 && warp < W_FMMA) {
+    // ------------------------------------------------------------ Toeplitz factor builder
+    const int bt = threadIdx.x - W_TB0 * 32;
+    constexpr int PER = 512 / TB_THREADS;  // hpad entries per thread
+    float pf_h[PER], pf_dec = 0.f;
+    // raw loads of a group's taps; the decay is applied at use so the loads stay in flight
+    auto prefetch = [&](int g) {
+      pf_dec = p.decay ? p.decay[g] : 0.f;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int tt = bt + r * TB_THREADS - 128;
+        pf_h[r] = (tt >= 0 && tt < p.lh) ? p.taps_hat[static_cast<size_t>(g) * p.lh + tt] : 0.f;
+      }
+    };
+    // one factor: unit (m, j) of T_f = [h[f*128+d], .., h[f*128+d-7]] with d = m - 8j;
+    // each thread builds the 16-byte vector of one diagonal d and stores it along it
+    auto build = [&](int fct) {
+      unsigned char* tbase = smem + (fct ? LY::OFF_T1 : LY::OFF_T0);
+      for (int i = bt; i < 248; i += TB_THREADS) {
+        const int d = i - 120;
+        const bf16* src = hpad + 128 + fct * 128 + d;
+        int4 raw;
+        bf16* e = reinterpret_cast<bf16*>(&raw);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) e[q] = src[-q];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = d + 8 * j;
+          if (m >= 0 && m < LB) *reinterpret_cast<int4*>(tbase + sw128_off(m, j, LB)) = raw;
+        }
+      }
+      fence_proxy_async();
+      named_bar_sync(BAR_TB, TB_THREADS);
+      if (bt == 0) mbar_arrive(&tready[fct]);
+    };
+    int gi = 0, g_prev = -1;
+    Tile t;
+    t.init(tb, p);
+    const int g_end = ntiles > 0 ? ((te - 1) / (p.tiles_per_seq * p.B)) / p.gs : -1;  // last group
+    if (ntiles > 0) prefetch(t.c / p.gs);
+    for (int j = 0; j < ntiles; ++j, t.next(p)) {
+      const int g = t.c / p.gs;
+      if (g == g_prev) continue;
+      g_prev = g;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int tt = bt + r * TB_THREADS - 128;
+        const float h = (tt >= 0 && tt < p.lh) ? pf_h[r] * exp2f(-pf_dec * static_cast<float>(tt)) : 0.f;
+        hpad[bt + r * TB_THREADS] = __float2bfloat16_rn(h);
+      }
+      named_bar_sync(BAR_TB, TB_THREADS);
+      if (gi > 0) mbar_wait(&tfree[0], (gi - 1) & 1);
+      build(0);
+      if (gi > 0) mbar_wait(&tfree[1], (gi - 1) & 1);
+      build(1);
+      if (g < g_end) prefetch(g + 1);  // next group's taps load during this group
+      ++gi;
+    }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == W_MMA) tmem_dealloc<2 * NCH>(tmem_base);
+  if (warp == W_MMA) tmem_dealloc<512>(tmem_base);
 }
 
-template <bool FEAT, bool GK, bool GQ, int LHF, int CW>
-static int launch_cw(const Params& p, cudaStream_t st) {
-  auto kern = two_stage_kernel<FEAT, GK, GQ, LHF, CW>;
+template <bool FEAT, bool GK, bool GQ, int KS>
+static int launch_ks(const Params& p, cudaStream_t st) {
+  auto kern = two_stage_kernel<FEAT, GK, GQ, KS>;
+  constexpr int smem = Layout<KS>::SMEM_BYTES;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
@@ -456,23 +605,16 @@ static int launch_cw(const Params& p, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = p.total_tiles < sms ? p.total_tiles : sms;
-  kern<<<grid, Roles<CW>::THREADS, SMEM_BYTES, st>>>(p);
+  kern<<<grid, THREADS, smem, st>>>(p);
   return check_launch("two_stage_kernel");
 }
 
-// Converter warp count: 8 (default) or 12 (HY_TS_CONV_WARPS=12), for tuning.
-static int conv_warps() {
-  static int cw = [] {
-    const char* e = getenv("HY_TS_CONV_WARPS");
-    return (e && atoi(e) == 12) ? 12 : 8;
-  }();
-  return cw;
-}
-
-template <bool FEAT, bool GK, bool GQ, int LHF>
-static int launch(const Params& p, cudaStream_t st) {
-  if (conv_warps() == 12) return launch_cw<FEAT, GK, GQ, LHF, 12>(p, st);
-  return launch_cw<FEAT, GK, GQ, LHF, 8>(p, st);
+template <bool FEAT, bool GK, bool GQ>
+static int launch(Params p, cudaStream_t st) {
+  static const int tr = [] { const char* e = getenv("HY_TS_TRACE"); return e ? atoi(e) : 0; }();
+  p.trace = tr;
+  if (p.lhf <= 9) return launch_ks<FEAT, GK, GQ, 1>(p, st);
+  return launch_ks<FEAT, GK, GQ, 2>(p, st);
 }
 
 int check_shapes(int B, int C, int L, int lh, int gs) {
@@ -510,15 +652,15 @@ extern "C" int hy_two_stage_fwd(const void* q, const void* k, const void* v, voi
   p.tiles_per_seq = (L + ts::TILE_T - 1) / ts::TILE_T;
   p.total_tiles = p.tiles_per_seq * B * C;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (q && k) return ts::launch<false, true, true, 1>(p, st);
-  if (k) return ts::launch<false, true, false, 1>(p, st);
-  if (q) return ts::launch<false, false, true, 1>(p, st);
-  return ts::launch<false, false, false, 1>(p, st);
+  if (q && k) return ts::launch<false, true, true>(p, st);
+  if (k) return ts::launch<false, true, false>(p, st);
+  if (q) return ts::launch<false, false, true>(p, st);
+  return ts::launch<false, false, false>(p, st);
 }
 
 // Fused MR mixer (bf16): featurizers + gates + two-stage conv in one pass.
 int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const float* taps_hat,
-                    const float* decay, int lh, int gs, int B, int C, int L, void* stream) {
+                     const float* decay, int lh, int gs, int B, int C, int L, void* stream) {
   int s = ts::check_shapes(B, C, L, lh, gs);
   if (s != HY_OK) return s;
   if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
@@ -532,7 +674,12 @@ int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf,
   p.B = B, p.C = C, p.L = L, p.lh = lh, p.gs = gs, p.lhf = lhf;
   p.tiles_per_seq = (L + ts::TILE_T - 1) / ts::TILE_T;
   p.total_tiles = p.tiles_per_seq * B * C;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (lhf <= 8) return ts::launch<true, true, true, 8>(p, st);
-  return ts::launch<true, true, true, 16>(p, st);
+  return ts::launch<true, true, true>(p, static_cast<cudaStream_t>(stream));
+}
+
+// Debug: copy the CTA-0 timeline of the last traced two-stage launch (HY_TS_TRACE=1).
+extern "C" HY_API int hy_debug_two_stage_trace(unsigned long long* host_out, int n) {
+  if (n > ts::TRACE_TILES * ts::TRACE_EV) n = ts::TRACE_TILES * ts::TRACE_EV;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, ts::g_trace, n * sizeof(unsigned long long));
+  return e == cudaSuccess ? HY_OK : fail(HY_ERR_CUDA, "trace copy: %s", cudaGetErrorString(e));
 }

@@ -1,0 +1,1 @@
+python scripts/trace_ts.py mixer; python scripts/trace_ts.py gated
