@@ -67,11 +67,12 @@ constexpr int THREADS = (W_PROD + 1) * 32;
 constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
 constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
 
-// TMEM columns (512 allocated): main accumulators [2] x 32, featurizer buffers [2] x 224
-constexpr uint32_t TM_ACC = 0, TM_FEAT = 2 * NCH, TM_FEAT_STRIDE = 224;
+// TMEM columns (512 allocated): main accumulators [2] x 32, Toeplitz factors T0 / T1
+// (A operand of the main MMA, 128 lanes x 64 columns of packed bf16 pairs each), one
+// featurizer buffer (k / v / q outputs; drained to registers right after it lands).
+constexpr uint32_t TM_ACC = 0, TM_T0 = 2 * NCH, TM_T1 = TM_T0 + 64, TM_FEAT = TM_T1 + 64;
 constexpr uint32_t TM_K = 0, TM_V = 16 * KV_MB, TM_Q = 32 * KV_MB;
-static_assert(TM_Q + 16 * Q_MB <= TM_FEAT_STRIDE, "feat TMEM layout");
-static_assert(TM_FEAT + 2 * TM_FEAT_STRIDE <= 512, "TMEM budget");
+static_assert(TM_FEAT + TM_Q + 16 * Q_MB <= 512, "TMEM budget");
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
 constexpr int KV_BYTES = round_up(KV_LEN * 2, 128);
@@ -79,13 +80,11 @@ constexpr int Q_BYTES = round_up(Q_LEN * 2, 128);
 constexpr int F_BYTES = 512;  // one 16x16 bf16 featurizer matrix (no-swizzle K-major)
 template <int KS>
 struct Layout {
-  static constexpr int STAGES = KS == 1 ? 4 : 3;
+  static constexpr int STAGES = 6;
   static constexpr int F_SET = 3 * KS * F_BYTES;  // q, k, v featurizer matrices
   static constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES + F_SET;
   static constexpr int OFF_ST = 0;  // stages first: window over-reads stay inside SMEM
-  static constexpr int OFF_T0 = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);
-  static constexpr int OFF_T1 = OFF_T0 + LB * LB * 2;
-  static constexpr int OFF_U = OFF_T1 + LB * LB * 2;        // U[2]
+  static constexpr int OFF_U = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);  // U[2]
   static constexpr int OFF_UP = OFF_U + 2 * NCH * LB * 2;   // U_prev[2]
   static constexpr int OFF_FQ = OFF_UP + 2 * NCH * LB * 2;  // featurized q, bf16 [2]
   static constexpr int OFF_HP = OFF_FQ + 2 * NCH * LB * 2;  // padded taps, bf16 [512]
@@ -192,8 +191,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LY::OFF_BAR);
   uint64_t* full = bars;                 // [STAGES] producer -> MMA
   uint64_t* empty = bars + STAGES;       // [STAGES] MMA commit (featurizer done) -> producer
-  uint64_t* ffull = bars + 2 * STAGES;   // [2] MMA commit -> converter (featurized in TMEM)
-  uint64_t* fempty = ffull + 2;          // [2] converter -> MMA (feat TMEM drained)
+  uint64_t* ffull = bars + 2 * STAGES;   // [1] MMA commit -> converter (featurized in TMEM)
+  uint64_t* fempty = ffull + 2;          // [1] converter warps -> MMA (feat TMEM drained)
   uint64_t* ufull = ffull + 4;           // [2] converter -> MMA
   uint64_t* uempty = ffull + 6;          // [2] MMA commit (U / U_prev read) -> converter
   uint64_t* tfull = ffull + 8;           // [2] MMA commit -> epilogue
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ffull[i], 1);
-      mbar_init(&fempty[i], 1);
+      mbar_init(&fempty[i], N_CONV_WARPS);
       mbar_init(&ufull[i], 1);
       mbar_init(&uempty[i], 1);
       mbar_init(&qfull[i], 1);
@@ -343,15 +342,15 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     {
       constexpr uint32_t idesc_feat = idesc_bf16_f32<128, 16>();
       for (int it = 0; it < ntiles; ++it) {
-        const int s = it % STAGES, f = it & 1;
+        const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         if (lane == 0) trace(p, it, 14);
-        mbar_wait(&fempty[f], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&fempty[0], (it & 1) ^ 1);
         if (lane == 0) trace(p, it, 15);
         tc_fence_after();
         const uint32_t st = smem_u32(smem + LY::OFF_ST + s * LY::STAGE_BYTES);
         const uint32_t fm = st + 2 * KV_BYTES + Q_BYTES;
-        const uint32_t dfe = tmem_base + TM_FEAT + f * TM_FEAT_STRIDE;
+        const uint32_t dfe = tmem_base + TM_FEAT;
         const uint32_t w0 = 2 * (HALO - 8 * KS);  // byte offset of window 0
 #pragma unroll
         for (int tensor = 0; tensor < 3; ++tensor) {
@@ -372,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         }
         if (elect_one()) {
           mma_commit(&empty[s]);
-          mma_commit(&ffull[f]);
+          mma_commit(&ffull[0]);
           trace(p, it, 13);
         }
         __syncwarp();
@@ -383,7 +382,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     // ------------------------------------------------------------ main MMA issuer
     {
       constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
-      const uint32_t t0a = smem_u32(smem + LY::OFF_T0), t1a = smem_u32(smem + LY::OFF_T1);
+      const uint32_t t0a = tmem_base + TM_T0, t1a = tmem_base + TM_T1;
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -405,9 +404,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         const uint32_t upa = smem_u32(smem + LY::OFF_UP + u * NCH * LB * 2);
 #pragma unroll
         for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
           const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          if (elect_one()) mma_bf16(d, desc_sw128(t0a + ao), desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+          if (elect_one()) mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           __syncwarp();
         }
         if (last && elect_one()) mma_commit(&tfree[0]);
@@ -418,9 +416,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         }
 #pragma unroll
         for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t ao = (ks >> 2) * (LB * 128) + (ks & 3) * 32;
           const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          if (elect_one()) mma_bf16(d, desc_sw128(t1a + ao), desc_sw128(upa + bo), idesc_main, 1u);
+          if (elect_one()) mma_bf16_ts(d, t1a + ks * 8, desc_sw128(upa + bo), idesc_main, 1u);
           __syncwarp();
         }
         if (elect_one()) {
@@ -438,61 +435,73 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - W_CONV0) >> 2;       // two warps per quarter split the M-blocks
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    // M-blocks of this warp: k / v blocks half, half+2, half+4; q blocks half, half+2
+    constexpr int KVB_PER = (KV_MB + 1) / 2, QB_PER = Q_MB / 2;
     for (int it = 0; it < ntiles; ++it) {
-      const int f = it & 1, u = it & 1;
-      mbar_wait(&ffull[f], (it >> 1) & 1);
+      const int u = it & 1;
+      // 1) drain the featurized k / v / q of this tile from TMEM into registers and
+      //    release the single featurizer buffer for the next tile's MMAs at once
+      mbar_wait(&ffull[0], it & 1);
       if (ctid == 0) trace(p, it, 1);
+      tc_fence_after();
+      const uint32_t tf = tmem_base + lane_addr + TM_FEAT;
+      uint32_t rv[KVB_PER][8], rk[KVB_PER][8], rq[QB_PER][8];
+#pragma unroll
+      for (int i = 0; i < KVB_PER; ++i) {
+        const int b = half + 2 * i;
+        if (b < KV_MB && b * 128 + quarter * 32 < KV_WIN) {  // warp-uniform
+          tmem_ld8(tf + TM_V + b * 16, rv[i]);
+          if (GK) tmem_ld8(tf + TM_K + b * 16, rk[i]);
+        }
+      }
+      if (GQ) {
+#pragma unroll
+        for (int i = 0; i < QB_PER; ++i) tmem_ld8(tf + TM_Q + (half + 2 * i) * 16, rq[i]);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fempty[0]);
+      // 2) u = k * v -> U / U_prev: window m holds times t0 - 128 + 8m .. +7, i.e. chunk
+      //    m/16 - 1, 16-byte unit m%16
       mbar_wait(&uempty[u], ((it >> 1) & 1) ^ 1);
       if (ctid == 0) trace(p, it, 2);
-      tc_fence_after();
-      const uint32_t tf = tmem_base + lane_addr + TM_FEAT + f * TM_FEAT_STRIDE;
       unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
       unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
-      // u = k * v: window m holds times t0 - 128 + 8m .. +7  ->  chunk m/16 - 1, unit m%16
-      for (int b = half; b < KV_MB; b += 2) {
-        const int m0 = b * 128 + quarter * 32;
-        if (m0 >= KV_WIN) continue;  // warp-uniform
-        uint32_t rv[8], rk[8];
-        tmem_ld8(tf + TM_V + b * 16, rv);
-        if (GK) tmem_ld8(tf + TM_K + b * 16, rk);
-        tmem_wait_ld();
-        const int m = m0 + lane;
-        if (m < KV_WIN) {
+#pragma unroll
+      for (int i = 0; i < KVB_PER; ++i) {
+        const int b = half + 2 * i;
+        const int m = b * 128 + quarter * 32 + lane;
+        if (b < KV_MB && m < KV_WIN) {
           float uv[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            uv[e] = GK ? __uint_as_float(rv[e]) * __uint_as_float(rk[e]) : __uint_as_float(rv[e]);
+            uv[e] = GK ? __uint_as_float(rv[i][e]) * __uint_as_float(rk[i][e]) : __uint_as_float(rv[i][e]);
           const int4 packed = pack8(uv);
           const int n = m / 16 - 1, j = m % 16;
           if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
           if (n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
         }
       }
-      // U is complete: hand it to the MMA before the featurized q is written
       fence_proxy_async();
       named_bar_sync(BAR_CONV, CONV_THREADS);
       if (ctid == 0) mbar_arrive(&ufull[u]);
+      // 3) featurized q -> SMEM for the epilogue (times t0 + 8m .. +7)
       if (GQ) {
         mbar_wait(&qempty[u], ((it >> 1) & 1) ^ 1);
         bf16* fq = reinterpret_cast<bf16*>(smem + LY::OFF_FQ + u * NCH * LB * 2);
-        for (int b = half; b < Q_MB; b += 2) {
-          uint32_t rq[8];
-          tmem_ld8(tf + TM_Q + b * 16, rq);
-          tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < QB_PER; ++i) {
           float o[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(rq[e]);
-          const int m = b * 128 + quarter * 32 + lane;  // times t0 + 8m .. +7
+          for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(rq[i][e]);
+          const int m = (half + 2 * i) * 128 + quarter * 32 + lane;
           *reinterpret_cast<int4*>(fq + 8 * m) = pack8(o);
         }
+        named_bar_sync(BAR_CONV, CONV_THREADS);
+        if (ctid == 0) mbar_arrive(&qfull[u]);
       }
-      tc_fence_before();
-      named_bar_sync(BAR_CONV, CONV_THREADS);
-      if (ctid == 0) {
-        trace(p, it, 3);
-        mbar_arrive(&fempty[f]);
-        mbar_arrive(&qfull[u]);
-      }
+      if (ctid == 0) trace(p, it, 3);
     }
   } else if (warp >= W_EPI0 && warp < W_TB0) {
     // ------------------------------------------------------------ epilogue
@@ -539,24 +548,25 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         pf_h[r] = (tt >= 0 && tt < p.lh) ? p.taps_hat[static_cast<size_t>(g) * p.lh + tt] : 0.f;
       }
     };
-    // one factor: unit (m, j) of T_f = [h[f*128+d], .., h[f*128+d-7]] with d = m - 8j;
-    // each thread builds the 16-byte vector of one diagonal d and stores it along it
+    // one factor into TMEM as the A operand of the main MMA: lane m = output row, column c
+    // = packed bf16 pair (T_f[m][2c], T_f[m][2c+1]) = (h[f*128 + m - 2c], h[f*128 + m - 2c - 1])
+    const int quarter = warp & 3;
+    const int mrow = quarter * 32 + lane;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
     auto build = [&](int fct) {
-      unsigned char* tbase = smem + (fct ? LY::OFF_T1 : LY::OFF_T0);
-      for (int i = bt; i < 248; i += TB_THREADS) {
-        const int d = i - 120;
-        const bf16* src = hpad + 128 + fct * 128 + d;
-        int4 raw;
-        bf16* e = reinterpret_cast<bf16*>(&raw);
+      const unsigned short* hp = reinterpret_cast<const unsigned short*>(hpad) + 128 + fct * 128 + mrow;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) e[q] = src[-q];
+      for (int half = 0; half < 2; ++half) {
+        uint32_t w[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = d + 8 * j;
-          if (m >= 0 && m < LB) *reinterpret_cast<int4*>(tbase + sw128_off(m, j, LB)) = raw;
+        for (int c = 0; c < 32; ++c) {
+          const int cc = half * 32 + c;
+          w[c] = static_cast<uint32_t>(hp[-2 * cc]) | (static_cast<uint32_t>(hp[-2 * cc - 1]) << 16);
         }
+        tmem_st_32x32b_x32(trow + (fct ? TM_T1 : TM_T0) + half * 32, w);
       }
-      fence_proxy_async();
+      tmem_wait_st();
+      tc_fence_before();
       named_bar_sync(BAR_TB, TB_THREADS);
       if (bt == 0) mbar_arrive(&tready[fct]);
     };
