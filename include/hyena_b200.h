@@ -78,14 +78,21 @@ HY_API int hy_two_stage_fwd(const void* q, const void* k, const void* v, void* y
                      const float* taps_hat, const float* decay,
                      int B, int C, int L, int lh, int group_size, int dtype, void* stream);
 
+/* Featurizer taps packed once per parameter set for the tcgen05 mixer: per channel the
+ * q / k / v banded matrices F[n][k] = h[8*KS + n - k] (KS = 1 for lhf <= 9, else 2) in the
+ * core-matrix order the featurizer MMAs read. out: hy_feat_pack_size() bytes of device memory. */
+HY_API size_t hy_feat_pack_size(int C, int lhf);
+HY_API int hy_feat_pack(const float* feat_taps, int C, int lhf, void* out, void* stream);
+
 /* Fused Hyena mixer (everything between the projections):
  *   proj: (B, 3C, L) = [W_q^T x ; W_k^T x ; W_v^T x] per batch element
  *   q,k,v = featurizer FIRs (feat_taps: (3, C, lhf) per CHANNEL, zero padded)
  *   y = q * inner(k * v)     (inner taps per group, optional decay as above)
- * SE (lh <= 14): CUDA-core kernel, fp32 or bf16. MR (bf16, lh <= 129): tcgen05.
+ * MR / SE in bf16 with lh <= 129 and feat_pack given: tcgen05 kernel (featurizers and the
+ * two-stage conv as MMAs). SE (lh <= 16) otherwise: CUDA-core kernel, fp32 or bf16.
  * HY_F64 and longer filters return HY_ERR_UNSUPPORTED (the host composes kernels). */
-HY_API int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,
-                       const void* inner_taps, const float* inner_decay, int lh, int group_size,
+HY_API int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, const void* feat_pack,
+                       int lhf, const void* inner_taps, const float* inner_decay, int lh, int group_size,
                        int B, int C, int L, int dtype, void* stream);
 
 /* SE mixer only (CUDA cores, fp32 / bf16, lh and lhf <= 16), same arguments. */

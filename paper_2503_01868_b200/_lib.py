@@ -27,7 +27,9 @@ SIGNATURES = {
     "hy_causal_conv_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_gated_conv_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_two_stage_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
-    "hy_hyena_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "hy_hyena_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "hy_feat_pack_size": (_SZ, [_I, _I]),
+    "hy_feat_pack": (_I, [_P, _I, _I, _P, _P]),
     "hy_se_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_fft_conv_workspace_size": (_SZ, [_I, _I, _I, _I, _I, _I]),
     "hy_fft_conv_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),

@@ -88,8 +88,7 @@ struct Layout {
   static constexpr int OFF_UP = OFF_U + 2 * NCH * LB * 2;   // U_prev[2]
   static constexpr int OFF_FQ = OFF_UP + 2 * NCH * LB * 2;  // featurized q, bf16 [2]
   static constexpr int OFF_HP = OFF_FQ + 2 * NCH * LB * 2;  // padded taps, bf16 [512]
-  static constexpr int OFF_FC = OFF_HP + 1024;               // F of the producer's channel
-  static constexpr int OFF_BAR = OFF_FC + F_SET;
+  static constexpr int OFF_BAR = OFF_HP + 1024;
   static constexpr int N_BARS = 2 * STAGES + 20;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
@@ -105,6 +104,7 @@ struct Params {
   const float* taps_hat;   // (n_groups, lh)
   const float* decay;      // (n_groups) rate*log2(base), or null
   const float* feat_taps;  // fused: (3, C, lhf), per channel
+  const bf16* fpack;       // fused: packed featurizer matrices, (C, 3, KS, 256) bf16, or null
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
@@ -239,29 +239,13 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     int stage_c[STAGES];
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) stage_c[s] = -1;
-    // featurizer taps (lane = tap index) of the current channel, and of the next channel
-    // already in flight: the global loads are issued one channel ahead of their use
-    float hl_cur[3], hl_nxt[3];
-    int cur_c = -1;
-    auto load_taps = [&](int c, float (&hl)[3]) {
-#pragma unroll
-      for (int tensor = 0; tensor < 3; ++tensor) {
-        if (FEAT)
-          hl[tensor] = lane < p.lhf ? p.feat_taps[(static_cast<size_t>(tensor) * p.C + c) * p.lhf + lane] : 0.f;
-        else
-          hl[tensor] = lane == 0 ? 1.f : 0.f;
-      }
-    };
     Tile t;
     t.init(tb, p);
-    if (ntiles > 0) load_taps(FEAT ? t.c : 0, hl_nxt);
-    const int c_end = ntiles > 0 ? (te - 1) / (p.tiles_per_seq * p.B) : -1;  // last channel in range
     for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int s = it % STAGES;
       if (lane == 0) trace(p, it, 12);
       mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
       if (lane == 0) trace(p, it, 0);
-      if (lane == 0) trace(p, it, 7);
       unsigned char* st = smem + LY::OFF_ST + s * LY::STAGE_BYTES;
       bf16* kbuf = reinterpret_cast<bf16*>(st);
       bf16* vbuf = reinterpret_cast<bf16*>(st + KV_BYTES);
@@ -271,68 +255,50 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       const int kvs = max(kws, 0), kve = min(kwe, p.L);
       const int qws = t.t0 - HALO, qwe = t.t0 + TILE_T;
       const int qvs = max(qws, 0), qve = min(qwe, p.L);
-      // zero the parts of the windows outside [0, L) (whole 8-element units)
-      const int4 z = make_int4(0, 0, 0, 0);
-      bool wrote = kvs != kws || kve != kwe || qvs != qws || qve != qwe;  // generic SMEM writes?
-      for (int i = lane * 8; i < kvs - kws; i += 256) {
-        *reinterpret_cast<int4*>(vbuf + i) = z;
-        if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
-      }
-      for (int i = (kve - kws) + lane * 8; i < KV_LEN; i += 256) {
-        *reinterpret_cast<int4*>(vbuf + i) = z;
-        if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
-      }
-      if (GQ) {
-        for (int i = lane * 8; i < qvs - qws; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
-        for (int i = (qve - qws) + lane * 8; i < Q_LEN; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
-      }
-      // featurizer matrices F[n][k] = h[8*KS + n - k] (n < 8), no-swizzle K-major:
-      // element (n, k) of K-step ks at (n%8)*16 + (n/8)*256 + (k%8)*2 + (k/8)*128 bytes.
-      // Taps come in with one load per lane (lane = tap index) and move by shuffles.
-      if (lane == 0) trace(p, it, 8);
-      const int want_c = FEAT ? t.c : 0;
-      if (want_c != cur_c) {
-        cur_c = want_c;
-#pragma unroll
-        for (int tensor = 0; tensor < 3; ++tensor) hl_cur[tensor] = hl_nxt[tensor];
-        if (FEAT && t.c < c_end) load_taps(t.c + 1, hl_nxt);
-        // F[n][k] = h[8*KS + n - k] (n < 8), no-swizzle K-major: element (n, k) of K-step
-        // ks at (n%8)*16 + (n/8)*256 + (k%8)*2 + (k/8)*128 bytes; taps move by shuffles.
-        bf16* fc = reinterpret_cast<bf16*>(smem + LY::OFF_FC);
-#pragma unroll
-        for (int tensor = 0; tensor < 3; ++tensor) {
-#pragma unroll 1
-          for (int r = 0; r < KS * 8; ++r) {
-            const int e = r * 32 + lane;  // 8*KS rounds of 32 lanes cover KS * 256 entries
-            const int ks = e / 256, n = (e / 16) % 16, kk = e % 16;
-            const int tap = 8 * KS + n - (16 * ks + kk);
-            const float hv = __shfl_sync(0xffffffffu, hl_cur[tensor], tap & 31);
-            const float h = (n < 8 && tap >= 0 && tap < MAX_LHF) ? hv : 0.f;
-            const int off = (n & 7) * 8 + (n >> 3) * 128 + (kk & 7) + (kk >> 3) * 64;
-            fc[(tensor * KS + ks) * 256 + off] = __float2bfloat16_rn(h);
-          }
+      bool wrote = false;  // generic-proxy SMEM writes to order before the async proxy
+      if (kvs != kws || kve != kwe || qvs != qws || qve != qwe) {
+        // zero the parts of the windows outside [0, L) (whole 8-element units)
+        const int4 z = make_int4(0, 0, 0, 0);
+        for (int i = lane * 8; i < kvs - kws; i += 256) {
+          *reinterpret_cast<int4*>(vbuf + i) = z;
+          if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
         }
-        __syncwarp();
-      }
-      if (stage_c[s] != want_c) {
-        // copy the channel's F set (built once per channel below) into the stage
-        const int4* src = reinterpret_cast<const int4*>(smem + LY::OFF_FC);
-        int4* dst = reinterpret_cast<int4*>(fmat);
-#pragma unroll
-        for (int i = lane; i < LY::F_SET / 16; i += 32) dst[i] = src[i];
-        stage_c[s] = want_c;
+        for (int i = (kve - kws) + lane * 8; i < KV_LEN; i += 256) {
+          *reinterpret_cast<int4*>(vbuf + i) = z;
+          if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
+        }
+        if (GQ) {
+          for (int i = lane * 8; i < qvs - qws; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
+          for (int i = (qve - qws) + lane * 8; i < Q_LEN; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
+        }
         wrote = true;
       }
-      if (lane == 0) trace(p, it, 9);
+      // featurizer matrices of this tile's channel: copied in from the packed table
+      // (FEAT), or the identity built in place once per stage (two_stage API)
+      const int want_c = FEAT ? t.c : 0;
+      const bool need_f = stage_c[s] != want_c;
+      stage_c[s] = want_c;
+      if (!FEAT && need_f) {
+        // F[n][k] = [8*KS + n - k == 0] (n < 8), no-swizzle K-major element (n, k) of K-step
+        // ks at (n%8)*16 + (n/8)*256 + (k%8)*2 + (k/8)*128 bytes
+        for (int e = lane; e < 3 * KS * 256; e += 32) {
+          const int ks = (e / 256) % KS, n = (e / 16) % 16, kk = e % 16;
+          const int off = (n & 7) * 8 + (n >> 3) * 128 + (kk & 7) + (kk >> 3) * 64;
+          fmat[(e / (KS * 256)) * KS * 256 + ks * 256 + off] =
+              __float2bfloat16_rn((n < 8 && 8 * KS + n == 16 * ks + kk) ? 1.f : 0.f);
+        }
+        wrote = true;
+      }
       if (wrote) fence_proxy_async();
       __syncwarp();
-      if (lane == 0) trace(p, it, 10);
       if (elect_one()) {
         const uint32_t kvb = static_cast<uint32_t>(kve - kvs) * 2, qb = static_cast<uint32_t>(qve - qvs) * 2;
-        mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0));
+        const uint32_t fb = (FEAT && need_f) ? static_cast<uint32_t>(LY::F_SET) : 0u;
+        mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0) + fb);
         bulk_g2s(vbuf + (kvs - kws), row_ptr<FEAT>(p, 2, t.b, t.c) + kvs, kvb, &full[s]);
         if (GK) bulk_g2s(kbuf + (kvs - kws), row_ptr<FEAT>(p, 1, t.b, t.c) + kvs, kvb, &full[s]);
         if (GQ) bulk_g2s(qbuf + (qvs - qws), row_ptr<FEAT>(p, 0, t.b, t.c) + qvs, qb, &full[s]);
+        if (fb) bulk_g2s(fmat, p.fpack + static_cast<size_t>(t.c) * (LY::F_SET / 2), fb, &full[s]);
         trace(p, it, 11);
       }
     }
@@ -669,14 +635,18 @@ extern "C" int hy_two_stage_fwd(const void* q, const void* k, const void* v, voi
 }
 
 // Fused MR mixer (bf16): featurizers + gates + two-stage conv in one pass.
-int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const float* taps_hat,
-                     const float* decay, int lh, int gs, int B, int C, int L, void* stream) {
+int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack, int lhf,
+                     const float* taps_hat, const float* decay, int lh, int gs, int B, int C, int L,
+                     void* stream) {
   int s = ts::check_shapes(B, C, L, lh, gs);
   if (s != HY_OK) return s;
   if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
   if (!aligned16(proj) || !aligned16(y)) return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  if (!feat_pack || !aligned16(feat_pack))
+    return fail(HY_ERR_INVALID, "tcgen05 mixer needs the packed featurizer (hy_feat_pack), 16-byte aligned");
   ts::Params p{};
   p.proj = static_cast<const ts::bf16*>(proj);
+  p.fpack = static_cast<const ts::bf16*>(feat_pack);
   p.y = static_cast<ts::bf16*>(y);
   p.taps_hat = taps_hat;
   p.decay = decay;
@@ -692,4 +662,42 @@ extern "C" HY_API int hy_debug_two_stage_trace(unsigned long long* host_out, int
   if (n > ts::TRACE_TILES * ts::TRACE_EV) n = ts::TRACE_TILES * ts::TRACE_EV;
   cudaError_t e = cudaMemcpyFromSymbol(host_out, ts::g_trace, n * sizeof(unsigned long long));
   return e == cudaSuccess ? HY_OK : fail(HY_ERR_CUDA, "trace copy: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- featurizer packing
+namespace hy {
+namespace ts {
+// out[c][tensor][ks][256]: F[n][k] = h[8*KS + n - k] for n < 8 in the no-swizzle K-major
+// core-matrix order the featurizer MMA reads (element (n,k) at (n%8)*8 + (n/8)*128 +
+// (k%8) + (k/8)*64 within a K-step).
+__global__ void feat_pack_kernel(const float* __restrict__ taps, int C, int lhf, int KS, bf16* __restrict__ out) {
+  const int per = 3 * KS * 256;
+  const long long total = static_cast<long long>(C) * per;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i / per), e = static_cast<int>(i % per);
+    const int tensor = e / (KS * 256), ks = (e / 256) % KS, r = e % 256;
+    // r = (n%8)*8 + (n/8)*128 + (k%8) + (k/8)*64
+    const int n = ((r >> 3) & 7) + ((r >> 7) & 1) * 8, kk = (r & 7) + ((r >> 6) & 1) * 8;
+    const int tap = 8 * KS + n - (16 * ks + kk);
+    float h = 0.f;
+    if (n < 8 && tap >= 0 && tap < lhf) h = taps[(static_cast<size_t>(tensor) * C + c) * lhf + tap];
+    out[i] = __float2bfloat16_rn(h);
+  }
+}
+}  // namespace ts
+}  // namespace hy
+
+extern "C" size_t hy_feat_pack_size(int C, int lhf) {
+  const int KS = lhf <= 9 ? 1 : 2;
+  return static_cast<size_t>(C) * 3 * KS * 256 * sizeof(ts::bf16);
+}
+
+extern "C" int hy_feat_pack(const float* feat_taps, int C, int lhf, void* out, void* stream) {
+  if (!feat_taps || !out) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (C < 1 || lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_INVALID, "bad featurizer shape C=%d lhf=%d", C, lhf);
+  const int KS = lhf <= 9 ? 1 : 2;
+  ts::feat_pack_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(feat_taps, C, lhf, KS,
+                                                                           static_cast<ts::bf16*>(out));
+  return check_launch("feat_pack_kernel");
 }

@@ -157,6 +157,7 @@ class HyenaOperator:
         for i, bank in enumerate((cfg.q_feat, cfg.k_feat, cfg.v_feat)):
             feat[i, :, :bank.filter_len] = bank.taps_per_channel()
         self.feat_taps = torch.from_numpy(feat).to(self.dev, tdt).contiguous()
+        self.feat_packed = ops.feat_pack(self.feat_taps) if dtype == torch.bfloat16 else None
         inner = cfg.inner
         self.gs = inner.group_size
         self.lh = inner.filter_len
@@ -187,7 +188,8 @@ class HyenaOperator:
         fused_ok = (self.dtype == torch.bfloat16 and self.lh <= 129) or \
                    (self.dtype in (torch.float32, torch.bfloat16) and self.lh <= 16)
         if fused_ok:
-            return ops.hyena_mixer(proj, self.feat_taps, self.inner_taps, self.gs, decay=self.decay)
+            return ops.hyena_mixer(proj, self.feat_taps, self.inner_taps, self.gs, decay=self.decay,
+                                   packed=self.feat_packed)
         # unfused: featurizers over all 3D rows in one launch, then the gated inner conv
         B, _, L = proj.shape
         feats = ops.causal_conv(proj, self.feat_taps.reshape(3 * D, self.lhf), 1)

@@ -119,8 +119,19 @@ def two_stage(v: torch.Tensor, taps_hat: torch.Tensor, group_size: int = 1, q=No
     return y[0] if squeeze else y
 
 
+def feat_pack(feat_taps: torch.Tensor) -> torch.Tensor:
+    """Pack (3, C, lhf) featurizer taps for the tcgen05 mixer (hy_feat_pack)."""
+    ft = feat_taps.to(dtype=torch.float32).contiguous()
+    _check_device(ft)
+    _, C, lhf = ft.shape
+    lib = _lib.load()
+    out = torch.empty(int(lib.hy_feat_pack_size(C, lhf)), dtype=torch.uint8, device=ft.device)
+    _lib.check(lib.hy_feat_pack(ft.data_ptr(), C, lhf, out.data_ptr(), _stream()), "feat_pack")
+    return out
+
+
 def hyena_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, inner_taps: torch.Tensor, group_size: int,
-                decay=None, out=None, se_only: bool = False) -> torch.Tensor:
+                decay=None, out=None, se_only: bool = False, packed=None) -> torch.Tensor:
     """Fused featurizers + gates + inner conv (hyena.py:162-186) from the (B, 3C, L) projections.
 
     feat_taps: (3, C, lhf) per-channel [q, k, v] featurizer taps (fp32);
@@ -139,9 +150,16 @@ def hyena_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, inner_taps: torch.T
         raise ValueError(f"feat_taps must be (3, {C}, lhf), got {tuple(ft.shape)}")
     y = out if out is not None else torch.empty((B, C, L), device=proj.device, dtype=proj.dtype)
     lib = _lib.load()
-    fn = lib.hy_se_mixer_fwd if se_only else lib.hy_hyena_mixer_fwd
-    _lib.check(fn(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), ft.shape[-1], it.data_ptr(), _ptr(decay),
-                  it.shape[-1], group_size, B, C, L, _dtype_code(proj), _stream()), "hyena_mixer")
+    if se_only:
+        _lib.check(lib.hy_se_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), ft.shape[-1], it.data_ptr(),
+                                       _ptr(decay), it.shape[-1], group_size, B, C, L, _dtype_code(proj),
+                                       _stream()), "se_mixer")
+        return y
+    if packed is None and proj.dtype == torch.bfloat16:
+        packed = feat_pack(ft)
+    _lib.check(lib.hy_hyena_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), _ptr(packed), ft.shape[-1],
+                                      it.data_ptr(), _ptr(decay), it.shape[-1], group_size, B, C, L,
+                                      _dtype_code(proj), _stream()), "hyena_mixer")
     return y
 
 

