@@ -62,15 +62,21 @@ constexpr int MAX_LHF = 16;
 // roles (producer, MMA issuers) take the top ids and the bulk CUDA-core roles the bottom.
 constexpr int N_CONV_WARPS = 8, N_EPI_WARPS = 4, N_TB_WARPS = 4;
 constexpr int W_CONV0 = 0, W_EPI0 = W_CONV0 + N_CONV_WARPS, W_TB0 = W_EPI0 + N_EPI_WARPS;
+// Two producer warps alternate tiles (each owns every other stage of the ring).
+constexpr int N_PROD_WARPS = 2;
 constexpr int W_FMMA = W_TB0 + N_TB_WARPS, W_MMA = W_FMMA + 1, W_PROD = W_MMA + 1;
-constexpr int THREADS = (W_PROD + 1) * 32;
+constexpr int THREADS = (W_PROD + N_PROD_WARPS) * 32;
 constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
 constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
 
-// TMEM columns (512 allocated): main accumulators [2] x 32, Toeplitz factors T0 / T1
+// Ring depth of the per-tile buffers between converter, main MMA and epilogue
+// (U / U_prev / featurized q in SMEM, accumulators in TMEM).
+constexpr int NBUF = 3;
+
+// TMEM columns (512 allocated): main accumulators [NBUF] x 32, Toeplitz factors T0 / T1
 // (A operand of the main MMA, 128 lanes x 64 columns of packed bf16 pairs each), one
 // featurizer buffer (k / v / q outputs; drained to registers right after it lands).
-constexpr uint32_t TM_ACC = 0, TM_T0 = 2 * NCH, TM_T1 = TM_T0 + 64, TM_FEAT = TM_T1 + 64;
+constexpr uint32_t TM_ACC = 0, TM_T0 = NBUF * NCH, TM_T1 = TM_T0 + 64, TM_FEAT = TM_T1 + 64;
 constexpr uint32_t TM_K = 0, TM_V = 16 * KV_MB, TM_Q = 32 * KV_MB;
 static_assert(TM_FEAT + TM_Q + 16 * Q_MB <= 512, "TMEM budget");
 
@@ -80,16 +86,16 @@ constexpr int Q_BYTES = round_up(Q_LEN * 2, 128);
 constexpr int F_BYTES = 512;  // one 16x16 bf16 featurizer matrix (no-swizzle K-major)
 template <int KS>
 struct Layout {
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = 4;  // even: stage s is always filled by producer s % 2
   static constexpr int F_SET = 3 * KS * F_BYTES;  // q, k, v featurizer matrices
   static constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES + F_SET;
   static constexpr int OFF_ST = 0;  // stages first: window over-reads stay inside SMEM
-  static constexpr int OFF_U = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);  // U[2]
-  static constexpr int OFF_UP = OFF_U + 2 * NCH * LB * 2;   // U_prev[2]
-  static constexpr int OFF_FQ = OFF_UP + 2 * NCH * LB * 2;  // featurized q, bf16 [2]
-  static constexpr int OFF_HP = OFF_FQ + 2 * NCH * LB * 2;  // padded taps, bf16 [512]
+  static constexpr int OFF_U = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);  // U[NBUF]
+  static constexpr int OFF_UP = OFF_U + NBUF * NCH * LB * 2;   // U_prev[NBUF]
+  static constexpr int OFF_FQ = OFF_UP + NBUF * NCH * LB * 2;  // featurized q, bf16 [NBUF]
+  static constexpr int OFF_HP = OFF_FQ + NBUF * NCH * LB * 2;  // padded taps, bf16 [512]
   static constexpr int OFF_BAR = OFF_HP + 1024;
-  static constexpr int N_BARS = 2 * STAGES + 20;
+  static constexpr int N_BARS = 2 * STAGES + 8 + 6 * NBUF;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -193,14 +199,14 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   uint64_t* empty = bars + STAGES;       // [STAGES] MMA commit (featurizer done) -> producer
   uint64_t* ffull = bars + 2 * STAGES;   // [1] MMA commit -> converter (featurized in TMEM)
   uint64_t* fempty = ffull + 2;          // [1] converter warps -> MMA (feat TMEM drained)
-  uint64_t* ufull = ffull + 4;           // [2] converter -> MMA
-  uint64_t* uempty = ffull + 6;          // [2] MMA commit (U / U_prev read) -> converter
-  uint64_t* tfull = ffull + 8;           // [2] MMA commit -> epilogue
-  uint64_t* tempty = ffull + 10;         // [2] epilogue warps -> MMA
-  uint64_t* tfree = ffull + 12;          // [2] MMA commit: last reader of T0 / T1 done
-  uint64_t* tready = ffull + 14;         // [2] T builder -> MMA: T0 / T1 of the next group
-  uint64_t* qfull = ffull + 16;          // [2] converter -> epilogue: featurized q in SMEM
-  uint64_t* qempty = ffull + 18;         // [2] epilogue warps -> converter
+  uint64_t* tfree = ffull + 4;           // [2] MMA commit: last reader of T0 / T1 done
+  uint64_t* tready = ffull + 6;          // [2] T builder -> MMA: T0 / T1 of the next group
+  uint64_t* ufull = ffull + 8;           // [NBUF] converter -> MMA
+  uint64_t* uempty = ufull + NBUF;       // [NBUF] MMA commit (U / U_prev read) -> converter
+  uint64_t* tfull = uempty + NBUF;       // [NBUF] MMA commit -> epilogue
+  uint64_t* tempty = tfull + NBUF;       // [NBUF] epilogue warps -> MMA
+  uint64_t* qfull = tempty + NBUF;       // [NBUF] converter -> epilogue: featurized q in SMEM
+  uint64_t* qempty = qfull + NBUF;       // [NBUF] epilogue warps -> converter
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -217,14 +223,16 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ffull[i], 1);
       mbar_init(&fempty[i], N_CONV_WARPS);
+      mbar_init(&tfree[i], 1);
+      mbar_init(&tready[i], 1);
+    }
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(&ufull[i], 1);
       mbar_init(&uempty[i], 1);
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
-      mbar_init(&tfree[i], 1);
-      mbar_init(&tready[i], 1);
     }
     fence_mbar_init();
   }
@@ -234,14 +242,16 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == W_PROD) {
-    // ------------------------------------------------------------ producer
+  if (warp >= W_PROD) {
+    // ------------------------------------------------------------ producers
+    const int pw = warp - W_PROD;  // tiles it with it % 2 == pw
     int stage_c[STAGES];
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) stage_c[s] = -1;
     Tile t;
     t.init(tb, p);
-    for (int it = 0; it < ntiles; ++it, t.next(p)) {
+    if (pw == 1 && ntiles > 0) t.next(p);
+    for (int it = pw; it < ntiles; it += N_PROD_WARPS, t.next(p), t.next(p)) {
       const int s = it % STAGES;
       if (lane == 0) trace(p, it, 12);
       mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -353,8 +363,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       Tile t;
       t.init(tb, p);
       for (int j = 0; j < ntiles; ++j, t.next(p)) {
-        const int u = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
+        const int u = j % NBUF;
+        const uint32_t ph = (j / NBUF) & 1;
         const int g = t.c / p.gs;
         const bool first = g != g_prev;
         const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
@@ -404,7 +414,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     // M-blocks of this warp: k / v blocks half, half+2, half+4; q blocks half, half+2
     constexpr int KVB_PER = (KV_MB + 1) / 2, QB_PER = Q_MB / 2;
     for (int it = 0; it < ntiles; ++it) {
-      const int u = it & 1;
+      const int u = it % NBUF;
+      const uint32_t uph = (it / NBUF) & 1;
       // 1) drain the featurized k / v / q of this tile from TMEM into registers and
       //    release the single featurizer buffer for the next tile's MMAs at once
       mbar_wait(&ffull[0], it & 1);
@@ -430,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (lane == 0) mbar_arrive(&fempty[0]);
       // 2) u = k * v -> U / U_prev: window m holds times t0 - 128 + 8m .. +7, i.e. chunk
       //    m/16 - 1, 16-byte unit m%16
-      mbar_wait(&uempty[u], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&uempty[u], uph ^ 1);
       if (ctid == 0) trace(p, it, 2);
       unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
       unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
@@ -454,7 +465,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (ctid == 0) mbar_arrive(&ufull[u]);
       // 3) featurized q -> SMEM for the epilogue (times t0 + 8m .. +7)
       if (GQ) {
-        mbar_wait(&qempty[u], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&qempty[u], uph ^ 1);
         bf16* fq = reinterpret_cast<bf16*>(smem + LY::OFF_FQ + u * NCH * LB * 2);
 #pragma unroll
         for (int i = 0; i < QB_PER; ++i) {
@@ -476,8 +487,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     Tile t;
     t.init(tb, p);
     for (int it = 0; it < ntiles; ++it, t.next(p)) {
-      const int a = it & 1;
-      mbar_wait(&tfull[a], (it >> 1) & 1);
+      const int a = it % NBUF;
+      const uint32_t aph = (it / NBUF) & 1;
+      mbar_wait(&tfull[a], aph);
       if (quarter == 0 && lane == 0) trace(p, it, 5);
       tc_fence_after();
       float acc[NCH];
@@ -485,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
-      if (GQ) mbar_wait(&qfull[a], (it >> 1) & 1);
+      if (GQ) mbar_wait(&qfull[a], aph);
       const bf16* fq = reinterpret_cast<const bf16*>(smem + LY::OFF_FQ + a * NCH * LB * 2);
       bf16* yrow = p.y + (static_cast<size_t>(t.b) * p.C + t.c) * p.L + t.t0;
       const int nt = min(TILE_T, p.L - t.t0);
