@@ -111,6 +111,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+    except OSError:
+        return None
+    vals = [v["traffic_bytes"] for k, v in sorted(d.items()) if v.get("kernel") == kernel]
+    return vals[-1] if vals else None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -225,7 +236,8 @@ def run_ours(args, wl):
                 "path": "HyenaOperator.forward on pinned host bf16 x; H2D + forward + D2H per step"},
         "roofline": {"kernel": "two_stage_kernel<FEAT> (hy_hyena_mixer_fwd: featurizers + gates + tcgen05 T0/T1)",
                      "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks_kind,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic("two_stage_kernel"),
+                     "peak_source": peaks_kind,
                      "algorithmic_bytes_per_launch": mix_bytes, "launch_ms": mix_ms},
         "roofline_operator": {"bound": "tensor", "achieved": op_flops / (ms_step * 1e-3) / 1e12 / 1,
                               "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
