@@ -4,7 +4,8 @@ context-parallel conv schemes). Compute runs in hand-written sm_100a kernels beh
 C-ABI of include/hyena_b200.h; there is no CPU fallback.
 """
 
-from . import fft
+from . import cp, fft
+from .cp import CPGroup, ShardedSeq, a2a_conv, a2a_conv_pipelined, gather, p2p_conv, p2p_conv_overlapped, shard
 from .blockconv import (
     MultiplyCounter,
     ToeplitzFactors,

@@ -1,0 +1,312 @@
+"""Context-parallel convolution over torch.distributed (one process per GPU, NCCL).
+
+Restates the reference's simulated schemes (/root/reference/pkg/src/convhybrid/cpsim.py)
+as real collectives. Every rank holds one time shard `(C, L/N)` (or `(B, C, L/N)`) of
+the sequence; the functions below take the rank's local tensor and return its local
+output, and tally the same accounting as the reference's SimGroup (cpsim.py:69-131):
+
+  p2p_conv             halo of lh-1 steps from rank r to r+1, conv on [halo | local]
+                       (cpsim.py:460-495)
+  p2p_conv_overlapped  local conv on zero history launched before the halo is consumed,
+                       then the correction conv of the halo (cpsim.py:498-534)
+  a2a_conv             two all_to_all_single rounds swap time shards <-> channel slabs,
+                       conv over the full sequence on the slab (cpsim.py:325-447)
+  a2a_conv_pipelined   the same in n_pipe channel segments (cpsim.py:449-454)
+
+`HyenaCP` composes them into the context-parallel Hyena operator:
+projections and gates are token-local; SE/MR receive the last 144 steps of the
+predecessor's projections and run the fused tcgen05 mixer with that history; LI swaps
+u = k*v to channel slabs with all-to-all for the long convolution.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .core import GroupSpec, SeqTensor
+
+LAYOUTS = ("sequential", "zigzag")
+
+
+@dataclass
+class CPGroup:
+    """A torch.distributed process group plus the reference's accounting fields."""
+
+    group: object = None  # torch.distributed ProcessGroup (None = default world group)
+    scheme_elements: dict = field(default_factory=dict)
+    scheme_messages: dict = field(default_factory=dict)
+    scheme_rounds: dict = field(default_factory=dict)
+    filter_elements: dict = field(default_factory=dict)
+    message_log: list = field(default_factory=list)
+
+    def __post_init__(self):
+        n = self.n_ranks
+        if n < 1 or (n & (n - 1)) != 0:
+            raise ValueError(f"rank count must be a power of two >= 1, got {n}")
+
+    @property
+    def n_ranks(self) -> int:
+        return dist.get_world_size(self.group)
+
+    @property
+    def rank(self) -> int:
+        return dist.get_rank(self.group)
+
+    def _send(self, scheme: str, src: int, dst: int, elements: int) -> None:
+        # every rank tallies every message of the scheme, so counters agree across ranks
+        self.message_log.append((len(self.message_log) + 1, scheme, src, dst, int(elements)))
+        self.scheme_elements[scheme] = self.scheme_elements.get(scheme, 0) + int(elements)
+        self.scheme_messages[scheme] = self.scheme_messages.get(scheme, 0) + 1
+
+    def count_rounds(self, scheme: str, n: int) -> None:
+        self.scheme_rounds[scheme] = self.scheme_rounds.get(scheme, 0) + n
+
+    def total_elements(self, scheme: str | None = None) -> int:
+        return self.scheme_elements.get(scheme, 0) if scheme else sum(self.scheme_elements.values())
+
+    def total_messages(self, scheme: str | None = None) -> int:
+        return self.scheme_messages.get(scheme, 0) if scheme else sum(self.scheme_messages.values())
+
+
+# ---------------------------------------------------------------- sharding (cpsim.py:244-319)
+
+
+@dataclass(frozen=True)
+class ShardedSeq:
+    """Per-rank (d, l/n_ranks) slices of one sequence (host view, cpsim.py:247-279)."""
+
+    shards: tuple
+    layout: str = "sequential"
+
+    def __post_init__(self):
+        shards = tuple(np.asarray(s) for s in self.shards)
+        if not shards:
+            raise ValueError("need at least one shard")
+        if any(s.shape != shards[0].shape for s in shards):
+            raise ValueError("all shards must share one shape")
+        if self.layout not in LAYOUTS:
+            raise ValueError(f"layout must be one of {LAYOUTS}, got {self.layout!r}")
+        object.__setattr__(self, "shards", shards)
+
+    @property
+    def n_ranks(self) -> int:
+        return len(self.shards)
+
+    @property
+    def channels(self) -> int:
+        return self.shards[0].shape[0]
+
+    @property
+    def shard_len(self) -> int:
+        return self.shards[0].shape[1]
+
+    @property
+    def total_len(self) -> int:
+        return self.shard_len * self.n_ranks
+
+
+def layout_chunks(layout: str, n_ranks: int):
+    """Chunk ids per rank in local time order; zigzag gives rank r chunks r and 2N-1-r."""
+    if layout == "sequential":
+        return [[r] for r in range(n_ranks)]
+    return [[r, 2 * n_ranks - 1 - r] for r in range(n_ranks)]
+
+
+def shard(x: SeqTensor, n_ranks: int, layout: str = "sequential") -> ShardedSeq:
+    """(cpsim.py:289-301)."""
+    if layout not in LAYOUTS:
+        raise ValueError(f"layout must be one of {LAYOUTS}, got {layout!r}")
+    divisor = n_ranks * (1 if layout == "sequential" else 2)
+    if x.length % divisor != 0:
+        raise ValueError(f"length {x.length} not divisible by {divisor} ({layout} layout over {n_ranks} ranks)")
+    clen = x.length // divisor
+    return ShardedSeq(tuple(np.concatenate([x.data[:, c * clen:(c + 1) * clen] for c in ids], axis=1)
+                            for ids in layout_chunks(layout, n_ranks)), layout)
+
+
+def gather(xs: ShardedSeq) -> SeqTensor:
+    """(cpsim.py:304-312)."""
+    ids = layout_chunks(xs.layout, xs.n_ranks)
+    clen = xs.shard_len // len(ids[0])
+    out = np.empty((xs.channels, xs.total_len), dtype=np.float64)
+    for r, cs in enumerate(ids):
+        for i, c in enumerate(cs):
+            out[:, c * clen:(c + 1) * clen] = xs.shards[r][:, i * clen:(i + 1) * clen]
+    return SeqTensor(out)
+
+
+def natural_cols(layout: str, n_ranks: int, total_len: int) -> np.ndarray:
+    """Assembled (rank-major) position i holds natural time column map[i] (cpsim.py:315-319)."""
+    ids = [c for cs in layout_chunks(layout, n_ranks) for c in cs]
+    clen = total_len // len(ids)
+    return np.concatenate([np.arange(c * clen, (c + 1) * clen) for c in ids])
+
+
+# ---------------------------------------------------------------- default (GPU) local kernels
+
+
+def _gpu_conv(taps: torch.Tensor, gs: int):
+    from . import ops
+
+    def conv(x):
+        return ops.long_conv(x.contiguous(), taps, gs) if taps.shape[-1] > 32 else ops.causal_conv(x.contiguous(), taps, gs)
+    return conv
+
+
+def _gpu_correct(taps: torch.Tensor, gs: int):
+    from . import ops
+
+    def correct(halo, y):
+        ops.halo_correction(halo.contiguous(), y, taps, gs)
+        return y
+    return correct
+
+
+def _taps_tensor(groups: GroupSpec, like: torch.Tensor) -> torch.Tensor:
+    from .ops import tap_dtype
+    dt = tap_dtype(like.dtype) if like.is_floating_point() else torch.float64
+    return torch.from_numpy(groups.materialized()).to(like.device, dt)
+
+
+# ---------------------------------------------------------------- p2p halo schemes
+
+
+def _check_p2p(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str) -> int:
+    if layout != "sequential":
+        raise ValueError("point-to-point schemes need the sequential layout")
+    if local.shape[-2] != groups.channels:
+        raise ValueError(f"input has {local.shape[-2]} channels, grouping expects {groups.channels}")
+    halo = groups.filter_len - 1
+    if local.shape[-1] < halo:
+        raise ValueError(f"shard length {local.shape[-1]} shorter than halo {halo}")
+    for r in range(grp.n_ranks):
+        grp.filter_elements[r] = groups.n_groups * groups.filter_len  # full bank everywhere
+    return halo
+
+
+def _exchange_halo(local: torch.Tensor, halo: int, grp: CPGroup, scheme: str):
+    """Start the send of the last `halo` steps to rank r+1 and the receive from r-1."""
+    n, r = grp.n_ranks, grp.rank
+    chans = int(np.prod(local.shape[:-1]))
+    for src in range(n - 1):  # every rank tallies the N-1 boundary messages
+        grp._send(scheme, src, src + 1, chans * halo)
+    left = torch.zeros(local.shape[:-1] + (halo,), dtype=local.dtype, device=local.device)
+    ops_ = []
+    if r < n - 1:
+        ops_.append(dist.P2POp(dist.isend, local[..., local.shape[-1] - halo:].contiguous(), r + 1, grp.group))
+    if r > 0:
+        ops_.append(dist.P2POp(dist.irecv, left, r - 1, grp.group))
+    reqs = dist.batch_isend_irecv(ops_) if ops_ else []
+    return left, reqs
+
+
+def p2p_conv(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str = "sequential",
+             conv=None) -> torch.Tensor:
+    """Halo exchange, then the conv over [halo | local] minus the first halo outputs."""
+    halo = _check_p2p(local, groups, grp, layout)
+    if halo == 0:
+        return (conv or _gpu_conv(_taps_tensor(groups, local), groups.group_size))(local)
+    left, reqs = _exchange_halo(local, halo, grp, "p2p_conv")
+    for q in reqs:
+        q.wait()
+    conv = conv or _gpu_conv(_taps_tensor(groups, local), groups.group_size)
+    return conv(torch.cat([left, local], dim=-1))[..., halo:].contiguous()
+
+
+def p2p_conv_overlapped(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str = "sequential",
+                        conv=None, correct=None) -> torch.Tensor:
+    """Local conv on zero history first (overlapping the halo transfer), then the correction
+    conv([halo | 0])[:, halo:] added to the first halo outputs (cpsim.py:498-510)."""
+    halo = _check_p2p(local, groups, grp, layout)
+    taps = None
+    if conv is None or correct is None:
+        taps = _taps_tensor(groups, local)
+    conv = conv or _gpu_conv(taps, groups.group_size)
+    if halo == 0:
+        return conv(local)
+    left, reqs = _exchange_halo(local, halo, grp, "p2p_conv_overlapped")
+    y = conv(local)  # issued before the halo is consumed
+    for q in reqs:
+        q.wait()
+    if grp.rank > 0:
+        y = (correct or _gpu_correct(taps, groups.group_size))(left, y)
+    return y
+
+
+# ---------------------------------------------------------------- all-to-all schemes
+
+
+def _slab_groups(groups: GroupSpec, start: int, count: int) -> GroupSpec:
+    """Sub-bank for a channel slab; slab edges must respect groups (cpsim.py:325-333)."""
+    if start % groups.group_size != 0 or count % groups.group_size != 0:
+        raise ValueError(f"channel slab [{start}, {start + count}) splits a filter group of size {groups.group_size}")
+    first = start // groups.group_size
+    return GroupSpec(count, groups.group_size, groups.filters[first:first + count // groups.group_size])
+
+
+def _a2a(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int, layout: str, scheme: str,
+         conv_slab) -> torch.Tensor:
+    n, r = grp.n_ranks, grp.rank
+    if local.dim() != 2:
+        raise ValueError("all-to-all schemes take the rank's (C, L/N) shard")
+    d, m = local.shape
+    if d != groups.channels:
+        raise ValueError(f"input has {d} channels, grouping expects {groups.channels}")
+    if d % n != 0:
+        raise ValueError(f"channel count {d} not divisible by {n} ranks")
+    if (d // n) % n_pipe != 0:
+        raise ValueError(f"per-rank slab {d // n} not divisible by {n_pipe} pipeline segments")
+    seg = d // n_pipe
+    slab = seg // n
+    for s in range(n_pipe):
+        for rr in range(n):
+            _slab_groups(groups, s * seg + rr * slab, slab)
+    for rr in range(n):
+        grp.filter_elements[rr] = sum(_slab_groups(groups, s * seg + rr * slab, slab).n_groups
+                                      for s in range(n_pipe)) * groups.filter_len
+    cols = torch.from_numpy(natural_cols(layout, n, m * n)).to(local.device)
+    out = torch.empty_like(local)
+    for s in range(n_pipe):
+        lo = s * seg
+        for src in range(n):  # scatter round: every rank sends N-1 slab pieces
+            for dst in range(n):
+                if dst != src:
+                    grp._send(scheme, src, dst, slab * m)
+        recv = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
+        dist.all_to_all_single(recv, local[lo:lo + seg].contiguous(), group=grp.group)
+        assembled = recv.permute(1, 0, 2).reshape(slab, n * m)  # rank-major time order
+        natural = torch.empty_like(assembled)
+        natural[:, cols] = assembled
+        result = conv_slab(natural, _slab_groups(groups, lo + r * slab, slab))
+        back = result[:, cols].reshape(slab, n, m).permute(1, 0, 2).contiguous()  # (dst, slab, m)
+        for src in range(n):  # return round
+            for dst in range(n):
+                if dst != src:
+                    grp._send(scheme, src, dst, slab * m)
+        ret = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
+        dist.all_to_all_single(ret, back, group=grp.group)
+        out[lo:lo + seg] = ret.reshape(seg, m)
+    grp.count_rounds(scheme, 2 * n_pipe)
+    return out
+
+
+def _gpu_slab_conv(natural: torch.Tensor, bank: GroupSpec) -> torch.Tensor:
+    return _gpu_conv(_taps_tensor(bank, natural), bank.group_size)(natural)
+
+
+def a2a_conv(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str = "sequential",
+             conv_slab=None) -> torch.Tensor:
+    """Time shard -> channel slab, conv over the full sequence, back (cpsim.py:428-437)."""
+    return _a2a(local, groups, grp, 1, layout, "a2a_conv", conv_slab or _gpu_slab_conv)
+
+
+def a2a_conv_pipelined(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int,
+                       layout: str = "sequential", conv_slab=None) -> torch.Tensor:
+    """The a2a scheme in n_pipe channel segments (cpsim.py:449-454)."""
+    if n_pipe < 1:
+        raise ValueError(f"n_pipe must be >= 1, got {n_pipe}")
+    return _a2a(local, groups, grp, n_pipe, layout, "a2a_conv_pipelined", conv_slab or _gpu_slab_conv)
