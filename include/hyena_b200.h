@@ -91,9 +91,13 @@ HY_API int hy_feat_pack(const float* feat_taps, int C, int lhf, void* out, void*
  * MR / SE in bf16 with lh <= 129 and feat_pack given: tcgen05 kernel (featurizers and the
  * two-stage conv as MMAs). SE (lh <= 16) otherwise: CUDA-core kernel, fp32 or bf16.
  * HY_F64 and longer filters return HY_ERR_UNSUPPORTED (the host composes kernels). */
+#define HY_MIXER_HISTORY 144
+/* hist (nullable, tcgen05 path only): (B, 3C, HY_MIXER_HISTORY) bf16, the projections of the
+ * HY_MIXER_HISTORY steps before t = 0 (context parallel: the predecessor rank's last steps);
+ * NULL means zeros (sequence start), as in the reference. */
 HY_API int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, const void* feat_pack,
-                       int lhf, const void* inner_taps, const float* inner_decay, int lh, int group_size,
-                       int B, int C, int L, int dtype, void* stream);
+                       const void* hist, int lhf, const void* inner_taps, const float* inner_decay,
+                       int lh, int group_size, int B, int C, int L, int dtype, void* stream);
 
 /* SE mixer only (CUDA cores, fp32 / bf16, lh and lhf <= 16), same arguments. */
 HY_API int hy_se_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,

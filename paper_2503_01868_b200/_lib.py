@@ -13,6 +13,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhyena_b200.so")
 
+MIXER_HISTORY = 144  # HY_MIXER_HISTORY
+
 HY_OK, HY_ERR_INVALID, HY_ERR_INELIGIBLE, HY_ERR_UNSUPPORTED, HY_ERR_CUDA = range(5)
 HY_F32, HY_BF16, HY_F64 = 0, 1, 2
 
@@ -27,7 +29,7 @@ SIGNATURES = {
     "hy_causal_conv_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_gated_conv_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_two_stage_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
-    "hy_hyena_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "hy_hyena_mixer_fwd": (_I, [_P, _P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_feat_pack_size": (_SZ, [_I, _I]),
     "hy_feat_pack": (_I, [_P, _I, _I, _P, _P]),
     "hy_se_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),

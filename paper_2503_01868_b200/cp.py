@@ -310,3 +310,76 @@ def a2a_conv_pipelined(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_p
     if n_pipe < 1:
         raise ValueError(f"n_pipe must be >= 1, got {n_pipe}")
     return _a2a(local, groups, grp, n_pipe, layout, "a2a_conv_pipelined", conv_slab or _gpu_slab_conv)
+
+
+# ---------------------------------------------------------------- context-parallel Hyena operator
+
+
+class HyenaCP:
+    """Context-parallel Hyena operator: each rank holds the (B, D, L/N) time
+    shard of x (sequential layout) and returns its shard of y.
+
+    * projections, gates and the output projection are token-local (no communication);
+    * SE / MR (fused tcgen05 mixer): one p2p round ships the last HY_MIXER_HISTORY = 144
+      steps of the projections (3D rows) to rank r+1, which the mixer reads as the history
+      before its t = 0 (the featurizer halo and the inner-conv halo in one message);
+    * LI and the unfused paths: featurizer halo (lhf-1 steps of the projections) by the
+      overlapped p2p scheme, then u = k*v either by the overlapped p2p halo (lh-1 steps)
+      or, for LI, by the two all-to-all rounds to channel slabs and back.
+    """
+
+    def __init__(self, cfg, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None):
+        from .hyena import HyenaOperator
+        self.op = HyenaOperator(cfg, dtype)
+        self.cfg = cfg
+        self.grp = grp or CPGroup()
+
+    def _fused(self) -> bool:
+        return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
+
+    def forward(self, x_local: torch.Tensor) -> torch.Tensor:
+        from . import _lib, ops
+        op, grp = self.op, self.grp
+        x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
+        B, D, m = x3.shape
+        proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
+        if self._fused():
+            hist, reqs = _exchange_halo(proj, _lib.MIXER_HISTORY, grp, "cp_hist")
+            for q in reqs:
+                q.wait()
+            mixed = ops.hyena_mixer(proj, op.feat_taps, op.inner_taps, op.gs, decay=op.decay,
+                                    packed=op.feat_packed, hist=hist if grp.rank > 0 else None)
+        else:
+            # featurizers over the 3D projected rows with their (lhf-1)-step halo
+            ft = op.feat_taps.reshape(3 * D, op.lhf)
+            feat_groups = _per_channel_groups(ft)
+            feats = p2p_conv_overlapped(proj, feat_groups, grp,
+                                        conv=lambda z: ops.causal_conv(z.contiguous(), ft, 1),
+                                        correct=lambda h, y: _correct(h, y, ft, 1))
+            q, k, v = (feats[:, i * D:(i + 1) * D].contiguous() for i in range(3))
+            u = k * v
+            taps = op.materialized_inner
+            if self.cfg.variant == "LI":
+                conv = torch.stack([a2a_conv(u[b], self.cfg.inner, grp) for b in range(B)])
+            else:
+                conv = p2p_conv_overlapped(u, self.cfg.inner, grp,
+                                           conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
+                                           correct=lambda h, y: _correct(h, y, taps, op.gs))
+            mixed = q * conv
+        y = torch.matmul(op.w_out_t, mixed)
+        return y[0] if x_local.dim() == 2 else y
+
+    __call__ = forward
+
+
+def _correct(halo, y, taps, gs):
+    from . import ops
+    y = y.contiguous()
+    ops.halo_correction(halo.contiguous(), y, taps, gs)
+    return y
+
+
+def _per_channel_groups(taps: torch.Tensor) -> GroupSpec:
+    from .core import ExplicitFilter
+    t = taps.detach().double().cpu().numpy()
+    return GroupSpec(t.shape[0], 1, tuple(ExplicitFilter(r) for r in t))

@@ -153,8 +153,8 @@ static int launch_se_dispatch(const void* proj, void* y, const float* ft, int lh
 using namespace hy;
 
 extern "C" int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, const void* feat_pack,
-                                  int lhf, const void* inner_taps, const float* inner_decay, int lh, int gs,
-                                  int B, int C, int L, int dtype, void* stream) {
+                                  const void* hist, int lhf, const void* inner_taps, const float* inner_decay,
+                                  int lh, int gs, int B, int C, int L, int dtype, void* stream) {
   if (!proj || !y || !feat_taps || !inner_taps) return fail(HY_ERR_INVALID, "null pointer argument");
   if (B < 1 || C < 1 || L < 1 || lh < 1 || gs < 1 || lhf < 1)
     return fail(HY_ERR_INVALID, "sizes must be >= 1");
@@ -165,7 +165,8 @@ extern "C" int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_ta
   const float* ft = static_cast<const float*>(feat_taps);
   const float* it = static_cast<const float*>(inner_taps);
   if (dtype == HY_BF16 && lh <= 129 && L % 8 == 0 && aligned16(proj) && aligned16(y) && feat_pack)
-    return mr_mixer_fwd(proj, y, ft, feat_pack, lhf, it, inner_decay, lh, gs, B, C, L, stream);
+    return mr_mixer_fwd(proj, y, ft, feat_pack, hist, lhf, it, inner_decay, lh, gs, B, C, L, stream);
+  if (hist) return fail(HY_ERR_UNSUPPORTED, "projection history (context parallel) needs the tcgen05 mixer path");
   if (lh <= 16) {
     if (dtype == HY_F32) return launch_se_dispatch<float>(proj, y, ft, lhf, it, inner_decay, lh, gs, B, C, L, st);
     if (dtype == HY_BF16)

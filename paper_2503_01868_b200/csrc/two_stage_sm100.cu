@@ -57,6 +57,10 @@ constexpr int KV_MB = (KV_WIN + 127) / 128;    // 5 M-blocks
 constexpr int Q_WIN = NCH * LB / 8;            // 512 windows for q
 constexpr int Q_MB = Q_WIN / 128;              // 4 M-blocks
 constexpr int MAX_LHF = 16;
+// Context parallel: history of the raw projections before t = 0 (the predecessor rank's
+// last steps) that the first tile of each sequence reads instead of zeros.
+constexpr int HIST = LB + HALO;  // 144 = HY_MIXER_HISTORY
+static_assert(HIST == 144, "keep in sync with include/hyena_b200.h");
 
 // The warp scheduler favours higher warp ids, so the latency-critical single-lane
 // roles (producer, MMA issuers) take the top ids and the bulk CUDA-core roles the bottom.
@@ -111,6 +115,7 @@ struct Params {
   const float* decay;      // (n_groups) rate*log2(base), or null
   const float* feat_taps;  // fused: (3, C, lhf), per channel
   const bf16* fpack;       // fused: packed featurizer matrices, (C, 3, KS, 256) bf16, or null
+  const bf16* hist;        // fused: (B, 3C, HIST) projections before t = 0, or null (zeros)
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
@@ -266,10 +271,12 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       const int qws = t.t0 - HALO, qwe = t.t0 + TILE_T;
       const int qvs = max(qws, 0), qve = min(qwe, p.L);
       bool wrote = false;  // generic-proxy SMEM writes to order before the async proxy
+      // first tile with a predecessor's history: the head of the windows comes from hist
+      const bool use_hist = FEAT && p.hist != nullptr && t.t0 == 0;
       if (kvs != kws || kve != kwe || qvs != qws || qve != qwe) {
         // zero the parts of the windows outside [0, L) (whole 8-element units)
         const int4 z = make_int4(0, 0, 0, 0);
-        for (int i = lane * 8; i < kvs - kws; i += 256) {
+        for (int i = lane * 8; !use_hist && i < kvs - kws; i += 256) {
           *reinterpret_cast<int4*>(vbuf + i) = z;
           if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
         }
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
         }
         if (GQ) {
-          for (int i = lane * 8; i < qvs - qws; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
+          for (int i = lane * 8; !use_hist && i < qvs - qws; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
           for (int i = (qve - qws) + lane * 8; i < Q_LEN; i += 256) *reinterpret_cast<int4*>(qbuf + i) = z;
         }
         wrote = true;
@@ -304,7 +311,15 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (elect_one()) {
         const uint32_t kvb = static_cast<uint32_t>(kve - kvs) * 2, qb = static_cast<uint32_t>(qve - qvs) * 2;
         const uint32_t fb = (FEAT && need_f) ? static_cast<uint32_t>(LY::F_SET) : 0u;
-        mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0) + fb);
+        const uint32_t hb = use_hist ? static_cast<uint32_t>(HIST + HALO) * 4 : 0u;  // k/v 144 + q 16 (x2 B)
+        mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0) + fb + hb);
+        if (use_hist) {
+          const bf16* hrow = p.hist + (static_cast<size_t>(t.b) * 3 * p.C + t.c) * HIST;  // q row
+          const size_t tstride = static_cast<size_t>(p.C) * HIST;                       // q -> k -> v
+          bulk_g2s(kbuf, hrow + tstride, HIST * 2, &full[s]);
+          bulk_g2s(vbuf, hrow + 2 * tstride, HIST * 2, &full[s]);
+          bulk_g2s(qbuf, hrow + (HIST - HALO), HALO * 2, &full[s]);
+        }
         bulk_g2s(vbuf + (kvs - kws), row_ptr<FEAT>(p, 2, t.b, t.c) + kvs, kvb, &full[s]);
         if (GK) bulk_g2s(kbuf + (kvs - kws), row_ptr<FEAT>(p, 1, t.b, t.c) + kvs, kvb, &full[s]);
         if (GQ) bulk_g2s(qbuf + (qvs - qws), row_ptr<FEAT>(p, 0, t.b, t.c) + qvs, qb, &full[s]);
@@ -647,9 +662,9 @@ extern "C" int hy_two_stage_fwd(const void* q, const void* k, const void* v, voi
 }
 
 // Fused MR mixer (bf16): featurizers + gates + two-stage conv in one pass.
-int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack, int lhf,
-                     const float* taps_hat, const float* decay, int lh, int gs, int B, int C, int L,
-                     void* stream) {
+int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack,
+                     const void* hist, int lhf, const float* taps_hat, const float* decay, int lh, int gs,
+                     int B, int C, int L, void* stream) {
   int s = ts::check_shapes(B, C, L, lh, gs);
   if (s != HY_OK) return s;
   if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
@@ -659,6 +674,8 @@ int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const vo
   ts::Params p{};
   p.proj = static_cast<const ts::bf16*>(proj);
   p.fpack = static_cast<const ts::bf16*>(feat_pack);
+  if (hist && !aligned16(hist)) return fail(HY_ERR_INVALID, "history buffer must be 16-byte aligned");
+  p.hist = static_cast<const ts::bf16*>(hist);
   p.y = static_cast<ts::bf16*>(y);
   p.taps_hat = taps_hat;
   p.decay = decay;

@@ -131,11 +131,12 @@ def feat_pack(feat_taps: torch.Tensor) -> torch.Tensor:
 
 
 def hyena_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, inner_taps: torch.Tensor, group_size: int,
-                decay=None, out=None, se_only: bool = False, packed=None) -> torch.Tensor:
+                decay=None, out=None, se_only: bool = False, packed=None, hist=None) -> torch.Tensor:
     """Fused featurizers + gates + inner conv (hyena.py:162-186) from the (B, 3C, L) projections.
 
     feat_taps: (3, C, lhf) per-channel [q, k, v] featurizer taps (fp32);
-    inner_taps: (G, lh) fp32; decay: (G,) fp32 or None.
+    inner_taps: (G, lh) fp32; decay: (G,) fp32 or None;
+    hist: (B, 3C, 144) projections before t = 0 (context parallel), None = zeros.
     """
     _check_device(proj)
     B, C3, L = proj.shape
@@ -157,7 +158,12 @@ def hyena_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, inner_taps: torch.T
         return y
     if packed is None and proj.dtype == torch.bfloat16:
         packed = feat_pack(ft)
-    _lib.check(lib.hy_hyena_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), _ptr(packed), ft.shape[-1],
+    if hist is not None:
+        _check_device(hist)
+        if tuple(hist.shape) != (B, C3, _lib.MIXER_HISTORY) or hist.dtype != proj.dtype:
+            raise ValueError(f"hist must be (B, 3C, {_lib.MIXER_HISTORY}) {proj.dtype}")
+    _lib.check(lib.hy_hyena_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), _ptr(packed), _ptr(hist),
+                                      ft.shape[-1],
                                       it.data_ptr(), _ptr(decay), it.shape[-1], group_size, B, C, L,
                                       _dtype_code(proj), _stream()), "hyena_mixer")
     return y

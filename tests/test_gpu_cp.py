@@ -1,0 +1,84 @@
+"""GPU checks of the context-parallel path.
+
+* single GPU: the fused mixer with a projection history equals the second half of a
+  full-sequence run (the property the CP operator relies on);
+* >= 2 GPUs (skipped otherwise): HyenaCP over NCCL equals the single-GPU operator.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2503_01868_b200 as hy
+from paper_2503_01868_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def test_mixer_history_equals_split():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B, C, L = 2, 16, 8192
+    proj = torch.randn((B, 3 * C, L), device="cuda", dtype=torch.bfloat16, generator=g)
+    feat = torch.randn((3, C, 7), device="cuda", generator=g) / 3
+    taps = torch.randn((C, 128), device="cuda", generator=g) / 11
+    decay = torch.linspace(0.01, 2.0, C, device="cuda")
+    full = ops.hyena_mixer(proj, feat, taps, 1, decay=decay)
+    for cut in (4096, 2048, 512):
+        hist = proj[..., cut - 144:cut].contiguous()
+        second = ops.hyena_mixer(proj[..., cut:].contiguous(), feat, taps, 1, decay=decay, hist=hist)
+        assert torch.equal(second, full[..., cut:]), cut
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cp_worker(rank, world, port, variant, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        D, L = 64, 8192 * world
+        kw = {"inner_len": 128, "block_size": 128} if variant == "MR" else {}
+        cfg = hy.make_hyena_config(variant, D, hy.make_rng(0), seq_len=L, **kw)
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        x = torch.randn((1, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
+        m = L // world
+        y_local = hy.cp.HyenaCP(cfg, torch.bfloat16).forward(x[..., rank * m:(rank + 1) * m].contiguous())
+        if rank == 0:
+            y_ref = hy.HyenaOperator(cfg, torch.bfloat16).forward(x)
+        parts = [torch.empty_like(y_local) for _ in range(world)]
+        dist.all_gather(parts, y_local)
+        if rank == 0:
+            y = torch.cat(parts, dim=-1).float()
+            err = float((y - y_ref.float()).abs().max() / max(1.0, float(y_ref.float().abs().max())))
+            q.put(err)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("variant", ["MR", "SE"])
+def test_hyena_cp_matches_single_gpu(variant):
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, variant, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert err < 2e-2, err
