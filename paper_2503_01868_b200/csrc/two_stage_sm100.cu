@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (elect_one()) {
         const uint32_t kvb = static_cast<uint32_t>(kve - kvs) * 2, qb = static_cast<uint32_t>(qve - qvs) * 2;
         const uint32_t fb = (FEAT && need_f) ? static_cast<uint32_t>(LY::F_SET) : 0u;
-        const uint32_t hb = use_hist ? static_cast<uint32_t>(HIST + HALO) * 4 : 0u;  // k/v 144 + q 16 (x2 B)
+        const uint32_t hb = use_hist ? static_cast<uint32_t>(2 * HIST + HALO) * 2 : 0u;  // k, v 144 + q 16 steps
         mbar_arrive_expect_tx(&full[s], kvb * (GK ? 2 : 1) + (GQ ? qb : 0) + fb + hb);
         if (use_hist) {
           const bf16* hrow = p.hist + (static_cast<size_t>(t.b) * 3 * p.C + t.c) * HIST;  // q row
