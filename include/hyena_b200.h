@@ -99,6 +99,20 @@ HY_API int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_taps, 
                        const void* hist, int lhf, const void* inner_taps, const float* inner_decay,
                        int lh, int group_size, int B, int C, int L, int dtype, void* stream);
 
+/* Hyena-LI on tcgen05 (bf16) for an implicit filter h_t = sum_n R_n lam_n^t (core.py:147-151,
+ * |lam| <= 1, npoles <= 8; residues / poles: fp32 (n_groups, npoles)): the causal conv over
+ * the whole sequence as intra-chunk Toeplitz MMAs (h[0..127]) plus the exact per-mode
+ * recurrence carried chunk to chunk (tf32 MMA). Same numbers as fft_conv on the materialised
+ * taps (fft.py:128-145); HBM-bound instead of FFT-bound.
+ *   hy_li_mixer_fwd: from the (B, 3C, L) projections, featurizers and gates fused (LI operator)
+ *   hy_li_conv_fwd:  y = q * (h conv (k * v)), q / k nullable */
+HY_API int hy_li_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack, int lhf,
+                           const float* residues, const float* poles, int npoles, int group_size,
+                           int B, int C, int L, int dtype, void* stream);
+HY_API int hy_li_conv_fwd(const void* q, const void* k, const void* v, void* y, const float* residues,
+                          const float* poles, int npoles, int group_size, int B, int C, int L, int dtype,
+                          void* stream);
+
 /* SE mixer only (CUDA cores, fp32 / bf16, lh and lhf <= 16), same arguments. */
 HY_API int hy_se_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,
                            const void* inner_taps, const float* inner_decay, int lh, int group_size,

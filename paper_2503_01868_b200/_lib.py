@@ -37,6 +37,8 @@ SIGNATURES = {
     "hy_fft_conv_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
     "hy_halo_correction_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_debug_two_stage_trace": (_I, [_P, _I]),
+    "hy_li_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "hy_li_conv_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
 }
 
 _lib = None

@@ -57,6 +57,7 @@ constexpr int KV_MB = (KV_WIN + 127) / 128;    // 5 M-blocks
 constexpr int Q_WIN = NCH * LB / 8;            // 512 windows for q
 constexpr int Q_MB = Q_WIN / 128;              // 4 M-blocks
 constexpr int MAX_LHF = 16;
+constexpr int NPOLE = 8;  // implicit-filter modes per group (ImplicitFilter poles), zero padded
 // Context parallel: history of the raw projections before t = 0 (the predecessor rank's
 // last steps) that the first tile of each sequence reads instead of zeros.
 constexpr int HIST = LB + HALO;  // 144 = HY_MIXER_HISTORY
@@ -98,7 +99,12 @@ struct Layout {
   static constexpr int OFF_UP = OFF_U + NBUF * NCH * LB * 2;   // U_prev[NBUF]
   static constexpr int OFF_FQ = OFF_UP + NBUF * NCH * LB * 2;  // featurized q, bf16 [NBUF]
   static constexpr int OFF_HP = OFF_FQ + NBUF * NCH * LB * 2;  // padded taps, bf16 [512]
-  static constexpr int OFF_BAR = OFF_HP + 1024;
+  // implicit (LI) mode: P[m][n] = R_n lam_n^(m+1) (tf32 A operand, 128 x 8), per-chunk mode
+  // inputs E[chunk][n], carried states S_prev[chunk][n] (tf32 B operand, [NBUF] x 32 x 8)
+  static constexpr int OFF_P = OFF_HP + 1024;
+  static constexpr int OFF_E = OFF_P + 128 * NPOLE * 4;
+  static constexpr int OFF_S = OFF_E + NCH * NPOLE * 4;
+  static constexpr int OFF_BAR = OFF_S + NBUF * NCH * NPOLE * 4;
   static constexpr int N_BARS = 2 * STAGES + 8 + 6 * NBUF;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
@@ -116,6 +122,9 @@ struct Params {
   const float* feat_taps;  // fused: (3, C, lhf), per channel
   const bf16* fpack;       // fused: packed featurizer matrices, (C, 3, KS, 256) bf16, or null
   const bf16* hist;        // fused: (B, 3C, HIST) projections before t = 0, or null (zeros)
+  const float* poles;      // implicit: (n_groups, npoles)
+  const float* residues;   // implicit: (n_groups, npoles)
+  int npoles;
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
@@ -192,7 +201,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // KS: K-steps of 16 in the featurizer GEMM (1 for lhf <= 9, 2 for lhf <= 16).
-template <bool FEAT, bool GK, bool GQ, int KS>
+// IMPL: implicit long filter h_t = sum_n R_n lam_n^t (Hyena-LI): the intra-chunk part is the
+// T0 MMA over h[0..127]; every longer lag goes through the exact per-mode recurrence
+// s_n[t] = lam_n s_n[t-1] + u[t] carried chunk to chunk (E = per-chunk mode inputs,
+// S_prev = state entering each chunk) and applied by one tf32 MMA, P . S_prev.
+template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL>
 __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   using LY = Layout<KS>;
   constexpr int STAGES = LY::STAGES;
@@ -216,8 +229,11 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tb = static_cast<int>((static_cast<long long>(blockIdx.x) * p.total_tiles) / gridDim.x);
-  const int te = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * p.total_tiles) / gridDim.x);
+  // IMPL carries the recurrence state from tile to tile, so a CTA owns whole sequences
+  const int units = IMPL ? p.total_tiles / p.tiles_per_seq : p.total_tiles;
+  const int per = IMPL ? p.tiles_per_seq : 1;
+  const int tb = per * static_cast<int>((static_cast<long long>(blockIdx.x) * units) / gridDim.x);
+  const int te = per * static_cast<int>((static_cast<long long>(blockIdx.x + 1) * units) / gridDim.x);
   const int ntiles = te - tb;
 
   if (threadIdx.x == 0) {
@@ -399,8 +415,24 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           if (elect_one()) mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           __syncwarp();
         }
+        if (IMPL) {
+          // inter-chunk term of the implicit filter: D[t][c] += sum_n P[t][n] S_prev[c][n] (tf32)
+          constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
+          const uint32_t pa = smem_u32(smem + LY::OFF_P);
+          const uint32_t sa = smem_u32(smem + LY::OFF_S + u * NCH * NPOLE * 4);
+          if (elect_one()) mma_tf32(d, desc_noswz(pa, 128, 256), desc_noswz(sa, 128, 256), idesc_tf32, 1u);
+          __syncwarp();
+        }
         if (last && elect_one()) mma_commit(&tfree[0]);
         __syncwarp();
+        if (IMPL) {
+          if (elect_one()) {
+            mma_commit(&uempty[u]);
+            mma_commit(&tfull[u]);
+          }
+          __syncwarp();
+          continue;
+        }
         if (first) {
           mbar_wait(&tready[1], gi & 1);
           tc_fence_after();
@@ -428,9 +460,26 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     // M-blocks of this warp: k / v blocks half, half+2, half+4; q blocks half, half+2
     constexpr int KVB_PER = (KV_MB + 1) / 2, QB_PER = Q_MB / 2;
-    for (int it = 0; it < ntiles; ++it) {
+    // IMPL: per-group mode constants. lam[n]; lamj[n] = lam^(120 - 8j) for this lane's 16-B
+    // unit j = lane % 16 (scales a unit's Horner sum to the chunk end); the scan lanes
+    // (converter warp 0, lane n < NPOLE) also keep lam^128 and the carried state.
+    float lam[NPOLE], lamj[NPOLE], lam128 = 0.f, carry = 0.f;
+    int cur_g = -1;
+    Tile t;
+    t.init(tb, p);
+    for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int u = it % NBUF;
       const uint32_t uph = (it / NBUF) & 1;
+      if (IMPL && t.c / p.gs != cur_g) {
+        cur_g = t.c / p.gs;
+        const int jj = lane & 15;
+#pragma unroll
+        for (int n = 0; n < NPOLE; ++n) {
+          lam[n] = n < p.npoles ? p.poles[static_cast<size_t>(cur_g) * p.npoles + n] : 0.f;
+          lamj[n] = powf(lam[n], static_cast<float>(120 - 8 * jj));
+        }
+        if (ctid < NPOLE) lam128 = powf(lam[ctid], 128.f);
+      }
       // 1) drain the featurized k / v / q of this tile from TMEM into registers and
       //    release the single featurizer buffer for the next tile's MMAs at once
       mbar_wait(&ffull[0], it & 1);
@@ -460,19 +509,57 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (ctid == 0) trace(p, it, 2);
       unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
       unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
+      float* ebuf = reinterpret_cast<float*>(smem + LY::OFF_E);
 #pragma unroll
       for (int i = 0; i < KVB_PER; ++i) {
         const int b = half + 2 * i;
         const int m = b * 128 + quarter * 32 + lane;
-        if (b < KV_MB && m < KV_WIN) {
-          float uv[8];
+        if (!(b < KV_MB && b * 128 + quarter * 32 < KV_WIN)) continue;  // warp-uniform
+        const int n = m / 16 - 1, j = m % 16;
+        float uv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            uv[e] = GK ? __uint_as_float(rv[i][e]) * __uint_as_float(rk[i][e]) : __uint_as_float(rv[i][e]);
+        for (int e = 0; e < 8; ++e)
+          uv[e] = GK ? __uint_as_float(rv[i][e]) * __uint_as_float(rk[i][e]) : __uint_as_float(rv[i][e]);
+        if (m < KV_WIN) {
           const int4 packed = pack8(uv);
-          const int n = m / 16 - 1, j = m % 16;
           if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
-          if (n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
+          if (!IMPL && n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
+        }
+        if (IMPL) {
+          // mode inputs of chunk n: E[n][k] = sum_t lam_k^(127 - t) u[t] (chunk-local t);
+          // per unit: Horner over its 8 samples, scaled by lam^(120 - 8j), then summed over
+          // the chunk's 16 units (16 consecutive lanes) with shuffles
+          const bool valid = n >= 0 && m < KV_WIN;
+          float e8[NPOLE];
+#pragma unroll
+          for (int k = 0; k < NPOLE; ++k) {
+            float a = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) a = fmaf(a, lam[k], uv[e]);
+            a = valid ? a * lamj[k] : 0.f;
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+            e8[k] = a;
+          }
+          if (valid && j == 0) {
+            *reinterpret_cast<float4*>(ebuf + n * NPOLE) = make_float4(e8[0], e8[1], e8[2], e8[3]);
+            *reinterpret_cast<float4*>(ebuf + n * NPOLE + 4) = make_float4(e8[4], e8[5], e8[6], e8[7]);
+          }
+        }
+      }
+      if (IMPL) {
+        // sequential scan over the tile's chunks (lanes = modes): the state entering chunk c
+        // is written as the tf32 B operand S_prev[c][n] (element (c, n) of a no-swizzle
+        // K-major tile at (c%8)*16 + (c/8)*256 + (n%4)*4 + (n/4)*128 bytes)
+        named_bar_sync(BAR_CONV, CONV_THREADS);
+        if (ctid < NPOLE) {
+          float* sp = reinterpret_cast<float*>(smem + LY::OFF_S + u * NCH * NPOLE * 4);
+          float st = t.t0 == 0 ? 0.f : carry;
+          for (int c = 0; c < NCH; ++c) {
+            sp[((c & 7) * 16 + (c >> 3) * 256 + (ctid & 3) * 4 + (ctid >> 2) * 128) / 4] = st;
+            st = fmaf(lam128, st, ebuf[c * NPOLE + ctid]);
+          }
+          carry = st;
         }
       }
       fence_proxy_async();
@@ -532,8 +619,18 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const int bt = threadIdx.x - W_TB0 * 32;
     constexpr int PER = 512 / TB_THREADS;  // hpad entries per thread
     float pf_h[PER], pf_dec = 0.f;
+    float pf_pole[NPOLE], pf_res[NPOLE];  // IMPL: the group's modes
     // raw loads of a group's taps; the decay is applied at use so the loads stay in flight
     auto prefetch = [&](int g) {
+      if (IMPL) {
+#pragma unroll
+        for (int n = 0; n < NPOLE; ++n) {
+          const bool ok = n < p.npoles;
+          pf_pole[n] = ok ? p.poles[static_cast<size_t>(g) * p.npoles + n] : 0.f;
+          pf_res[n] = ok ? p.residues[static_cast<size_t>(g) * p.npoles + n] : 0.f;
+        }
+        return;
+      }
       pf_dec = p.decay ? p.decay[g] : 0.f;
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
@@ -572,6 +669,32 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       const int g = t.c / p.gs;
       if (g == g_prev) continue;
       g_prev = g;
+      if (IMPL) {
+        // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states)
+        // and P[m][n] = R_n lam_n^(m+1) as the tf32 A operand: element (m, n) at
+        // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes
+        if (gi > 0) mbar_wait(&tfree[0], (gi - 1) & 1);
+        float hv = 0.f, pm[NPOLE];
+#pragma unroll
+        for (int n = 0; n < NPOLE; ++n) {
+          const float lt = powf(pf_pole[n], static_cast<float>(bt));
+          hv = fmaf(pf_res[n], lt, hv);
+          pm[n] = pf_res[n] * lt * pf_pole[n];
+        }
+        hpad[bt] = __float2bfloat16_rn(0.f);
+        hpad[128 + bt] = __float2bfloat16_rn(hv);
+        hpad[256 + bt] = __float2bfloat16_rn(0.f);
+        hpad[384 + bt] = __float2bfloat16_rn(0.f);
+        float* pa = reinterpret_cast<float*>(smem + LY::OFF_P + (bt & 7) * 16 + (bt >> 3) * 256);
+        *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
+        *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
+        fence_proxy_async();
+        named_bar_sync(BAR_TB, TB_THREADS);
+        build(0);
+        if (g < g_end) prefetch(g + 1);
+        ++gi;
+        continue;
+      }
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
         const int tt = bt + r * TB_THREADS - 128;
@@ -594,9 +717,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   if (warp == W_MMA) tmem_dealloc<512>(tmem_base);
 }
 
-template <bool FEAT, bool GK, bool GQ, int KS>
+template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL = false>
 static int launch_ks(const Params& p, cudaStream_t st) {
-  auto kern = two_stage_kernel<FEAT, GK, GQ, KS>;
+  auto kern = two_stage_kernel<FEAT, GK, GQ, KS, IMPL>;
   constexpr int smem = Layout<KS>::SMEM_BYTES;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -607,17 +730,18 @@ static int launch_ks(const Params& p, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = p.total_tiles < sms ? p.total_tiles : sms;
+  const int units = IMPL ? p.total_tiles / p.tiles_per_seq : p.total_tiles;  // IMPL: whole sequences
+  const int grid = units < sms ? units : sms;
   kern<<<grid, THREADS, smem, st>>>(p);
   return check_launch("two_stage_kernel");
 }
 
-template <bool FEAT, bool GK, bool GQ>
+template <bool FEAT, bool GK, bool GQ, bool IMPL = false>
 static int launch(Params p, cudaStream_t st) {
   static const int tr = [] { const char* e = getenv("HY_TS_TRACE"); return e ? atoi(e) : 0; }();
   p.trace = tr;
-  if (p.lhf <= 9) return launch_ks<FEAT, GK, GQ, 1>(p, st);
-  return launch_ks<FEAT, GK, GQ, 2>(p, st);
+  if (p.lhf <= 9) return launch_ks<FEAT, GK, GQ, 1, IMPL>(p, st);
+  return launch_ks<FEAT, GK, GQ, 2, IMPL>(p, st);
 }
 
 int check_shapes(int B, int C, int L, int lh, int gs) {
@@ -684,6 +808,68 @@ int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const vo
   p.tiles_per_seq = (L + ts::TILE_T - 1) / ts::TILE_T;
   p.total_tiles = p.tiles_per_seq * B * C;
   return ts::launch<true, true, true>(p, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- implicit long filter (Hyena-LI)
+
+static int check_impl(const void* residues, const void* poles, int npoles, int B, int C, int L, int gs) {
+  if (!residues || !poles) return fail(HY_ERR_INVALID, "null residues / poles");
+  if (npoles < 1 || npoles > ts::NPOLE) return fail(HY_ERR_UNSUPPORTED, "implicit filter needs 1..%d poles", ts::NPOLE);
+  return ts::check_shapes(B, C, L, 1, gs);
+}
+
+// LI mixer: featurizers + u = k*v + implicit long conv + q gate, bf16 (hyena.py:162-186, LI).
+extern "C" HY_API int hy_li_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack,
+                                      int lhf, const float* residues, const float* poles, int npoles, int gs,
+                                      int B, int C, int L, int dtype, void* stream) {
+  if (dtype != HY_BF16) return fail(HY_ERR_UNSUPPORTED, "hy_li_mixer_fwd: tcgen05 path is bf16 only");
+  if (!proj || !y || !feat_taps || !feat_pack) return fail(HY_ERR_INVALID, "null pointer argument");
+  int s = check_impl(residues, poles, npoles, B, C, L, gs);
+  if (s != HY_OK) return s;
+  if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
+  if (!aligned16(proj) || !aligned16(y) || !aligned16(feat_pack))
+    return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  ts::Params p{};
+  p.proj = static_cast<const ts::bf16*>(proj);
+  p.y = static_cast<ts::bf16*>(y);
+  p.feat_taps = feat_taps;
+  p.fpack = static_cast<const ts::bf16*>(feat_pack);
+  p.poles = poles;
+  p.residues = residues;
+  p.npoles = npoles;
+  p.B = B, p.C = C, p.L = L, p.lh = 1, p.gs = gs, p.lhf = lhf;
+  p.tiles_per_seq = (L + ts::TILE_T - 1) / ts::TILE_T;
+  p.total_tiles = p.tiles_per_seq * B * C;
+  return ts::launch<true, true, true, true>(p, static_cast<cudaStream_t>(stream));
+}
+
+// Gated implicit long conv y = q * (h conv (k * v)), h_t = sum_n R_n lam_n^t over the whole
+// sequence (fft.py:128-145 on an ImplicitFilter, core.py:147-151); q / k may be NULL.
+extern "C" HY_API int hy_li_conv_fwd(const void* q, const void* k, const void* v, void* y, const float* residues,
+                                     const float* poles, int npoles, int gs, int B, int C, int L, int dtype,
+                                     void* stream) {
+  if (dtype != HY_BF16) return fail(HY_ERR_UNSUPPORTED, "hy_li_conv_fwd: tcgen05 path is bf16 only");
+  if (!v || !y) return fail(HY_ERR_INVALID, "null pointer argument");
+  int s = check_impl(residues, poles, npoles, B, C, L, gs);
+  if (s != HY_OK) return s;
+  if (!aligned16(v) || !aligned16(y) || (q && !aligned16(q)) || (k && !aligned16(k)))
+    return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  ts::Params p{};
+  p.q = static_cast<const ts::bf16*>(q);
+  p.k = static_cast<const ts::bf16*>(k);
+  p.v = static_cast<const ts::bf16*>(v);
+  p.y = static_cast<ts::bf16*>(y);
+  p.poles = poles;
+  p.residues = residues;
+  p.npoles = npoles;
+  p.B = B, p.C = C, p.L = L, p.lh = 1, p.gs = gs, p.lhf = 1;
+  p.tiles_per_seq = (L + ts::TILE_T - 1) / ts::TILE_T;
+  p.total_tiles = p.tiles_per_seq * B * C;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (q && k) return ts::launch<false, true, true, true>(p, st);
+  if (k) return ts::launch<false, true, false, true>(p, st);
+  if (q) return ts::launch<false, false, true, true>(p, st);
+  return ts::launch<false, false, false, true>(p, st);
 }
 
 // Debug: copy the CTA-0 timeline of the last traced two-stage launch (HY_TS_TRACE=1).

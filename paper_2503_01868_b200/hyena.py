@@ -162,8 +162,16 @@ class HyenaOperator:
         self.gs = inner.group_size
         self.lh = inner.filter_len
         self.decay = None
+        self.li_modes = None
         if isinstance(inner.filters[0], ImplicitFilter):
-            self.inner_taps = _implicit_taps_device(inner, self.dev, tdt)
+            self.inner_taps = None  # materialised lazily (unfused / fp32 / fp64 paths only)
+            npoles = {f.poles.size for f in inner.filters}
+            if dtype == torch.bfloat16 and len(npoles) == 1 and max(npoles) <= 8:
+                # (residues, poles) per group for the tcgen05 implicit-filter kernel
+                self.li_modes = (torch.tensor(np.stack([f.residues for f in inner.filters]), dtype=torch.float32,
+                                              device=self.dev),
+                                 torch.tensor(np.stack([f.poles for f in inner.filters]), dtype=torch.float32,
+                                              device=self.dev))
         elif isinstance(inner.filters[0], RegularizedFilter) and dtype != torch.float64:
             # taps_hat + per-group rate*log2(base): the decay is applied inside the kernels
             self.inner_taps = torch.from_numpy(np.stack([f.taps_hat for f in inner.filters])).to(self.dev, tdt)
@@ -175,6 +183,8 @@ class HyenaOperator:
 
     @property
     def materialized_inner(self) -> torch.Tensor:
+        if self.inner_taps is None:
+            self.inner_taps = _implicit_taps_device(self.cfg.inner, self.dev, ops.tap_dtype(self.dtype))
         if self.decay is None:
             return self.inner_taps
         if self._mat_taps is None:
@@ -185,6 +195,9 @@ class HyenaOperator:
     def mixer(self, proj: torch.Tensor) -> torch.Tensor:
         """q * inner(k * v) from the (B, 3D, L) projections."""
         D = self.cfg.width
+        if self.li_modes is not None and proj.shape[-1] % 8 == 0:
+            return ops.li_mixer(proj, self.feat_taps, self.li_modes[0], self.li_modes[1], self.gs,
+                                packed=self.feat_packed)
         fused_ok = (self.dtype == torch.bfloat16 and self.lh <= 129) or \
                    (self.dtype in (torch.float32, torch.bfloat16) and self.lh <= 16)
         if fused_ok:

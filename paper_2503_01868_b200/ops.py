@@ -205,3 +205,46 @@ def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, 
         return fft_conv(v, taps, group_size, q=q, k=k)
     except NotImplementedError:
         return gated_conv(v, taps, group_size, q=q, k=k)
+
+
+def _modes(residues: torch.Tensor, poles: torch.Tensor, dev):
+    r = residues.to(device=dev, dtype=torch.float32).contiguous()
+    p = poles.to(device=dev, dtype=torch.float32).contiguous()
+    if r.shape != p.shape or r.dim() != 2:
+        raise ValueError("residues and poles must be matching (n_groups, n_poles) tensors")
+    return r, p
+
+
+def li_conv(v: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_size: int = 1, q=None,
+            k=None) -> torch.Tensor:
+    """y = q * (h conv (k * v)) with h_t = sum_n R_n lam_n^t over the whole sequence (tcgen05, bf16)."""
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    if v3.dtype != torch.bfloat16:
+        raise ValueError("li_conv (tcgen05) takes bfloat16 activations")
+    r, p = _modes(residues, poles, v3.device)
+    B, C, L = v3.shape
+    y = torch.empty_like(v3)
+    lib = _lib.load()
+    _lib.check(lib.hy_li_conv_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), r.data_ptr(), p.data_ptr(),
+                                  p.shape[1], group_size, B, C, L, _lib.HY_BF16, _stream()), "li_conv")
+    return y[0] if squeeze else y
+
+
+def li_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor,
+             group_size: int, packed=None) -> torch.Tensor:
+    """Hyena-LI mixer from the (B, 3C, L) projections: featurizers, gates, implicit long conv."""
+    _check_device(proj)
+    B, C3, L = proj.shape
+    C = C3 // 3
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    if packed is None:
+        packed = feat_pack(ft)
+    r, p = _modes(residues, poles, proj.device)
+    y = torch.empty((B, C, L), device=proj.device, dtype=proj.dtype)
+    lib = _lib.load()
+    _lib.check(lib.hy_li_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), packed.data_ptr(), ft.shape[-1],
+                                   r.data_ptr(), p.data_ptr(), p.shape[1], group_size, B, C, L,
+                                   _dtype_code(proj), _stream()), "li_mixer")
+    return y

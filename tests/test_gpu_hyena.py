@@ -114,3 +114,25 @@ def test_operator_bf16_vs_oracle(variant, B, D, L, kw):
         want = oracle.hyena_forward(x[b], ocfg)
         err = oracle.rel_err(y[b], want)
         assert err < 1e-2, (b, err)
+
+
+def test_li_operator_bf16_vs_oracle():
+    """Hyena-LI operator (bf16, tcgen05 implicit-filter mixer) vs the fp64 oracle (fft backend)."""
+    D, L = 32, 8192
+    cfg = hy.make_hyena_config("LI", D, hy.make_rng(5), seq_len=L, backend="fft")
+    rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+    feats = {n: hy.GroupSpec(D, 1, tuple(hy.ExplicitFilter(bf16_round(f.taps)) for f in getattr(cfg, n).filters))
+             for n in ("q_feat", "k_feat", "v_feat")}
+    inner = hy.GroupSpec(D, 1, tuple(hy.ImplicitFilter(f.residues, np.clip(f.poles * 1.05, -1, 1), L)
+                                     for f in cfg.inner.filters))
+    cfg = hy.HyenaConfig(**{**cfg.__dict__, **rnd, **feats, "inner": inner})
+    x = bf16_round(hy.make_rng(9).standard_normal((D, L)))
+    y = hy.HyenaOperator(cfg, torch.bfloat16).forward(torch.from_numpy(x).to("cuda", torch.bfloat16))
+    ocfg = {"variant": "LI", "width": D, "block_size": 16, "backend": "fft",
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")},
+            **{n: {"channels": D, "group_size": 1, "filters": [("explicit", f.taps) for f in getattr(cfg, n).filters]}
+               for n in ("q_feat", "k_feat", "v_feat")},
+            "inner": {"channels": D, "group_size": 1,
+                      "filters": [("implicit", f.residues, f.poles, L) for f in inner.filters]}}
+    want = oracle.hyena_forward(x, ocfg)
+    assert oracle.rel_err(y.float().cpu().numpy(), want) < 1e-2

@@ -243,3 +243,48 @@ def test_halo_correction_matches_overlap_scheme():
     y = ops.causal_conv(dev(local, torch.float64), dev(taps, torch.float64), 1)
     ops.halo_correction(dev(halo, torch.float64), y, dev(taps, torch.float64), 1)
     assert oracle.rel_err(y.cpu().numpy(), want) < 1e-12
+
+
+# ---------------------------------------------------------------- implicit long filter (LI)
+
+
+def _implicit_bank(residues, poles, L, gs):
+    return {"channels": residues.shape[0] * gs, "group_size": gs,
+            "filters": [("implicit", r, p, L) for r, p in zip(residues, poles)]}
+
+
+@pytest.mark.parametrize("B,C,L,gs,gated", [(1, 4, 8192, 1, True), (2, 3, 12288, 1, True), (1, 4, 4096, 2, False),
+                                            (1, 2, 5000 // 8 * 8, 1, True)])
+def test_li_conv_vs_oracle(B, C, L, gs, gated):
+    rng = np.random.default_rng(L + C)
+    G = C // gs
+    poles = rng.uniform(-0.95, 0.95, (G, 8))
+    poles[0, :4] = [0.999, -0.999, 1.0, -1.0]  # the long tail (SURVEY 7.4 hard part 5)
+    poles[-1, 0] = 0.0
+    residues = rng.standard_normal((G, 8)) / 8
+    v = bf16_round(rng.standard_normal((B, C, L)))
+    q = bf16_round(rng.standard_normal((B, C, L))) if gated else None
+    k = bf16_round(rng.standard_normal((B, C, L))) if gated else None
+    y = ops.li_conv(dev(v, torch.bfloat16), dev(residues), dev(poles), gs,
+                    q=None if q is None else dev(q, torch.bfloat16),
+                    k=None if k is None else dev(k, torch.bfloat16)).float().cpu().numpy()
+    taps = oracle.bank_taps_per_channel(_implicit_bank(residues, poles, L, gs))
+    for b in range(B):
+        u = v[b] * (k[b] if gated else 1.0)
+        want = oracle.fft_conv(u, taps) * (q[b] if gated else 1.0)
+        err = oracle.rel_err(y[b], want)
+        assert err < TOL["bf16"], (b, err)
+
+
+def test_li_conv_many_sequences_per_cta():
+    # more sequences than SMs: each CTA walks several sequences and must reset the carried state
+    rng = np.random.default_rng(11)
+    C, L = 320, 4096
+    poles = rng.uniform(-0.99, 0.99, (C, 8))
+    residues = rng.standard_normal((C, 8)) / 8
+    v = bf16_round(rng.standard_normal((1, C, L)))
+    y = ops.li_conv(dev(v, torch.bfloat16), dev(residues), dev(poles), 1).float().cpu().numpy()
+    taps = oracle.bank_taps_per_channel(_implicit_bank(residues, poles, L, 1))
+    sel = [0, 1, 147, 148, 149, 200, 319]
+    want = oracle.fft_conv(v[0][sel], taps[sel])
+    assert oracle.rel_err(y[0][sel], want) < TOL["bf16"]
