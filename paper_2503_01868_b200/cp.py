@@ -337,7 +337,8 @@ class HyenaCP:
     def _fused(self) -> bool:
         return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
 
-    def forward(self, x_local: torch.Tensor) -> torch.Tensor:
+    def forward(self, x_local: torch.Tensor, events=None) -> torch.Tensor:
+        """events: optional (start, end) CUDA events recorded around the mixer / local conv."""
         from . import _lib, ops
         op, grp = self.op, self.grp
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
@@ -347,12 +348,18 @@ class HyenaCP:
             hist, reqs = _exchange_halo(proj, _lib.MIXER_HISTORY, grp, "cp_hist")
             for q in reqs:
                 q.wait()
+            if events is not None:
+                events[0].record()
             mixed = ops.hyena_mixer(proj, op.feat_taps, op.inner_taps, op.gs, decay=op.decay,
                                     packed=op.feat_packed, hist=hist if grp.rank > 0 else None)
+            if events is not None:
+                events[1].record()
         else:
             # featurizers over the 3D projected rows with their (lhf-1)-step halo
             ft = op.feat_taps.reshape(3 * D, op.lhf)
-            feat_groups = _per_channel_groups(ft)
+            if getattr(self, "_feat_groups", None) is None:
+                self._feat_groups = _per_channel_groups(ft)
+            feat_groups = self._feat_groups
             feats = p2p_conv_overlapped(proj, feat_groups, grp,
                                         conv=lambda z: ops.causal_conv(z.contiguous(), ft, 1),
                                         correct=lambda h, y: _correct(h, y, ft, 1))
@@ -360,7 +367,13 @@ class HyenaCP:
             u = k * v
             taps = op.materialized_inner
             if self.cfg.variant == "LI":
-                conv = torch.stack([a2a_conv(u[b], self.cfg.inner, grp) for b in range(B)])
+                slab_conv = _li_slab_conv(op) if op.li_modes is not None else None
+                if events is not None:
+                    events[0].record()
+                conv = torch.stack([a2a_conv(u[b].contiguous(), self.cfg.inner, grp, conv_slab=slab_conv)
+                                    for b in range(B)])
+                if events is not None:
+                    events[1].record()
             else:
                 conv = p2p_conv_overlapped(u, self.cfg.inner, grp,
                                            conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
@@ -370,6 +383,26 @@ class HyenaCP:
         return y[0] if x_local.dim() == 2 else y
 
     __call__ = forward
+
+
+def _li_slab_conv(op):
+    """Implicit long conv of a channel slab over the full sequence (tcgen05 li_conv)."""
+    from . import ops
+    res, poles = op.li_modes
+
+    def conv(natural, slab_groups):
+        g0 = _group_index(op.cfg.inner, slab_groups)
+        ng = slab_groups.n_groups
+        return ops.li_conv(natural.contiguous(), res[g0:g0 + ng], poles[g0:g0 + ng], slab_groups.group_size)
+    return conv
+
+
+def _group_index(bank: GroupSpec, sub: GroupSpec) -> int:
+    first = sub.filters[0]
+    for i, f in enumerate(bank.filters):
+        if f is first:
+            return i
+    raise ValueError("slab filters not found in the operator's bank")
 
 
 def _correct(halo, y, taps, gs):

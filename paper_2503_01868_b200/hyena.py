@@ -211,7 +211,8 @@ class HyenaOperator:
             return ops.long_conv(v, self.materialized_inner, self.gs, q=q, k=k)
         return ops.gated_conv(v, self.materialized_inner, self.gs, q=q, k=k)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, events=None) -> torch.Tensor:
+        """events: optional (start, end) CUDA events recorded around the mixer kernel."""
         squeeze = x.dim() == 2
         x3 = x.unsqueeze(0) if squeeze else x
         if x3.shape[1] != self.cfg.width:
@@ -222,7 +223,11 @@ class HyenaOperator:
         if x3.dtype != self.dtype:
             raise ValueError(f"operator packed for {self.dtype}, got {x3.dtype}")
         proj = torch.matmul(self.w_qkv_t, x3)
+        if events is not None:
+            events[0].record()
         mixed = self.mixer(proj)
+        if events is not None:
+            events[1].record()
         y = torch.matmul(self.w_out_t, mixed)
         return y[0] if squeeze else y
 

@@ -67,7 +67,7 @@ def _cp_worker(rank, world, port, variant, q):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("variant", ["MR", "SE"])
+@pytest.mark.parametrize("variant", ["MR", "SE", "LI"])
 def test_hyena_cp_matches_single_gpu(variant):
     import torch.multiprocessing as mp
     world = min(torch.cuda.device_count(), 4)
