@@ -36,11 +36,27 @@ if ROOT not in sys.path:
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 WORKLOADS = {
-    "mr": dict(variant="MR", B=4, L=8192, D=4096, inner_len=128, block_size=128,
+    # N=1: BASELINE.json configs[1]; N>1: the same per-rank shard, context-parallel over a
+    # sequence of N x 8192 tokens (weak scaling, 144-step p2p history between ranks)
+    "mr": dict(kind="op", variant="MR", B=4, L=8192, D=4096, inner_len=128, block_size=128, dtype="bf16",
                desc="Hyena-MR operator fwd (filter len 128, blocked T0/T1), B=4, L=8192, D=4096, bf16"),
-    "se": dict(variant="SE", B=1, L=4096, D=4096, inner_len=7, block_size=16,
-               desc="Hyena-SE operator fwd (filter len 7), B=1, L=4096, D=4096, bf16"),
+    "se": dict(kind="op", variant="SE", B=1, L=4096, D=4096, inner_len=7, block_size=16, dtype="f32",
+               desc="Hyena-SE operator fwd (filter len 7), B=1, L=4096, D=4096, fp32"),
+    "li": dict(kind="op", variant="LI", B=1, L=131072, D=4096, inner_len=None, block_size=128, dtype="bf16",
+               desc="Hyena-LI operator fwd (implicit long filter, 8 poles), B=1, L=131072, D=4096, bf16"),
+    "stripe": dict(kind="stripe", B=1, L=16384, D=4096, dtype="bf16",
+                   desc="StripedHyena 2 stripe fwd (SE-MR-LI-MHA, residual), B=1, L=16384, D=4096, bf16"),
+    # BASELINE.json configs[4]: L = 1M over N ranks (strong scaling), LI all-to-all
+    "li_cp": dict(kind="cp", variant="LI", B=1, L=1 << 20, D=4096, inner_len=None, block_size=128,
+                  dtype="bf16", desc="Context-parallel Hyena-LI operator fwd, L=1M, D=4096, bf16 "
+                                     "(all-to-all sequence <-> channel sharding)"),
 }
+
+# algorithmic HBM bytes per token of the fused mixer kernels: 3 projected rows in + 1 out
+MIXER_KERNEL = {"MR": "two_stage_kernel<FEAT> (hy_hyena_mixer_fwd: featurizers + gates + tcgen05 T0/T1)",
+                "SE": "se_mixer_kernel (hy_hyena_mixer_fwd: featurizers + gates + short conv)",
+                "LI": "two_stage_kernel<FEAT,IMPL> (hy_li_mixer_fwd: featurizers + gates + implicit long conv)"}
+MIXER_NCU_NAME = {"MR": "two_stage_kernel", "SE": "se_mixer_kernel", "LI": "two_stage_kernel"}
 
 
 def load_peaks():
@@ -111,14 +127,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_traffic(workload: str):
+    """dram read+write bytes per launch of the workload's dominant kernel, from the committed
+    ncu --set full summaries (profiles/ncu_traffic.json, written by scripts/ncu_summary.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
     except OSError:
         return None
-    vals = [v["traffic_bytes"] for k, v in sorted(d.items()) if v.get("kernel") == kernel]
+    vals = [v["traffic_bytes"] for k, v in sorted(d.items()) if v.get("workload") == workload]
     return vals[-1] if vals else None
 
 
@@ -129,175 +146,287 @@ def dist_env():
     return ws, rank, local
 
 
-def build_config(wl: dict):
+def build_config(wl: dict, variant=None, L=None):
     import paper_2503_01868_b200 as hy
-    return hy.make_hyena_config(wl["variant"], wl["D"], hy.make_rng(0), seq_len=wl["L"], group_size=1,
-                                inner_len=wl["inner_len"], block_size=wl["block_size"])
+    return hy.make_hyena_config(variant or wl["variant"], wl["D"], hy.make_rng(0), seq_len=L or wl["L"],
+                                group_size=1, inner_len=wl.get("inner_len"), block_size=wl.get("block_size", 16))
+
+
+def _max_over_ranks(ms: float, ws: int) -> float:
+    import torch
+    import torch.distributed as dist
+    if ws == 1:
+        return ms
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Runner:
+    """One workload on this rank: device-resident input, a step with kernel events, the
+    public-API forward used for e2e, and the accounting the JSON line needs."""
+
+    def __init__(self, wl, ws, rank):
+        import torch
+        import paper_2503_01868_b200 as hy
+        from paper_2503_01868_b200 import cp
+        from paper_2503_01868_b200.stripe import Stripe
+
+        self.wl, self.ws, self.rank = wl, ws, rank
+        dt = {"bf16": torch.bfloat16, "f32": torch.float32}[wl["dtype"]]
+        self.esize = 2 if dt == torch.bfloat16 else 4
+        B, D, L = wl["B"], wl["D"], wl["L"]
+        kind = wl["kind"]
+        self.kernels = []  # (label, variant, algorithmic bytes per launch)
+        if kind == "op" and ws == 1:
+            op = hy.HyenaOperator(build_config(wl), dt)
+            self.m = L
+            self.fwd = lambda x, ev=None: op.forward(x, events=None if ev is None else ev[0])
+            self.kernels = [(wl["variant"], wl["variant"], 4 * self.esize * D * B * L)]
+            self.parallelism = "single"
+            self.l_global = L
+        elif kind == "op":  # context parallel, weak scaling: N x 8192-token shards of one sequence
+            if wl["variant"] != "MR":
+                raise SystemExit(f"workload {wl['variant']} has no multi-GPU mode; use mr or li_cp")
+            mod = cp.HyenaCP(build_config(wl, L=L * ws), dt)
+            self.m = L
+            self.fwd = lambda x, ev=None: mod.forward(x, events=None if ev is None else ev[0])
+            self.kernels = [("MR", "MR", 4 * self.esize * D * B * L)]
+            self.parallelism = f"cp{ws} (sequence sharded {L} tokens/rank, 144-step p2p history)"
+            self.l_global = L * ws
+        elif kind == "stripe":
+            cfgs = [build_config(dict(wl, inner_len=ln, block_size=128), variant=v)
+                    for v, ln in (("SE", 7), ("MR", 128), ("LI", None))]
+            st = Stripe(cfgs, dt)
+            self.m = L
+            self.fwd = lambda x, ev=None: st.forward(x, events=ev)
+            self.kernels = [(v, v, 4 * self.esize * D * B * L) for v in ("SE", "MR", "LI")]
+            self.parallelism = "single"
+            self.l_global = L
+        elif kind == "cp":  # strong scaling: L tokens over ws ranks
+            if L % ws:
+                raise SystemExit("sequence not divisible by the rank count")
+            mod = cp.HyenaCP(build_config(wl), dt)
+            self.m = L // ws
+            self.fwd = lambda x, ev=None: mod.forward(x, events=None if ev is None else ev[0])
+            # the slab long conv (ungated li_conv): D/ws channels x L tokens, in + out
+            self.kernels = [("LI slab conv", "LI", 2 * self.esize * (D // ws) * B * L)]
+            self.parallelism = f"cp{ws} (sequence sharded, all-to-all to channel slabs for the long conv)"
+            self.l_global = L
+        self.B, self.D, self.dt = B, D, dt
+        gen = torch.Generator(device="cuda").manual_seed(1 + rank)
+        self.x = torch.randn((B, D, self.m), device="cuda", dtype=dt, generator=gen)
+        self.tokens_step = B * self.l_global
+        self.op_flops = 8 * D * D * B * self.l_global * (3 if kind == "stripe" else 1)
+        if kind == "stripe":
+            self.op_flops += 8 * D * D * B * L // 2 + 2 * B * L * L * D  # MHA projections + causal attention
+
+    def step(self, ev=None):
+        return self.fwd(self.x, ev)
 
 
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
 
-    import paper_2503_01868_b200 as hy
+    from paper_2503_01868_b200 import _lib
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    B, D, L = wl["B"], wl["D"], wl["L"]
-    cfg = build_config(wl)
-    op = hy.HyenaOperator(cfg, torch.bfloat16)
-    gen = torch.Generator(device="cuda").manual_seed(1 + rank)
-    x = torch.randn((B, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
+    if ws > 1 or wl["kind"] == "cp":
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=torch.device("cuda", local))
+    run = Runner(wl, ws, rank)
     stream = torch.cuda.current_stream()
-
-    def step(ev=None):
-        proj = torch.matmul(op.w_qkv_t, x)
-        if ev is not None:
-            ev[0].record(stream)
-        mixed = op.mixer(proj)
-        if ev is not None:
-            ev[1].record(stream)
-        return torch.matmul(op.w_out_t, mixed)
+    nk = len(run.kernels)
 
     for _ in range(args.warmup):
-        step()
+        run.step()
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist.is_initialized():
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nk)]
+           for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
     t0.record(stream)
     for i in range(args.steps):
-        step(evs[i])
+        run.step(evs[i])
     t1.record(stream)
     torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
     clocks = sampler.stop()
-    ms_total = t0.elapsed_time(t1)
-    mixer_ms = [a.elapsed_time(b) for a, b in evs]
-    if ws > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_step = _max_over_ranks(t0.elapsed_time(t1), ws) / args.steps
+    kern_ms = [statistics.mean(evs[i][j][0].elapsed_time(evs[i][j][1]) for i in range(args.steps))
+               for j in range(nk)]
+    if dist.is_initialized():
         dist.barrier()
-    ms_step = ms_total / args.steps
 
     # ---- end to end through the public API: pinned host x -> device -> forward -> host y
-    xh = torch.empty((B, D, L), dtype=torch.bfloat16, pin_memory=True)
-    xh.copy_(x.cpu())
-    yh = torch.empty((B, D, L), dtype=torch.bfloat16, pin_memory=True)
+    xh = torch.empty(tuple(run.x.shape), dtype=run.dt, pin_memory=True)
+    xh.copy_(run.x.cpu())
+    yh = torch.empty(tuple(run.x.shape), dtype=run.dt, pin_memory=True)
     for _ in range(max(1, args.warmup)):
-        yh.copy_(op.forward(xh.to("cuda", non_blocking=True)), non_blocking=True)
+        yh.copy_(run.fwd(xh.to("cuda", non_blocking=True)), non_blocking=True)
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist.is_initialized():
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        yh.copy_(op.forward(xh.to("cuda", non_blocking=True)), non_blocking=True)
+        yh.copy_(run.fwd(xh.to("cuda", non_blocking=True)), non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = _max_over_ranks(e0.elapsed_time(e1), ws)
 
-    tokens_step = B * L * ws
     peaks, peaks_kind = load_peaks()
-    mix_ms = statistics.mean(mixer_ms)
-    mix_bytes = 8 * D * B * L  # (q, k, v projections in + y out) x 2 B per channel per token
-    achieved = mix_bytes / (mix_ms * 1e-3) / 1e9
-    op_flops = (8 * D * D + 4 * wl["block_size"] * D) * B * L
+    kinfo = []
+    for (label, variant, nbytes), ms in zip(run.kernels, kern_ms):
+        ach = nbytes / (ms * 1e-3) / 1e9
+        kinfo.append({"kernel": MIXER_KERNEL[variant] if wl["kind"] != "cp" else
+                      "two_stage_kernel<IMPL> (hy_li_conv_fwd: implicit long conv of the rank's channel slab)",
+                      "label": label, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                      "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": nbytes, "launch_ms": ms})
+    dom = max(kinfo, key=lambda k: k["launch_ms"])
+    dom = dict(dom, traffic=ncu_traffic(args.workload), peak_source=peaks_kind)
+    op_tf = run.op_flops / ws / (ms_step * 1e-3) / 1e12
+    l2_bytes = run.x.numel() * run.esize * 3
     result = {
-        "metric": "Hyena-MR operator fwd tokens/s (D=4096, % HBM/TC roofline)",
-        "value": tokens_step / (ms_step * 1e-3),
+        "metric": "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU",
+        "value": run.tokens_step / (ms_step * 1e-3),
         "unit": "tokens/s",
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if wl["kind"] == "cp" else "weak",
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": wl["dtype"],
         "data": "synthetic N(0,1) inputs, random-init weights (make_hyena_config seed 0)",
-        "config": {"workload": wl["desc"], "global_batch": B * ws, "seq_len": L, "width": D,
-                   "filter_len": wl["inner_len"], "group_size": 1,
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single",
-                   "l2": "inputs (268 MB) larger than L2 (126 MB); no flush"},
-        "e2e": {"value": tokens_step / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s",
+        "config": {"workload": wl["desc"], "global_batch": run.B, "seq_len": run.l_global, "width": run.D,
+                   "group_size": 1, "parallelism": run.parallelism,
+                   "l2": f"per-step projections ({l2_bytes / 1e6:.0f} MB per rank) larger than L2 (126 MB); "
+                         f"no flush" if l2_bytes > 126e6 else "inputs smaller than L2; no flush"},
+        "e2e": {"value": run.tokens_step / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                 "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
-                "path": "HyenaOperator.forward on pinned host bf16 x; H2D + forward + D2H per step"},
-        "roofline": {"kernel": "two_stage_kernel<FEAT> (hy_hyena_mixer_fwd: featurizers + gates + tcgen05 T0/T1)",
-                     "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic("two_stage_kernel"),
-                     "peak_source": peaks_kind,
-                     "algorithmic_bytes_per_launch": mix_bytes, "launch_ms": mix_ms},
-        "roofline_operator": {"bound": "tensor", "achieved": op_flops / (ms_step * 1e-3) / 1e12 / 1,
-                              "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                              "frac": op_flops / (ms_step * 1e-3) / 1e12 / peaks["bf16_tflops"],
-                              "flops_per_step": op_flops},
-        "phases_ms": {"mixer": mix_ms, "gemms": ms_step - mix_ms},
+                "path": "public forward on pinned host x (per-rank shard); H2D + forward + D2H per step"},
+        "roofline": dom,
+        "roofline_kernels": kinfo,
+        "roofline_operator": {"bound": "tensor", "achieved": op_tf, "peak": peaks["bf16_tflops"],
+                              "unit": "TFLOP/s", "frac": op_tf / peaks["bf16_tflops"],
+                              "flops_per_step_per_rank": run.op_flops // ws},
+        "phases_ms": {"kernels": {k["label"]: k["launch_ms"] for k in kinfo},
+                      "rest (cuBLAS GEMMs, comm, elementwise)": ms_step - sum(kern_ms)},
         "clocks": clocks,
-        "gpu_launches": args.steps,  # one hy_hyena_mixer_fwd launch per step (projections are cuBLAS)
+        "gpu_launches": launches,
     }
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return result, rank
 
 
-def run_cpu_baseline(wl, max_seconds=30.0):
-    """Oracle (numpy, float64 like the reference) on one batch element of the workload."""
+# ---------------------------------------------------------------- CPU legs (oracle: test/baseline only)
+
+
+def _oracle_cfg(variant, D, L, inner_len, block_size, backend="blocked"):
     import oracle
-    cfg = oracle.make_hyena_config(wl["variant"], wl["D"], oracle.make_rng(0), seq_len=wl["L"], group_size=1,
-                                   inner_len=wl["inner_len"], block_size=wl["block_size"])
-    x = oracle.make_rng(1, stream=0).standard_normal((wl["D"], wl["L"]))
-    times = []
-    start = time.perf_counter()
-    while True:
+    return oracle.make_hyena_config(variant, D, oracle.make_rng(0), seq_len=L, group_size=1,
+                                    inner_len=inner_len, block_size=block_size, backend=backend)
+
+
+def _time(fn, reps=1):
+    ts = []
+    for _ in range(reps):
         t = time.perf_counter()
-        oracle.hyena_forward(x, cfg)
-        times.append(time.perf_counter() - t)
-        if time.perf_counter() - start > max_seconds * 0.5 or len(times) >= 3:
-            break
-    med = statistics.median(times)
-    return {"value": wl["L"] / med, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle.hyena_forward (numpy float64 restatement of hyena.py:157-190) on 1 of {wl['B']} "
-                      f"batch elements ({wl['L']} tokens, D={wl['D']}), median of {len(times)} calls; "
-                      f"OpenBLAS threads = all {os.cpu_count()} host cores"}
+        fn()
+        ts.append(time.perf_counter() - t)
+    return statistics.median(ts)
 
 
-def run_reference(args, wl, sample_len=2048):
-    """Reference arm: the reference algorithm's CPU implementation (numpy oracle port, float64)
-    on the host; each step is one forward over a (D, sample_len) token sample of one batch
-    element (per-token cost of the operator is independent of L: projections, featurizer
-    and two-stage conv are all linear in L)."""
+def cpu_seconds_per_element(variant, D, L, inner_len=None, block_size=16, sample_len=2048, f32=False):
+    """(seconds for the oracle's forward of one (D, L) batch element, description, wall seconds
+    actually spent).
+
+    SE / MR: every stage is linear in L, so a (D, sample_len) window is timed and scaled.
+    LI: the token-local part (projections, featurizers, gates) is timed on a sample_len
+    window; the long conv (filter materialisation + radix-2 FFT conv, fft.py:128-145) is
+    timed on a few channels at the full L and scaled to D channels."""
+    import oracle
+    rng = oracle.make_rng(1, stream=0)
+    n = min(L, sample_len)
+    w0 = time.perf_counter()
+    if variant in ("SE", "MR"):
+        cfg = _oracle_cfg(variant, D, L, inner_len, block_size)
+        x = rng.standard_normal((D, n)).astype(np.float32 if f32 else np.float64)
+        t = _time(lambda: oracle.hyena_forward(x, cfg), 1)
+        return t * L / n, f"oracle.hyena_forward over a ({D}, {n}) token window, scaled x{L / n:g}", \
+            time.perf_counter() - w0
+    cfg = _oracle_cfg("LI", D, n, None, block_size, backend="fft")
+    x = rng.standard_normal((D, n))
+    t_local = _time(lambda: oracle.hyena_forward(x, cfg), 1)
+    ch = max(1, min(16, 16 * 131072 // L))
+    full = _oracle_cfg("LI", ch, L, None, block_size, backend="fft")
+    u = rng.standard_normal((ch, L))
+    t_conv = _time(lambda: oracle.fft_conv(u, oracle.bank_taps_per_channel(full["inner"])), 1)
+    return (t_local * L / n + t_conv * D / ch,
+            f"oracle LI forward on a ({D}, {n}) window (scaled x{L / n:g}) + filter materialisation and "
+            f"FFT long conv on {ch} channels at L={L} (scaled x{D / ch:g})", time.perf_counter() - w0)
+
+
+def _stripe_or_single(wl):
+    if wl["kind"] == "stripe":
+        return (("SE", 7), ("MR", 128), ("LI", None))
+    return ((wl["variant"], wl.get("inner_len")),)
+
+
+def cpu_sample(wl, sample_len=2048):
+    """Summed over the workload's Hyena layers: (tokens/s, description, wall seconds)."""
+    D, L = wl["D"], wl["L"]
+    parts = [cpu_seconds_per_element(v, D, L, ln, 128 if wl["kind"] == "stripe" else wl.get("block_size", 16),
+                                     sample_len=sample_len, f32=wl["dtype"] == "f32")
+             for v, ln in _stripe_or_single(wl)]
+    sec = sum(p[0] for p in parts)
+    desc = "; ".join(p[1] for p in parts)
+    if wl["kind"] == "stripe":
+        desc = "stripe Hyena layers only (the reference has no MHA): " + desc
+    return L / sec, desc, sum(p[2] for p in parts)
+
+
+def run_cpu_baseline(wl):
+    """Oracle (numpy, float64 like the reference) on a bounded sample of the workload."""
+    value, desc, _ = cpu_sample(wl, sample_len=8192 if wl["kind"] == "op" and wl["variant"] == "MR" else 4096)
+    return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{desc}; numpy float64 restatement of hyena.py:157-190, OpenBLAS on all "
+                      f"{os.cpu_count()} host cores"}
+
+
+def run_reference(args, wl):
+    """Reference arm: the reference algorithm's CPU implementation (the numpy oracle port,
+    float64 as the reference computes) on the host, rank 0 only. Each step is one bounded
+    sample of the workload (see cpu_seconds_per_element); value = tokens/s of the workload
+    extrapolated from the sample."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return None, rank
-    import oracle
-    cfg = oracle.make_hyena_config(wl["variant"], wl["D"], oracle.make_rng(0), seq_len=wl["L"], group_size=1,
-                                   inner_len=wl["inner_len"], block_size=wl["block_size"])
-    x = oracle.make_rng(1, stream=0).standard_normal((wl["D"], wl["L"]))[:, :sample_len].copy()
-    for _ in range(args.warmup):
-        oracle.hyena_forward(x, cfg)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.hyena_forward(x, cfg)
-    ms = (time.perf_counter() - t) * 1e3 / args.steps
-    value = sample_len / (ms * 1e-3)
-    sample = (f"each step: one forward over {sample_len} of the {wl['L']} tokens of one batch element at full "
-              f"D={wl['D']} (numpy float64 oracle port of hyena.py:157-190; OpenBLAS on all host cores)")
+    vals, walls = [], []
+    for i in range(args.warmup + args.steps):
+        v, desc, wall = cpu_sample(wl)
+        if i >= args.warmup:
+            vals.append(v)
+            walls.append(wall)
+    value = statistics.median(vals)
+    sample = f"each step: {desc}; numpy float64 oracle port of hyena.py:157-190, OpenBLAS on all host cores"
     return {
-        "impl": "reference", "metric": "Hyena-MR operator fwd tokens/s (D=4096, % HBM/TC roofline)",
+        "impl": "reference", "metric": "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU",
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "f32" else "f64",
         "data": "synthetic N(0,1) inputs, random-init weights (make_hyena_config seed 0)",
         "config": {"workload": wl["desc"], "global_batch": wl["B"], "seq_len": wl["L"], "width": wl["D"]},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",

@@ -70,9 +70,18 @@ def last_error() -> str:
     return load().hy_last_error().decode(errors="replace")
 
 
+_LAUNCHES = [0]
+
+
+def launch_count() -> int:
+    """Kernel-launching C-ABI calls that returned HY_OK in this process (bench accounting)."""
+    return _LAUNCHES[0]
+
+
 def check(status: int, what: str) -> None:
     """Map an hy_status to the reference's exception types."""
     if status == HY_OK:
+        _LAUNCHES[0] += 1
         return
     msg = f"{what}: {last_error()}"
     if status == HY_ERR_INVALID:

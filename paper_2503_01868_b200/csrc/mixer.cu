@@ -4,9 +4,9 @@
 //   SE (inner lh <= 16, fp32 or bf16): se_mixer_kernel, CUDA cores
 //   MR (inner lh <= 129, bf16):        tcgen05 two-stage kernel with in-kernel featurizers
 //
-// se_mixer_kernel: one CTA per (row tile of 1024 outputs, channel, batch). Raw
-// projected q/k/v windows are staged with 128-bit loads; the converter step
-// forms u = feat_k * feat_v over [t0 - NI, t0 + 1024) in shared memory, then
+// se_mixer_kernel: one CTA per (row tile of 2048 outputs, channel, batch). Raw
+// projected q/k/v windows are staged with 16-byte cp.async copies (all in flight at once); the converter step
+// forms u = feat_k * feat_v over [t0 - NI, t0 + 2048) in shared memory, then
 // every thread produces 8 outputs y = feat_q * (h_inner conv u) from register
 // sliding windows and stores them as 128-bit vectors. HBM traffic is the 3
 // projected rows in and y out (16 B/token/channel at fp32).
@@ -15,15 +15,15 @@
 
 namespace hy {
 
-constexpr int kMxThreads = 128;
+constexpr int kMxThreads = 256;
 constexpr int kMxV = 8;
-constexpr int kMxTT = kMxThreads * kMxV;
+constexpr int kMxTT = kMxThreads * kMxV;  // outputs per CTA
 
-template <typename A, int NJ>
-__device__ __forceinline__ void fir8_smem(A (&acc)[kMxV], const A* xs, const A* hs, int base) {
+template <typename A, typename S, int NJ>
+__device__ __forceinline__ void fir8_smem(A (&acc)[kMxV], const S* xs, const A* hs, int base) {
   A r[kMxV];
 #pragma unroll
-  for (int vv = 0; vv < kMxV; ++vv) r[vv] = xs[base + vv];
+  for (int vv = 0; vv < kMxV; ++vv) r[vv] = static_cast<A>(xs[base + vv]);
 #pragma unroll
   for (int jj = 0; jj < NJ; ++jj) {
     const A h = hs[jj];
@@ -31,46 +31,46 @@ __device__ __forceinline__ void fir8_smem(A (&acc)[kMxV], const A* xs, const A* 
     for (int vv = 0; vv < kMxV; ++vv) acc[vv] = fma(h, r[vv], acc[vv]);
 #pragma unroll
     for (int vv = kMxV - 1; vv > 0; --vv) r[vv] = r[vv - 1];
-    r[0] = xs[base - jj - 1];
+    r[0] = static_cast<A>(xs[base - jj - 1]);
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// Stage row[s0, s0 + n) into xs (zeros outside [0, L)). vec: every 16-byte unit is issued as
+// one asynchronous copy (all of the CTA's loads in flight at once, no register staging).
 template <typename T>
-__device__ __forceinline__ void stage_row(float* xs, const T* __restrict__ row, int s0, int n, int L,
-                                          bool vec) {
+__device__ __forceinline__ void stage_row(T* xs, const T* __restrict__ row, int s0, int n, int L, bool vec) {
   constexpr int VEC = Elem<T>::VEC;
   if (vec) {
     for (int i = threadIdx.x * VEC; i < n; i += blockDim.x * VEC) {
       const int t = s0 + i;
-      float vals[VEC];
-      if (t >= 0 && t < L) {
-        unpack16<T>(ld_stream16(row + t), vals);
-      } else {
-#pragma unroll
-        for (int m = 0; m < VEC; ++m) vals[m] = 0.f;
-      }
-#pragma unroll
-      for (int m = 0; m < VEC; m += 4)
-        *reinterpret_cast<float4*>(xs + i + m) = *reinterpret_cast<const float4*>(vals + m);
+      const bool ok = t >= 0 && t < L;  // L % VEC == 0 and s0 % VEC == 0: whole units
+      cp_async16(xs + i, ok ? row + t : row, ok);
     }
   } else {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int t = s0 + i;
-      xs[i] = (t >= 0 && t < L) ? Elem<T>::to_a(row[t]) : 0.f;
+      xs[i] = (t >= 0 && t < L) ? row[t] : Elem<T>::from_a(0.f);
     }
   }
 }
 
 // NF: featurizer taps padded (8 or 16); NI: inner taps padded (8 or 16).
 template <typename T, int NF, int NI>
-__global__ void __launch_bounds__(kMxThreads)
+__global__ void __launch_bounds__(kMxThreads, 4)
 se_mixer_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __restrict__ feat_taps,
                 int lhf, const float* __restrict__ inner_taps, const float* __restrict__ decay, int lh,
                 int gs, int C, int L, int vec) {
   constexpr int KW = kMxTT + NI + NF + 8;  // raw k / v window
   constexpr int QW = kMxTT + NF + 8;       // raw q window
   constexpr int UW = kMxTT + NI;           // u window
-  __shared__ __align__(16) float pk[KW], pv[KW], pq[QW], us[UW];
+  __shared__ __align__(16) T pk[KW], pv[KW], pq[QW];
+  __shared__ __align__(16) float us[UW];
   __shared__ float hk[NF], hv[NF], hq[NF], hi[NI];
 
   const int c = blockIdx.y, b = blockIdx.z;
@@ -79,6 +79,13 @@ se_mixer_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __re
   const T* krow = qrow + static_cast<size_t>(C) * L;
   const T* vrow = krow + static_cast<size_t>(C) * L;
   const int tid = threadIdx.x;
+  const int tu = t0 - NI;           // u window origin
+  const int sk = tu - NF - 8;       // raw k/v window origin
+  const int sq = t0 - NF - 8;       // raw q window origin
+  stage_row<T>(pk, krow, sk, KW, L, vec != 0);
+  stage_row<T>(pv, vrow, sk, KW, L, vec != 0);
+  stage_row<T>(pq, qrow, sq, QW, L, vec != 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   if (tid < NF) {
     const bool ok = tid < lhf;
     hq[tid] = ok ? feat_taps[(static_cast<size_t>(0) * C + c) * lhf + tid] : 0.f;
@@ -94,26 +101,22 @@ se_mixer_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __re
     }
     hi[tid] = h;
   }
-  const int tu = t0 - NI;           // u window origin
-  const int sk = tu - NF - 8;       // raw k/v window origin
-  const int sq = t0 - NF - 8;       // raw q window origin
-  stage_row<T>(pk, krow, sk, KW, L, vec != 0);
-  stage_row<T>(pv, vrow, sk, KW, L, vec != 0);
-  stage_row<T>(pq, qrow, sq, QW, L, vec != 0);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  using S = T;
   // u = feat_k * feat_v over the u window, 8 consecutive times per unit
   for (int unit = tid; unit < UW / kMxV; unit += kMxThreads) {
     float fk[kMxV] = {}, fv[kMxV] = {};
     const int base = (tu + unit * kMxV) - sk;
-    fir8_smem<float, NF>(fk, pk, hk, base);
-    fir8_smem<float, NF>(fv, pv, hv, base);
+    fir8_smem<float, S, NF>(fk, pk, hk, base);
+    fir8_smem<float, S, NF>(fv, pv, hv, base);
 #pragma unroll
     for (int vv = 0; vv < kMxV; ++vv) us[unit * kMxV + vv] = fk[vv] * fv[vv];
   }
   __syncthreads();
   float acc[kMxV] = {}, fq[kMxV] = {};
-  fir8_smem<float, NI>(acc, us, hi, NI + tid * kMxV);
-  fir8_smem<float, NF>(fq, pq, hq, t0 + tid * kMxV - sq);
+  fir8_smem<float, float, NI>(acc, us, hi, NI + tid * kMxV);
+  fir8_smem<float, S, NF>(fq, pq, hq, t0 + tid * kMxV - sq);
 #pragma unroll
   for (int vv = 0; vv < kMxV; ++vv) acc[vv] *= fq[vv];
   T* yrow = y + (static_cast<size_t>(b) * C + c) * L;

@@ -111,6 +111,14 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
          (static_cast<uint64_t>(2) << 61);
 }
 
+// SW128 K-major with an explicit stride between 8-row groups (sbo = 0 re-reads the same
+// 8 rows for every group: an M = 128 operand whose only non-trivial rows are 0..7).
+__device__ __forceinline__ uint64_t desc_sw128_sbo(uint32_t saddr, uint32_t sbo) {
+  return (static_cast<uint64_t>((saddr >> 4) & 0x3FFF)) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(sbo >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+
 // kind::f16 instruction descriptor: bf16 A/B, fp32 accumulator, both K-major.
 template <int M, int N>
 __host__ __device__ constexpr uint32_t idesc_bf16_f32() {

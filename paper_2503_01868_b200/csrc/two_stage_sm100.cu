@@ -83,6 +83,8 @@ constexpr int NBUF = 3;
 // featurizer buffer (k / v / q outputs; drained to registers right after it lands).
 constexpr uint32_t TM_ACC = 0, TM_T0 = NBUF * NCH, TM_T1 = TM_T0 + 64, TM_FEAT = TM_T1 + 64;
 constexpr uint32_t TM_K = 0, TM_V = 16 * KV_MB, TM_Q = 32 * KV_MB;
+// implicit mode has no T1: its columns hold the mode-input accumulators E[2] x 32
+constexpr uint32_t TM_E = TM_T1;
 static_assert(TM_FEAT + TM_Q + 16 * Q_MB <= 512, "TMEM budget");
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
@@ -104,8 +106,12 @@ struct Layout {
   static constexpr int OFF_P = OFF_HP + 1024;
   static constexpr int OFF_E = OFF_P + 128 * NPOLE * 4;
   static constexpr int OFF_S = OFF_E + NCH * NPOLE * 4;
-  static constexpr int OFF_BAR = OFF_S + NBUF * NCH * NPOLE * 4;
-  static constexpr int N_BARS = 2 * STAGES + 8 + 6 * NBUF;
+  // implicit mode: Lam[n][t] = lam_n^(127 - t), the bf16 A operand of the mode-input MMA
+  // E[n][chunk] = Lam . U (SW128 K-major, 8 rows, two 64-element K atoms; the descriptor's
+  // zero group stride lets the M = 128 MMA re-read these rows for every 8-row group)
+  static constexpr int OFF_L = round_up(OFF_S + NBUF * NCH * NPOLE * 4, 1024);
+  static constexpr int OFF_BAR = OFF_L + 2048;
+  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -225,6 +231,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   uint64_t* tempty = tfull + NBUF;       // [NBUF] epilogue warps -> MMA
   uint64_t* qfull = tempty + NBUF;       // [NBUF] converter -> epilogue: featurized q in SMEM
   uint64_t* qempty = qfull + NBUF;       // [NBUF] epilogue warps -> converter
+  uint64_t* efull = qempty + NBUF;       // [2] IMPL: MMA commit -> scan warp (E in TMEM)
+  uint64_t* eempty = efull + 2;          // [2] IMPL: scan warp -> MMA (E drained)
+  uint64_t* sready = eempty + 2;         // [NBUF] IMPL: scan warp -> MMA (S_prev in SMEM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -254,6 +263,11 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       mbar_init(&qempty[i], N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
+      mbar_init(&sready[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&efull[i], 1);
+      mbar_init(&eempty[i], 1);
     }
     fence_mbar_init();
   }
@@ -387,9 +401,75 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     __syncwarp();
   } else if (warp == W_MMA) {
     // ------------------------------------------------------------ main MMA issuer
-    {
-      constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
-      const uint32_t t0a = tmem_base + TM_T0, t1a = tmem_base + TM_T1;
+    constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
+    const uint32_t t0a = tmem_base + TM_T0, t1a = tmem_base + TM_T1;
+    if (IMPL) {
+      // per tile j: T0 . U and E = Lam . U (one commit -> scan warp); the inter-chunk term
+      // P . S_prev of tile j waits for the scan and is issued after tile j+1's MMAs (or
+      // before them when tile j+1 starts a new group, whose factors wait on it)
+      constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
+      const uint32_t pa = smem_u32(smem + LY::OFF_P);
+      const uint32_t la = smem_u32(smem + LY::OFF_L);
+      int pend = -1;
+      bool pend_last = false;
+      auto finish = [&](int jj, bool lst) {
+        const int uu = jj % NBUF;
+        mbar_wait(&sready[uu], (jj / NBUF) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + LY::OFF_S + uu * NCH * NPOLE * 4);
+        if (elect_one()) {
+          mma_tf32(tmem_base + TM_ACC + uu * NCH, desc_noswz(pa, 128, 256), desc_noswz(sa, 128, 256), idesc_tf32,
+                   1u);
+          if (lst) mma_commit(&tfree[1]);
+          mma_commit(&tfull[uu]);
+        }
+        __syncwarp();
+      };
+      int gi = -1, g_prev = -1;
+      Tile t;
+      t.init(tb, p);
+      for (int j = 0; j < ntiles; ++j, t.next(p)) {
+        const int u = j % NBUF;
+        const uint32_t ph = (j / NBUF) & 1;
+        const int g = t.c / p.gs;
+        const bool first = g != g_prev;
+        const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
+        if (first) ++gi;
+        g_prev = g;
+        mbar_wait(&ufull[u], ph);
+        mbar_wait(&tempty[u], ph ^ 1);
+        if (first && pend >= 0) {
+          finish(pend, pend_last);
+          pend = -1;
+        }
+        if (first) mbar_wait(&tready[0], gi & 1);
+        mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + TM_ACC + u * NCH;
+        const uint32_t de = tmem_base + TM_E + (j & 1) * NCH;
+        const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
+#pragma unroll
+        for (int ks = 0; ks < LB / 16; ++ks) {
+          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+          if (elect_one()) {
+            mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_main,
+                     ks > 0 ? 1u : 0u);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          mma_commit(&efull[j & 1]);
+          mma_commit(&uempty[u]);
+          if (last) mma_commit(&tfree[0]);
+        }
+        __syncwarp();
+        if (pend >= 0) finish(pend, pend_last);
+        pend = j;
+        pend_last = last;
+      }
+      if (pend >= 0) finish(pend, pend_last);
+    } else {
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -415,24 +495,8 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           if (elect_one()) mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           __syncwarp();
         }
-        if (IMPL) {
-          // inter-chunk term of the implicit filter: D[t][c] += sum_n P[t][n] S_prev[c][n] (tf32)
-          constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
-          const uint32_t pa = smem_u32(smem + LY::OFF_P);
-          const uint32_t sa = smem_u32(smem + LY::OFF_S + u * NCH * NPOLE * 4);
-          if (elect_one()) mma_tf32(d, desc_noswz(pa, 128, 256), desc_noswz(sa, 128, 256), idesc_tf32, 1u);
-          __syncwarp();
-        }
         if (last && elect_one()) mma_commit(&tfree[0]);
         __syncwarp();
-        if (IMPL) {
-          if (elect_one()) {
-            mma_commit(&uempty[u]);
-            mma_commit(&tfull[u]);
-          }
-          __syncwarp();
-          continue;
-        }
         if (first) {
           mbar_wait(&tready[1], gi & 1);
           tc_fence_after();
@@ -460,26 +524,11 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     // M-blocks of this warp: k / v blocks half, half+2, half+4; q blocks half, half+2
     constexpr int KVB_PER = (KV_MB + 1) / 2, QB_PER = Q_MB / 2;
-    // IMPL: per-group mode constants. lam[n]; lamj[n] = lam^(120 - 8j) for this lane's 16-B
-    // unit j = lane % 16 (scales a unit's Horner sum to the chunk end); the scan lanes
-    // (converter warp 0, lane n < NPOLE) also keep lam^128 and the carried state.
-    float lam[NPOLE], lamj[NPOLE], lam128 = 0.f, carry = 0.f;
-    int cur_g = -1;
     Tile t;
     t.init(tb, p);
     for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int u = it % NBUF;
       const uint32_t uph = (it / NBUF) & 1;
-      if (IMPL && t.c / p.gs != cur_g) {
-        cur_g = t.c / p.gs;
-        const int jj = lane & 15;
-#pragma unroll
-        for (int n = 0; n < NPOLE; ++n) {
-          lam[n] = n < p.npoles ? p.poles[static_cast<size_t>(cur_g) * p.npoles + n] : 0.f;
-          lamj[n] = powf(lam[n], static_cast<float>(120 - 8 * jj));
-        }
-        if (ctid < NPOLE) lam128 = powf(lam[ctid], 128.f);
-      }
       // 1) drain the featurized k / v / q of this tile from TMEM into registers and
       //    release the single featurizer buffer for the next tile's MMAs at once
       mbar_wait(&ffull[0], it & 1);
@@ -509,7 +558,6 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (ctid == 0) trace(p, it, 2);
       unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
       unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
-      float* ebuf = reinterpret_cast<float*>(smem + LY::OFF_E);
 #pragma unroll
       for (int i = 0; i < KVB_PER; ++i) {
         const int b = half + 2 * i;
@@ -524,42 +572,6 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           const int4 packed = pack8(uv);
           if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
           if (!IMPL && n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
-        }
-        if (IMPL) {
-          // mode inputs of chunk n: E[n][k] = sum_t lam_k^(127 - t) u[t] (chunk-local t);
-          // per unit: Horner over its 8 samples, scaled by lam^(120 - 8j), then summed over
-          // the chunk's 16 units (16 consecutive lanes) with shuffles
-          const bool valid = n >= 0 && m < KV_WIN;
-          float e8[NPOLE];
-#pragma unroll
-          for (int k = 0; k < NPOLE; ++k) {
-            float a = 0.f;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) a = fmaf(a, lam[k], uv[e]);
-            a = valid ? a * lamj[k] : 0.f;
-#pragma unroll
-            for (int off = 8; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-            e8[k] = a;
-          }
-          if (valid && j == 0) {
-            *reinterpret_cast<float4*>(ebuf + n * NPOLE) = make_float4(e8[0], e8[1], e8[2], e8[3]);
-            *reinterpret_cast<float4*>(ebuf + n * NPOLE + 4) = make_float4(e8[4], e8[5], e8[6], e8[7]);
-          }
-        }
-      }
-      if (IMPL) {
-        // sequential scan over the tile's chunks (lanes = modes): the state entering chunk c
-        // is written as the tf32 B operand S_prev[c][n] (element (c, n) of a no-swizzle
-        // K-major tile at (c%8)*16 + (c/8)*256 + (n%4)*4 + (n/4)*128 bytes)
-        named_bar_sync(BAR_CONV, CONV_THREADS);
-        if (ctid < NPOLE) {
-          float* sp = reinterpret_cast<float*>(smem + LY::OFF_S + u * NCH * NPOLE * 4);
-          float st = t.t0 == 0 ? 0.f : carry;
-          for (int c = 0; c < NCH; ++c) {
-            sp[((c & 7) * 16 + (c >> 3) * 256 + (ctid & 3) * 4 + (ctid >> 2) * 128) / 4] = st;
-            st = fmaf(lam128, st, ebuf[c * NPOLE + ctid]);
-          }
-          carry = st;
         }
       }
       fence_proxy_async();
@@ -660,6 +672,32 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       named_bar_sync(BAR_TB, TB_THREADS);
       if (bt == 0) mbar_arrive(&tready[fct]);
     };
+    // IMPL scan (warp W_TB0, lane n < NPOLE = mode n): E[n][chunk] from TMEM, then the
+    // sequential state recurrence over the tile's chunks; the state entering chunk c is written
+    // as the tf32 B operand S_prev[c][n] (element (c, n) at (c%8)*16 + (c/8)*256 + (n%4)*4 +
+    // (n/4)*128 bytes) and carried to the next tile of the channel
+    float lam128 = 0.f, carry = 0.f;
+    auto scan = [&](int j, const Tile& tl) {
+      const int eb = j & 1;
+      mbar_wait(&efull[eb], (j >> 1) & 1);
+      tc_fence_after();
+      float ev[NCH];
+      tmem_ld_32x32b_x32(tmem_base + TM_E + eb * NCH, ev);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&eempty[eb]);
+      float* sp = reinterpret_cast<float*>(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
+      float st = tl.t0 == 0 ? 0.f : carry;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (lane < NPOLE) sp[((c & 7) * 16 + (c >> 3) * 256 + (lane & 3) * 4 + (lane >> 2) * 128) / 4] = st;
+        st = fmaf(lam128, st, ev[c]);
+      }
+      carry = st;
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sready[j % NBUF]);
+    };
     int gi = 0, g_prev = -1;
     Tile t;
     t.init(tb, p);
@@ -667,19 +705,35 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     if (ntiles > 0) prefetch(t.c / p.gs);
     for (int j = 0; j < ntiles; ++j, t.next(p)) {
       const int g = t.c / p.gs;
-      if (g == g_prev) continue;
+      if (g == g_prev) {
+        if (IMPL && warp == W_TB0) scan(j, t);
+        continue;
+      }
       g_prev = g;
       if (IMPL) {
-        // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states)
-        // and P[m][n] = R_n lam_n^(m+1) as the tf32 A operand: element (m, n) at
-        // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes
-        if (gi > 0) mbar_wait(&tfree[0], (gi - 1) & 1);
+        // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states),
+        // P[m][n] = R_n lam_n^(m+1) as the tf32 A operand (element (m, n) at
+        // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes) and Lam[n][t] = lam_n^(127 - t)
+        if (gi > 0) {
+          mbar_wait(&tfree[0], (gi - 1) & 1);  // T0 / Lam: last T0 . U and Lam . U retired
+          mbar_wait(&tfree[1], (gi - 1) & 1);  // P: last P . S_prev retired
+        }
         float hv = 0.f, pm[NPOLE];
+        unsigned char* lrow = smem + LY::OFF_L + (bt >> 6) * 1024 + (bt & 7) * 2;
 #pragma unroll
         for (int n = 0; n < NPOLE; ++n) {
           const float lt = powf(pf_pole[n], static_cast<float>(bt));
           hv = fmaf(pf_res[n], lt, hv);
           pm[n] = pf_res[n] * lt * pf_pole[n];
+          const int jj = (bt >> 3) & 7;
+          *reinterpret_cast<bf16*>(lrow + n * 128 + ((jj ^ n) << 4)) =
+              __float2bfloat16_rn(powf(pf_pole[n], static_cast<float>(127 - bt)));
+        }
+        if (warp == W_TB0) {
+          lam128 = 0.f;
+#pragma unroll
+          for (int n = 0; n < NPOLE; ++n)
+            if (n == lane) lam128 = powf(pf_pole[n], 128.f);
         }
         hpad[bt] = __float2bfloat16_rn(0.f);
         hpad[128 + bt] = __float2bfloat16_rn(hv);
@@ -693,6 +747,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         build(0);
         if (g < g_end) prefetch(g + 1);
         ++gi;
+        if (warp == W_TB0) scan(j, t);
         continue;
       }
 #pragma unroll
