@@ -67,6 +67,14 @@ def main():
         ms = timeit(lambda: ops.two_stage(v, taps, 1, q=q, k=k, decay=decay))
         report("two_stage_tcgen05_gated", ms, 8 * D * B * L, B=B, D=D, L=L)
         del proj, v, k, q
+    if args.which in ("all", "se", "copy"):
+        for mb in (134, 537, 2147):  # torch copy with the same total traffic as SE/LI kernels
+            n = mb * 1000 * 1000 // 4
+            a = torch.empty(n, device=dev, dtype=torch.float32)
+            b = torch.empty_like(a)
+            ms = timeit(lambda: b.copy_(a))
+            report(f"torch_copy_{2 * mb}MB", ms, 2 * n * 4)
+            del a, b
     if args.which in ("all", "se"):
         B, D, L = 1, 4096, 4096
         for dt, name in ((torch.float32, "se_mixer_f32"), (torch.bfloat16, "se_mixer_bf16")):
@@ -78,6 +86,25 @@ def main():
             x = proj.reshape(B * 3, D, L)
             ms = timeit(lambda: ops.causal_conv(x, feat.reshape(3 * D, 7), 1))
             report(name.replace("se_mixer", "featurizer"), ms, 2 * x.numel() * x.element_size(), rows=3 * D, L=L)
+        for dt, name in ((torch.float32, "se_mixer_f32_B4"),):
+            proj = torch.randn((4, 3 * D, L), device=dev, dtype=dt, generator=g)
+            ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, se_only=True))
+            report(name, ms, 4 * D * 4 * L * proj.element_size(), B=4, D=D, L=L)
+            del proj
+    if args.which in ("all", "li"):
+        D = 4096
+        for L in (131072, 16384):
+            proj = torch.randn((1, 3 * D, L), device=dev, dtype=torch.bfloat16, generator=g)
+            feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
+            packed = ops.feat_pack(feat)
+            res = torch.randn((D, 8), device=dev, generator=g) / 8
+            poles = torch.rand((D, 8), device=dev, generator=g) * 1.9 - 0.95
+            ms = timeit(lambda: ops.li_mixer(proj, feat, res, poles, 1, packed=packed))
+            report("li_mixer_tcgen05", ms, 8 * D * L, D=D, L=L)
+            v = proj[:, :D]
+            ms = timeit(lambda: ops.li_conv(v, res, poles, 1))
+            report("li_conv_ungated", ms, 4 * D * L, D=D, L=L)
+            del proj, v
 
 
 if __name__ == "__main__":
