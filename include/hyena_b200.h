@@ -112,6 +112,13 @@ HY_API int hy_li_mixer_fwd(const void* proj, void* y, const float* feat_taps, co
 HY_API int hy_li_conv_fwd(const void* q, const void* k, const void* v, void* y, const float* residues,
                           const float* poles, int npoles, int group_size, int B, int C, int L, int dtype,
                           void* stream);
+/* Ungated implicit long conv of C rows stored in time segments, element (c, t) of v and y at
+ * c * seg_len + (t / seg_len) * seg_stride + t % seg_len (seg_len a multiple of 4096 dividing
+ * L, seg_stride >= C * seg_len): the rank-major buffer of the context-parallel all-to-all
+ * (cpsim.py:336-375), convolved in place of the reference's slab conv without a transpose. */
+HY_API int hy_li_conv_segmented_fwd(const void* v, void* y, const float* residues, const float* poles,
+                                    int npoles, int group_size, int C, int L, int seg_len,
+                                    long long seg_stride, int dtype, void* stream);
 
 /* SE mixer only (CUDA cores, fp32 / bf16, lh and lhf <= 16), same arguments. */
 HY_API int hy_se_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,

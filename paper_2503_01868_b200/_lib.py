@@ -39,6 +39,7 @@ SIGNATURES = {
     "hy_debug_two_stage_trace": (_I, [_P, _I]),
     "hy_li_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_li_conv_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "hy_li_conv_segmented_fwd": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_longlong, _I, _P]),
 }
 
 _lib = None

@@ -268,7 +268,8 @@ def _a2a(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int, layo
     for rr in range(n):
         grp.filter_elements[rr] = sum(_slab_groups(groups, s * seg + rr * slab, slab).n_groups
                                       for s in range(n_pipe)) * groups.filter_len
-    cols = torch.from_numpy(natural_cols(layout, n, m * n)).to(local.device)
+    segmented = getattr(conv_slab, "segmented", False) and layout == "sequential"
+    cols = None if segmented else torch.from_numpy(natural_cols(layout, n, m * n)).to(local.device)
     out = torch.empty_like(local)
     for s in range(n_pipe):
         lo = s * seg
@@ -278,18 +279,26 @@ def _a2a(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int, layo
                     grp._send(scheme, src, dst, slab * m)
         recv = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
         dist.all_to_all_single(recv, local[lo:lo + seg].contiguous(), group=grp.group)
-        assembled = recv.permute(1, 0, 2).reshape(slab, n * m)  # rank-major time order
-        natural = torch.empty_like(assembled)
-        natural[:, cols] = assembled
-        result = conv_slab(natural, _slab_groups(groups, lo + r * slab, slab))
-        back = result[:, cols].reshape(slab, n, m).permute(1, 0, 2).contiguous()  # (dst, slab, m)
+        if segmented:
+            # recv[src, c] is time segment src of slab row c: the conv reads and writes this
+            # rank-major layout directly, and its output is already the return send buffer
+            back = conv_slab(recv, _slab_groups(groups, lo + r * slab, slab))
+        else:
+            assembled = recv.permute(1, 0, 2).reshape(slab, n * m)  # rank-major time order
+            natural = torch.empty_like(assembled)
+            natural[:, cols] = assembled
+            result = conv_slab(natural, _slab_groups(groups, lo + r * slab, slab))
+            back = result[:, cols].reshape(slab, n, m).permute(1, 0, 2).contiguous()  # (dst, slab, m)
         for src in range(n):  # return round
             for dst in range(n):
                 if dst != src:
                     grp._send(scheme, src, dst, slab * m)
-        ret = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
-        dist.all_to_all_single(ret, back, group=grp.group)
-        out[lo:lo + seg] = ret.reshape(seg, m)
+        if n_pipe == 1:
+            dist.all_to_all_single(out.view(n, slab, m), back, group=grp.group)
+        else:
+            ret = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
+            dist.all_to_all_single(ret, back, group=grp.group)
+            out[lo:lo + seg] = ret.reshape(seg, m)
     grp.count_rounds(scheme, 2 * n_pipe)
     return out
 
@@ -343,9 +352,12 @@ class HyenaCP:
         op, grp = self.op, self.grp
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
         B, D, m = x3.shape
-        proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
-        if self._fused():
-            hist, reqs = _exchange_halo(proj, _lib.MIXER_HISTORY, grp, "cp_hist")
+        if self._fused() and m >= _lib.MIXER_HISTORY:
+            # the successor needs only the projections of the last 144 steps: compute those
+            # first and start the send, so the transfer overlaps the full projection GEMM
+            tail = torch.matmul(op.w_qkv_t, x3[..., m - _lib.MIXER_HISTORY:])
+            hist, reqs = _exchange_halo(tail, _lib.MIXER_HISTORY, grp, "cp_hist")
+            proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
             for q in reqs:
                 q.wait()
             if events is not None:
@@ -355,6 +367,7 @@ class HyenaCP:
             if events is not None:
                 events[1].record()
         else:
+            proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
             # featurizers over the 3D projected rows with their (lhf-1)-step halo
             ft = op.feat_taps.reshape(3 * D, op.lhf)
             if getattr(self, "_feat_groups", None) is None:
@@ -367,13 +380,13 @@ class HyenaCP:
             u = k * v
             taps = op.materialized_inner
             if self.cfg.variant == "LI":
-                slab_conv = _li_slab_conv(op) if op.li_modes is not None else None
-                if events is not None:
-                    events[0].record()
+                m = u.shape[-1]
+                if op.li_modes is not None and m % 4096 == 0:
+                    slab_conv = _li_slab_conv(op, events)
+                else:
+                    slab_conv = None  # materialised taps, direct conv on the natural-order slab
                 conv = torch.stack([a2a_conv(u[b].contiguous(), self.cfg.inner, grp, conv_slab=slab_conv)
                                     for b in range(B)])
-                if events is not None:
-                    events[1].record()
             else:
                 conv = p2p_conv_overlapped(u, self.cfg.inner, grp,
                                            conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
@@ -385,15 +398,23 @@ class HyenaCP:
     __call__ = forward
 
 
-def _li_slab_conv(op):
-    """Implicit long conv of a channel slab over the full sequence (tcgen05 li_conv)."""
+def _li_slab_conv(op, events=None):
+    """Implicit long conv of a channel slab over the full sequence, read and written in the
+    rank-major all-to-all layout (tcgen05 li_conv_segmented); events: optional (start, end)
+    CUDA events around the kernel."""
     from . import ops
     res, poles = op.li_modes
 
-    def conv(natural, slab_groups):
+    def conv(recv, slab_groups):
         g0 = _group_index(op.cfg.inner, slab_groups)
         ng = slab_groups.n_groups
-        return ops.li_conv(natural.contiguous(), res[g0:g0 + ng], poles[g0:g0 + ng], slab_groups.group_size)
+        if events is not None:
+            events[0].record()
+        y = ops.li_conv_segmented(recv, res[g0:g0 + ng], poles[g0:g0 + ng], slab_groups.group_size)
+        if events is not None:
+            events[1].record()
+        return y
+    conv.segmented = True
     return conv
 
 

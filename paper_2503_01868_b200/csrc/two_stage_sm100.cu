@@ -134,7 +134,19 @@ struct Params {
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
+  // implicit, non-fused only: rows stored as L / seg_len time segments, element (row, t) at
+  // row * seg_len + (t / seg_len) * seg_stride + t % seg_len (the rank-major layout of an
+  // all-to-all buffer); seg_len = 0: plain rows of L. seg_len is a multiple of TILE_T.
+  int seg_len;
+  long long seg_stride;
 };
+
+// offset of element (row, t) of a q / k / v / y row
+__device__ __forceinline__ size_t elem_off(const Params& p, int row, int t) {
+  if (p.seg_len == 0) return static_cast<size_t>(row) * p.L + t;
+  const int sg = t / p.seg_len;
+  return static_cast<size_t>(row) * p.seg_len + static_cast<size_t>(sg) * p.seg_stride + (t - sg * p.seg_len);
+}
 
 // Optional timeline trace (debug/tuning): CTA 0 records clock64 per tile and event.
 constexpr int TRACE_TILES = 256, TRACE_EV = 16;
@@ -170,12 +182,12 @@ struct Tile {
   }
 };
 
+// window start in row `which` (0 = q, 1 = k, 2 = v) at time t
 template <bool FEAT>
-__device__ __forceinline__ const bf16* row_ptr(const Params& p, int which, int b, int c) {
-  // which: 0 = q, 1 = k, 2 = v
-  if (FEAT) return p.proj + (static_cast<size_t>(b) * 3 * p.C + which * p.C + c) * p.L;
+__device__ __forceinline__ const bf16* src_ptr(const Params& p, int which, int b, int c, int t) {
+  if (FEAT) return p.proj + (static_cast<size_t>(b) * 3 * p.C + which * p.C + c) * p.L + t;
   const bf16* base = which == 0 ? p.q : which == 1 ? p.k : p.v;
-  return base + (static_cast<size_t>(b) * p.C + c) * p.L;
+  return base + elem_off(p, b * p.C + c, t);
 }
 
 __device__ __forceinline__ int4 pack8(const float* in) {
@@ -297,9 +309,12 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       bf16* qbuf = reinterpret_cast<bf16*>(st + 2 * KV_BYTES);
       bf16* fmat = reinterpret_cast<bf16*>(st + 2 * KV_BYTES + Q_BYTES);  // [3 tensors][KS][256]
       const int kws = t.t0 - LB - HALO, kwe = t.t0 + TILE_T;
-      const int kvs = max(kws, 0), kve = min(kwe, p.L);
+      // segmented rows: windows stop at the segment start (the history there is unused
+      // in implicit mode, whose earlier steps arrive through the carried states)
+      const int lo = p.seg_len ? (t.t0 / p.seg_len) * p.seg_len : 0;
+      const int kvs = max(kws, lo), kve = min(kwe, p.L);
       const int qws = t.t0 - HALO, qwe = t.t0 + TILE_T;
-      const int qvs = max(qws, 0), qve = min(qwe, p.L);
+      const int qvs = max(qws, lo), qve = min(qwe, p.L);
       bool wrote = false;  // generic-proxy SMEM writes to order before the async proxy
       // first tile with a predecessor's history: the head of the windows comes from hist
       const bool use_hist = FEAT && p.hist != nullptr && t.t0 == 0;
@@ -350,9 +365,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           bulk_g2s(vbuf, hrow + 2 * tstride, HIST * 2, &full[s]);
           bulk_g2s(qbuf, hrow + (HIST - HALO), HALO * 2, &full[s]);
         }
-        bulk_g2s(vbuf + (kvs - kws), row_ptr<FEAT>(p, 2, t.b, t.c) + kvs, kvb, &full[s]);
-        if (GK) bulk_g2s(kbuf + (kvs - kws), row_ptr<FEAT>(p, 1, t.b, t.c) + kvs, kvb, &full[s]);
-        if (GQ) bulk_g2s(qbuf + (qvs - qws), row_ptr<FEAT>(p, 0, t.b, t.c) + qvs, qb, &full[s]);
+        bulk_g2s(vbuf + (kvs - kws), src_ptr<FEAT>(p, 2, t.b, t.c, kvs), kvb, &full[s]);
+        if (GK) bulk_g2s(kbuf + (kvs - kws), src_ptr<FEAT>(p, 1, t.b, t.c, kvs), kvb, &full[s]);
+        if (GQ) bulk_g2s(qbuf + (qvs - qws), src_ptr<FEAT>(p, 0, t.b, t.c, qvs), qb, &full[s]);
         if (fb) bulk_g2s(fmat, p.fpack + static_cast<size_t>(t.c) * (LY::F_SET / 2), fb, &full[s]);
         trace(p, it, 11);
       }
@@ -423,6 +438,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           if (lst) mma_commit(&tfree[1]);
           mma_commit(&tfull[uu]);
         }
+        if (lane == 0) trace(p, jj, 8);
         __syncwarp();
       };
       int gi = -1, g_prev = -1;
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           finish(pend, pend_last);
           pend = -1;
         }
+        if (lane == 0) trace(p, j, 4);
         if (first) mbar_wait(&tready[0], gi & 1);
         mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -463,6 +480,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           mma_commit(&uempty[u]);
           if (last) mma_commit(&tfree[0]);
         }
+        if (lane == 0) trace(p, j, 7);
         __syncwarp();
         if (pend >= 0) finish(pend, pend_last);
         pend = j;
@@ -613,7 +631,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (lane == 0) mbar_arrive(&tempty[a]);
       if (GQ) mbar_wait(&qfull[a], aph);
       const bf16* fq = reinterpret_cast<const bf16*>(smem + LY::OFF_FQ + a * NCH * LB * 2);
-      bf16* yrow = p.y + (static_cast<size_t>(t.b) * p.C + t.c) * p.L + t.t0;
+      bf16* yrow = p.y + elem_off(p, t.b * p.C + t.c, t.t0);
       const int nt = min(TILE_T, p.L - t.t0);
 #pragma unroll
       for (int n = 0; n < NCH; ++n) {
@@ -680,6 +698,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     auto scan = [&](int j, const Tile& tl) {
       const int eb = j & 1;
       mbar_wait(&efull[eb], (j >> 1) & 1);
+      if (lane == 0) trace(p, j, 9);
       tc_fence_after();
       float ev[NCH];
       tmem_ld_32x32b_x32(tmem_base + TM_E + eb * NCH, ev);
@@ -697,6 +716,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sready[j % NBUF]);
+      if (lane == 0) trace(p, j, 10);
     };
     int gi = 0, g_prev = -1;
     Tile t;
@@ -925,6 +945,36 @@ extern "C" HY_API int hy_li_conv_fwd(const void* q, const void* k, const void* v
   if (k) return ts::launch<false, true, false, true>(p, st);
   if (q) return ts::launch<false, false, true, true>(p, st);
   return ts::launch<false, false, false, true>(p, st);
+}
+
+// Ungated implicit long conv of rows stored in time segments (the all-to-all buffer of the
+// context-parallel LI layer, cp.py): element (c, t) of v and y at
+// c * seg_len + (t / seg_len) * seg_stride + t % seg_len; seg_len a multiple of 4096.
+extern "C" HY_API int hy_li_conv_segmented_fwd(const void* v, void* y, const float* residues, const float* poles,
+                                               int npoles, int gs, int C, int L, int seg_len,
+                                               long long seg_stride, int dtype, void* stream) {
+  if (dtype != HY_BF16) return fail(HY_ERR_UNSUPPORTED, "hy_li_conv_segmented_fwd: tcgen05 path is bf16 only");
+  if (!v || !y) return fail(HY_ERR_INVALID, "null pointer argument");
+  int s = check_impl(residues, poles, npoles, 1, C, L, gs);
+  if (s != HY_OK) return s;
+  if (seg_len < ts::TILE_T || seg_len % ts::TILE_T != 0 || L % seg_len != 0)
+    return fail(HY_ERR_INVALID, "segment length %d must be a multiple of %d dividing L = %d", seg_len, ts::TILE_T,
+                L);
+  if (seg_stride < static_cast<long long>(C) * seg_len)
+    return fail(HY_ERR_INVALID, "segment stride %lld overlaps the %d rows of a segment", seg_stride, C);
+  if (!aligned16(v) || !aligned16(y)) return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  ts::Params p{};
+  p.v = static_cast<const ts::bf16*>(v);
+  p.y = static_cast<ts::bf16*>(y);
+  p.poles = poles;
+  p.residues = residues;
+  p.npoles = npoles;
+  p.B = 1, p.C = C, p.L = L, p.lh = 1, p.gs = gs, p.lhf = 1;
+  p.seg_len = seg_len;
+  p.seg_stride = seg_stride;
+  p.tiles_per_seq = L / ts::TILE_T;
+  p.total_tiles = p.tiles_per_seq * C;
+  return ts::launch<false, false, false, true>(p, static_cast<cudaStream_t>(stream));
 }
 
 // Debug: copy the CTA-0 timeline of the last traced two-stage launch (HY_TS_TRACE=1).

@@ -232,6 +232,27 @@ def li_conv(v: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_
     return y[0] if squeeze else y
 
 
+def li_conv_segmented(buf: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_size: int = 1,
+                      out=None) -> torch.Tensor:
+    """Ungated implicit long conv of a (n_seg, C, seg_len) buffer whose row c is the time
+    concatenation of buf[0, c], buf[1, c], ... (the rank-major all-to-all buffer of the
+    context-parallel LI layer); returns y in the same layout (tcgen05, bf16)."""
+    if buf.dim() != 3:
+        raise ValueError("segmented buffer must be (n_seg, C, seg_len)")
+    _check_device(buf)
+    if buf.dtype != torch.bfloat16:
+        raise ValueError("li_conv (tcgen05) takes bfloat16 activations")
+    buf = buf.contiguous()
+    n, C, m = buf.shape
+    r, p = _modes(residues, poles, buf.device)
+    y = torch.empty_like(buf) if out is None else out
+    lib = _lib.load()
+    _lib.check(lib.hy_li_conv_segmented_fwd(buf.data_ptr(), y.data_ptr(), r.data_ptr(), p.data_ptr(), p.shape[1],
+                                            group_size, C, n * m, m, C * m, _lib.HY_BF16, _stream()),
+               "li_conv_segmented")
+    return y
+
+
 def li_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor,
              group_size: int, packed=None) -> torch.Tensor:
     """Hyena-LI mixer from the (B, 3C, L) projections: featurizers, gates, implicit long conv."""

@@ -105,6 +105,14 @@ def main():
             ms = timeit(lambda: ops.li_conv(v, res, poles, 1))
             report("li_conv_ungated", ms, 4 * D * L, D=D, L=L)
             del proj, v
+    if args.which in ("all", "fft"):
+        D = 4096
+        for L, dt in ((131072, torch.bfloat16), (16384, torch.float32)):
+            v = torch.randn((1, D, L), device=dev, dtype=dt, generator=g)
+            taps = torch.randn((D, L), device=dev, generator=g) / 100
+            ms = timeit(lambda: ops.fft_conv(v, taps, 1, q=v, k=v), iters=3, warmup=1)
+            report("fft_conv", ms, 4 * D * L * v.element_size(), D=D, L=L, dtype=str(dt))
+            del v, taps
 
 
 if __name__ == "__main__":

@@ -288,3 +288,52 @@ def test_li_conv_many_sequences_per_cta():
     sel = [0, 1, 147, 148, 149, 200, 319]
     want = oracle.fft_conv(v[0][sel], taps[sel])
     assert oracle.rel_err(y[0][sel], want) < TOL["bf16"]
+
+
+def test_li_conv_segmented_equals_natural():
+    # the all-to-all buffer layout (n_seg, C, seg_len): row c = buf[0, c] | buf[1, c] | ...
+    rng = np.random.default_rng(12)
+    n, C, m = 3, 40, 8192
+    poles = dev(rng.uniform(-0.99, 0.99, (C, 8)))
+    residues = dev(rng.standard_normal((C, 8)) / 8)
+    v = dev(bf16_round(rng.standard_normal((C, n * m))), torch.bfloat16)
+    want = ops.li_conv(v, residues, poles, 1)
+    buf = v.reshape(C, n, m).permute(1, 0, 2).contiguous()
+    got = ops.li_conv_segmented(buf, residues, poles, 1)
+    assert torch.equal(got.permute(1, 0, 2).reshape(C, n * m), want)
+    with pytest.raises(ValueError):
+        ops.li_conv_segmented(buf[..., :1000].contiguous(), residues, poles, 1)
+
+
+@pytest.mark.parametrize("dtype,B,C,L,lh,gs,gated", [
+    ("f32", 1, 3, 4096, 4096, 1, True),        # N = 8192: one row pass, N1 = 2
+    ("f32", 2, 4, 1000, 777, 2, True),         # ragged L, lh < L, groups
+    ("f32", 1, 2, 20000, 20000, 1, False),     # N = 65536: N1 = 16 column transforms
+    ("f32", 1, 2, 5, 3, 1, True),              # tiny: N padded to 16
+    ("bf16", 1, 3, 16384, 16384, 1, True),
+])
+def test_fft_conv_vs_oracle(dtype, B, C, L, lh, gs, gated):
+    # fp32 complex FFT conv (fft.py:128-145 semantics: zero-padded, truncated to L) vs the
+    # float64 radix-2 oracle; fp32 tolerance 1e-5, bf16 1e-2
+    rng = np.random.default_rng(L + lh)
+    G = C // gs
+    taps = rng.standard_normal((G, lh)) / np.sqrt(lh)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: a.astype(np.float32).astype(np.float64))
+    v = rnd(rng.standard_normal((B, C, L)))
+    q = rnd(rng.standard_normal((B, C, L))) if gated else None
+    k = rnd(rng.standard_normal((B, C, L))) if gated else None
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    y = ops.fft_conv(dev(v, tdt), dev(taps), gs, q=None if q is None else dev(q, tdt),
+                     k=None if k is None else dev(k, tdt)).double().cpu().numpy()
+    per_ch = np.repeat(taps, gs, axis=0)
+    for b in range(B):
+        u = v[b] * (k[b] if gated else 1.0)
+        want = oracle.fft_conv(u, per_ch) * (q[b] if gated else 1.0)
+        err = oracle.rel_err(y[b], want)
+        assert err < TOL[dtype], (b, err)
+
+
+def test_fft_conv_errors():
+    v = torch.zeros((1, 2, 64), device="cuda")
+    with pytest.raises(ValueError):
+        ops.fft_conv(v, torch.zeros((2, 65), device="cuda"), 1)  # lh > L
