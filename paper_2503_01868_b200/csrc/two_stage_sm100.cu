@@ -149,7 +149,7 @@ __device__ __forceinline__ size_t elem_off(const Params& p, int row, int t) {
 }
 
 // Optional timeline trace (debug/tuning): CTA 0 records clock64 per tile and event.
-constexpr int TRACE_TILES = 256, TRACE_EV = 16;
+constexpr int TRACE_TILES = 256, TRACE_EV = 24;
 __device__ unsigned long long g_trace[TRACE_TILES * TRACE_EV];
 __device__ __forceinline__ void trace(const Params& p, int it, int ev) {
   if (p.trace && blockIdx.x == 0 && it < TRACE_TILES) g_trace[it * TRACE_EV + ev] = clock64();
@@ -388,24 +388,25 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         const uint32_t fm = st + 2 * KV_BYTES + Q_BYTES;
         const uint32_t dfe = tmem_base + TM_FEAT;
         const uint32_t w0 = 2 * (HALO - 8 * KS);  // byte offset of window 0
+        // one elected lane issues the whole tile's featurizer MMAs back to back
+        if (elect_one()) {
 #pragma unroll
-        for (int tensor = 0; tensor < 3; ++tensor) {
-          if (tensor == 0 && !GQ) continue;
-          if (tensor == 1 && !GK) continue;
-          const uint32_t buf = tensor == 0 ? st + 2 * KV_BYTES : st + (tensor == 1 ? 0 : KV_BYTES);
-          const int nmb = tensor == 0 ? Q_MB : KV_MB;
-          const uint32_t dcol = tensor == 0 ? TM_Q : tensor == 1 ? TM_K : TM_V;
-          for (int b = 0; b < nmb; ++b) {
+          for (int tensor = 0; tensor < 3; ++tensor) {
+            if (tensor == 0 && !GQ) continue;
+            if (tensor == 1 && !GK) continue;
+            const uint32_t buf = tensor == 0 ? st + 2 * KV_BYTES : st + (tensor == 1 ? 0 : KV_BYTES);
+            const int nmb = tensor == 0 ? Q_MB : KV_MB;
+            const uint32_t dcol = tensor == 0 ? TM_Q : tensor == 1 ? TM_K : TM_V;
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-              const uint64_t ad = desc_noswz(buf + w0 + b * 2048 + ks * 32, 16, 128);
-              const uint64_t bd = desc_noswz(fm + (tensor * KS + ks) * F_BYTES, 128, 256);
-              if (elect_one()) mma_bf16(dfe + dcol + b * 16, ad, bd, idesc_feat, ks > 0 ? 1u : 0u);
-              __syncwarp();
+            for (int b = 0; b < nmb; ++b) {
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks) {
+                const uint64_t ad = desc_noswz(buf + w0 + b * 2048 + ks * 32, 16, 128);
+                const uint64_t bd = desc_noswz(fm + (tensor * KS + ks) * F_BYTES, 128, 256);
+                mma_bf16(dfe + dcol + b * 16, ad, bd, idesc_feat, ks > 0 ? 1u : 0u);
+              }
             }
           }
-        }
-        if (elect_one()) {
           mma_commit(&empty[s]);
           mma_commit(&ffull[0]);
           trace(p, it, 13);
@@ -429,7 +430,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       bool pend_last = false;
       auto finish = [&](int jj, bool lst) {
         const int uu = jj % NBUF;
+        if (lane == 0) trace(p, jj, 19);
         mbar_wait(&sready[uu], (jj / NBUF) & 1);
+        if (lane == 0) trace(p, jj, 20);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + LY::OFF_S + uu * NCH * NPOLE * 4);
         if (elect_one()) {
@@ -453,7 +456,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         if (first) ++gi;
         g_prev = g;
         mbar_wait(&ufull[u], ph);
+        if (lane == 0) trace(p, j, 16);
         mbar_wait(&tempty[u], ph ^ 1);
+        if (lane == 0) trace(p, j, 17);
         if (first && pend >= 0) {
           finish(pend, pend_last);
           pend = -1;
@@ -461,26 +466,28 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         if (lane == 0) trace(p, j, 4);
         if (first) mbar_wait(&tready[0], gi & 1);
         mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
+        if (lane == 0) trace(p, j, 18);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
         const uint32_t de = tmem_base + TM_E + (j & 1) * NCH;
         const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
+        if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          if (elect_one()) {
+          for (int ks = 0; ks < LB / 16; ++ks) {
+            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
             mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+          }
+#pragma unroll
+          for (int ks = 0; ks < LB / 16; ++ks) {
+            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
             mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_main,
                      ks > 0 ? 1u : 0u);
           }
-          __syncwarp();
-        }
-        if (elect_one()) {
           mma_commit(&efull[j & 1]);
           mma_commit(&uempty[u]);
           if (last) mma_commit(&tfree[0]);
+          trace(p, j, 7);
         }
-        if (lane == 0) trace(p, j, 7);
         __syncwarp();
         if (pend >= 0) finish(pend, pend_last);
         pend = j;
@@ -507,25 +514,22 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
         const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
         const uint32_t upa = smem_u32(smem + LY::OFF_UP + u * NCH * LB * 2);
-#pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          if (elect_one()) mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
-          __syncwarp();
-        }
-        if (last && elect_one()) mma_commit(&tfree[0]);
-        __syncwarp();
-        if (first) {
-          mbar_wait(&tready[1], gi & 1);
-          tc_fence_after();
-        }
-#pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          if (elect_one()) mma_bf16_ts(d, t1a + ks * 8, desc_sw128(upa + bo), idesc_main, 1u);
-          __syncwarp();
-        }
         if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < LB / 16; ++ks) {
+            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+            mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+          }
+          if (last) mma_commit(&tfree[0]);
+          if (first) {
+            mbar_wait(&tready[1], gi & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int ks = 0; ks < LB / 16; ++ks) {
+            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+            mma_bf16_ts(d, t1a + ks * 8, desc_sw128(upa + bo), idesc_main, 1u);
+          }
           if (last) mma_commit(&tfree[1]);
           mma_commit(&uempty[u]);
           mma_commit(&tfull[u]);

@@ -23,9 +23,9 @@ for _ in range(3):
         v, k, q = (proj[:, i * D:(i + 1) * D].contiguous() for i in range(3))
         ops.two_stage(v, taps, 1, q=q, k=k)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 4096)()
-_lib.check(_lib.load().hy_debug_two_stage_trace(buf, 4096), "trace")
-tr = np.array(buf, dtype=np.int64).reshape(256, 16)
+buf = (ctypes.c_ulonglong * 6144)()
+_lib.check(_lib.load().hy_debug_two_stage_trace(buf, 6144), "trace")
+tr = np.array(buf, dtype=np.int64).reshape(256, 24)
 n = 221
 tr = tr[:n].astype(np.float64)
 tr -= tr[0, 0]

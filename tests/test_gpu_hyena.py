@@ -136,3 +136,18 @@ def test_li_operator_bf16_vs_oracle():
                       "filters": [("implicit", f.residues, f.poles, L) for f in inner.filters]}}
     want = oracle.hyena_forward(x, ocfg)
     assert oracle.rel_err(y.float().cpu().numpy(), want) < 1e-2
+
+
+def test_host_pipeline_matches_forward():
+    # each step's own H2D / forward / D2H, overlapped across steps, equals the plain forward
+    from paper_2503_01868_b200.streaming import HostPipeline
+    cfg = hy.make_hyena_config("MR", 64, hy.make_rng(0), inner_len=128, block_size=128)
+    op = hy.HyenaOperator(cfg, torch.bfloat16)
+    g = torch.Generator().manual_seed(5)
+    xs = [torch.randn((2, 64, 4096), generator=g).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    pipe = HostPipeline(op.forward, tuple(xs[0].shape), torch.bfloat16)
+    pipe.run(xs, ys, 3)
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        assert torch.equal(y, op.forward(x.cuda()).cpu())
