@@ -54,9 +54,9 @@ WORKLOADS = {
 
 # algorithmic HBM bytes per token of the fused mixer kernels: 3 projected rows in + 1 out
 MIXER_KERNEL = {"MR": "two_stage_kernel<FEAT> (hy_hyena_mixer_fwd: featurizers + gates + tcgen05 T0/T1)",
-                "SE": "se_mixer_kernel (hy_hyena_mixer_fwd: featurizers + gates + short conv)",
+                "SE": "se_stream_kernel (hy_hyena_mixer_fwd: featurizers + gates + short conv, TMA-fed chunk stream)",
                 "LI": "two_stage_kernel<FEAT,IMPL> (hy_li_mixer_fwd: featurizers + gates + implicit long conv)"}
-MIXER_NCU_NAME = {"MR": "two_stage_kernel", "SE": "se_mixer_kernel", "LI": "two_stage_kernel"}
+MIXER_NCU_NAME = {"MR": "two_stage_kernel", "SE": "se_stream_kernel", "LI": "two_stage_kernel"}
 
 
 def load_peaks():

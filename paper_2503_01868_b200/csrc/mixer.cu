@@ -13,6 +13,7 @@
 // out (16 B/token/channel at fp32, 8 at bf16).
 #include "common.cuh"
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace hy {
 
@@ -158,7 +159,7 @@ se_mixer_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __re
   // 16-byte cp.async copies (zero-filled outside [0, L)) in two halves of 16 bytes per lane,
   // so each 16-byte read below is bank-conflict free (!VEC: register prefetch)
   // (measured: the ring wins for bf16, register prefetch for fp32)
-  constexpr bool RING = VEC && sizeof(T) == 2;
+  constexpr bool RING = VEC;
   extern __shared__ __align__(16) unsigned char se_ring[];
   constexpr int HALF = 32 * (16 / static_cast<int>(sizeof(T)));
   constexpr int NHALF = 8 * static_cast<int>(sizeof(T)) / 16;
@@ -280,12 +281,226 @@ se_mixer_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __re
   }
 }
 
+// se_stream_kernel: the SE mixer for filters of <= 8 taps on 16-byte aligned rows. Each warp
+// owns a contiguous range of 256-step chunks (row-major over (b, c, chunk)), so every chunk's
+// FIR history is carried from the previous chunk instead of re-read: lane l holds steps
+// [8l, 8l + 8), takes the last samples of lane l - 1 by one rotation shuffle, and lane 0
+// takes them from the previous chunk (raw rows: the previous ring stage, still resident;
+// u = k * v: a register carried across chunks). Chunks stream in by 1-D bulk copies (TMA)
+// issued by one lane into a per-warp ring of kSsStages stages with an mbarrier each; a warp
+// whose range starts mid-row first loads the 16 preceding steps (a warm-up chunk, no store).
+// FIRs run on packed fp32 FMAs with the tap broadcast as a scalar operand and both sample
+// pair alignments of the window built once per row. HBM traffic: 3 rows in, 1 out, once.
+constexpr int kSsWarps = 8;
+constexpr int kSsStages = 3;
+constexpr int kSsChunk = 256;
+
+template <typename T>
+__device__ __forceinline__ void lds8(float (&x)[8], const T* p) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+  } else {
+    unpack16<T>(*reinterpret_cast<const int4*>(p), x);
+  }
+}
+
+// out[i] = sum_{j < NJ} h[j] x[i - j], i < 8, from this lane's samples x[0..7] and the window
+// history x[-8..-1] (hist[e] = x[e - 8]); output pairs on packed FMAs. Even taps read the
+// naturally aligned pairs (x[2q], x[2q+1]); odd taps the pairs (x[2q-1], x[2q]), built once.
+template <int NJ>
+__device__ __forceinline__ void fir_pairs(float (&out)[8], const float (&x)[8], const float (&hist)[8],
+                                          const float (&h)[NJ]) {
+  auto at = [&](int i) { return i >= 0 ? x[i] : hist[8 + i]; };
+  float2 ev[8], od[8];  // ev[q + 4] = (x[2q], x[2q+1]); od[q + 4] = (x[2q-1], x[2q]), q in [-4, 3]
+#pragma unroll
+  for (int q = -4; q < 4; ++q) {
+    ev[q + 4] = make_float2(at(2 * q), at(2 * q + 1));
+    od[q + 4] = make_float2(2 * q - 1 >= -8 ? at(2 * q - 1) : 0.f, at(2 * q));
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const float2 w = (j & 1) ? od[p - (j - 1) / 2 + 4] : ev[p - j / 2 + 4];
+      a = ffma2(make_float2(h[j], h[j]), w, a);
+    }
+    out[2 * p] = a.x;
+    out[2 * p + 1] = a.y;
+  }
+}
+
+// hist[e] (e >= 8 - NH) = sample e - 8 of this row window: lane l - 1's x[e] by a rotation
+// shuffle; lane 0 takes `first` (the previous chunk's tail, or zeros at the row start).
+template <int NH>
+__device__ __forceinline__ void hist_shfl(float (&hist)[8], const float (&x)[8], const float (&first)[8], int lane) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e >= 8 - NH) {
+      const float s = __shfl_sync(kFull, x[e], (lane + 31) & 31);
+      hist[e] = lane == 0 ? first[e] : s;
+    } else {
+      hist[e] = 0.f;
+    }
+  }
+}
+
+template <typename T, int NF, int NI>
+__global__ void __launch_bounds__(kSsWarps * 32, 2)
+se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __restrict__ feat_taps, int lhf,
+                 const float* __restrict__ inner_taps, const float* __restrict__ decay, int lh, int gs, int B,
+                 int C, int L) {
+  using namespace sm100;
+  constexpr int ROWB = kSsChunk * static_cast<int>(sizeof(T));  // bytes per row per stage
+  constexpr int NHF = NF - 1, NHI = NI - 1;  // history samples each FIR needs
+  extern __shared__ __align__(128) unsigned char ss_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* ring = reinterpret_cast<T*>(ss_smem + warp * (kSsStages * 3 * ROWB));  // [stage][k, v, q][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ss_smem + kSsWarps * kSsStages * 3 * ROWB) + warp * kSsStages;
+
+  const int nch = (L + kSsChunk - 1) / kSsChunk;
+  const long long total = static_cast<long long>(B) * C * nch;  // < 2^31 (host check)
+  const long long gw = static_cast<long long>(blockIdx.x) * kSsWarps + warp, nw = static_cast<long long>(gridDim.x) * kSsWarps;
+  const int i0 = static_cast<int>(total * gw / nw), i1 = static_cast<int>(total * (gw + 1) / nw);
+  if (i0 >= i1) return;
+  if (lane == 0) {
+    for (int s = 0; s < kSsStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // issue list: [warm-up chunk (when i0 starts mid-row)] + items i0 .. i1 - 1
+  const bool warm = (i0 % nch) != 0;
+  const int n_issue = (i1 - i0) + (warm ? 1 : 0);
+  const int base = i0 - (warm ? 1 : 0);
+  struct Cur {  // (row, chunk) of an issue-list entry, advanced without divisions
+    int row, k;
+    __device__ void next(int nch_) {
+      if (++k == nch_) k = 0, ++row;
+    }
+  };
+  const Cur start{base / nch, base % nch};
+  // lane 0's issue cursor: the q row of the next entry to issue, its chunk, channel, stage
+  const size_t CL = static_cast<size_t>(C) * L;
+  const T* iss_q = proj + (static_cast<size_t>(start.row / C) * 3 * C + start.row % C) * L;
+  int iss_k = start.k, iss_c = start.row % C, iss_st = 0, n_iss = 0;
+  auto issue = [&]() {  // lane 0: entry n_iss into stage n_iss % S
+    int t0 = iss_k * kSsChunk, cnt = min(kSsChunk, L - t0), off = 0;
+    if (warm && n_iss == 0) off = kSsChunk - 16, t0 += kSsChunk - 16, cnt = 16;  // the 16 steps before i0
+    T* dst = ring + iss_st * 3 * kSsChunk + off;
+    const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(T));
+    const T* src = iss_q + t0;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bars[iss_st], 3 * bytes);
+    bulk_g2s(dst, src + CL, bytes, &bars[iss_st]);                  // k
+    bulk_g2s(dst + kSsChunk, src + 2 * CL, bytes, &bars[iss_st]);  // v
+    bulk_g2s(dst + 2 * kSsChunk, src, bytes, &bars[iss_st]);       // q
+    if (++iss_k == nch) {
+      iss_k = 0;
+      iss_q += L;
+      if (++iss_c == C) iss_c = 0, iss_q += 2 * CL;
+    }
+    if (++iss_st == kSsStages) iss_st = 0;
+    ++n_iss;
+  };
+  if (lane == 0)
+    while (n_iss < kSsStages - 1 && n_iss < n_issue) issue();
+
+  float hq[NF], hk[NF], hv[NF], hi[NI];
+  int cur_row = -1;
+  float ucarry[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ucarry[e] = 0.f;
+
+  Cur pos = start;
+  int st = 0, prv_st = kSsStages - 1;
+  uint32_t parity = 0;
+  for (int n = 0; n < n_issue; ++n) {
+    const int row = pos.row, k = pos.k;
+    if (row != cur_row) {  // new channel: taps into registers
+      cur_row = row;
+      const int c = row % C;
+      const int g = c / gs;
+      const float dr = decay ? __ldg(decay + g) : 0.f;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        hq[j] = j < lhf ? __ldg(feat_taps + (static_cast<size_t>(0) * C + c) * lhf + j) : 0.f;
+        hk[j] = j < lhf ? __ldg(feat_taps + (static_cast<size_t>(1) * C + c) * lhf + j) : 0.f;
+        hv[j] = j < lhf ? __ldg(feat_taps + (static_cast<size_t>(2) * C + c) * lhf + j) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        float h = j < lh ? __ldg(inner_taps + static_cast<size_t>(g) * lh + j) : 0.f;
+        if (decay) h *= exp2f(-dr * static_cast<float>(j));
+        hi[j] = h;
+      }
+    }
+    mbar_wait(&bars[st], parity);
+    const T* cur = ring + st * 3 * kSsChunk;
+    const T* prv = ring + prv_st * 3 * kSsChunk;
+    const bool row_start = (k == 0);
+    float rk[8], rv[8], rq[8], pk[8], pv[8], pq[8];
+    lds8<T>(rk, cur + 8 * lane);
+    lds8<T>(rv, cur + kSsChunk + 8 * lane);
+    lds8<T>(rq, cur + 2 * kSsChunk + 8 * lane);
+    lds8<T>(pk, prv + kSsChunk - 8);  // the previous chunk's last 8 steps (broadcast)
+    lds8<T>(pv, prv + 2 * kSsChunk - 8);
+    lds8<T>(pq, prv + 3 * kSsChunk - 8);
+    __syncwarp();
+    // the stage read before this one is free now: refill it S - 1 entries ahead
+    if (lane == 0 && n_iss < n_issue) issue();
+    prv_st = st;
+    if (++st == kSsStages) st = 0, parity ^= 1u;
+    pos.next(nch);
+    if (row_start) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pk[e] = pv[e] = pq[e] = ucarry[e] = 0.f;
+    }
+    float hist[8], fk[8], fv[8], u[8], acc[8], fq[8];
+    hist_shfl<NHF>(hist, rk, pk, lane);
+    fir_pairs<NF>(fk, rk, hist, hk);
+    hist_shfl<NHF>(hist, rv, pv, lane);
+    fir_pairs<NF>(fv, rv, hist, hv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) u[e] = fk[e] * fv[e];
+    // u history: lane l - 1's u; lane 0 the previous chunk's lane 31 (carried)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (e >= 8 - NHI) {
+        const float s = __shfl_sync(kFull, u[e], (lane + 31) & 31);
+        hist[e] = lane == 0 ? ucarry[e] : s;
+        ucarry[e] = s;  // lane 0 receives lane 31's u: the next chunk's carry
+      } else {
+        hist[e] = 0.f;
+      }
+    }
+    fir_pairs<NI>(acc, u, hist, hi);
+    hist_shfl<NHF>(hist, rq, pq, lane);
+    fir_pairs<NF>(fq, rq, hist, hq);
+    const bool store = !(warm && n == 0);
+    const int t = k * kSsChunk + 8 * lane;
+    if (store && t < L) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = acc[e] * fq[e];
+      T* yp = y + static_cast<size_t>(row) * L + t;
+      if constexpr (sizeof(T) == 4) {
+        st_stream16(yp, pack16<T>(o));
+        st_stream16(yp + 4, pack16<T>(o + 4));
+      } else {
+        st_stream16(yp, pack16<T>(o));
+      }
+    }
+  }
+}
+
 template <typename T, int NF, int NI>
 static int launch_se(const void* proj, void* y, const float* ft, int lhf, const float* it, const float* dec,
                      int lh, int gs, int B, int C, int L, cudaStream_t st) {
   const bool vec = (L % 8 == 0) && aligned16(proj) && aligned16(y);
   auto kern = vec ? se_mixer_kernel<T, NF, NI, true> : se_mixer_kernel<T, NF, NI, false>;
-  constexpr int RING = sizeof(T) == 2 ? (kSeThreads / 32) * 2 * 3 * 256 * static_cast<int>(sizeof(T)) : 0;
+  constexpr int RING = (kSeThreads / 32) * 2 * 3 * 256 * static_cast<int>(sizeof(T));
   const int smem = vec ? RING : 0;
   static bool attr_set = false;
   if (!attr_set && RING > 0) {
@@ -311,9 +526,37 @@ static int launch_se(const void* proj, void* y, const float* ft, int lhf, const 
   return check_launch("se_mixer_kernel");
 }
 
+template <typename T, int NF, int NI>
+static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf, const float* it, const float* dec,
+                            int lh, int gs, int B, int C, int L, cudaStream_t st) {
+  auto kern = se_stream_kernel<T, NF, NI>;
+  constexpr int SMEM = kSsWarps * kSsStages * (3 * kSsChunk * static_cast<int>(sizeof(T)) + 8);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSsWarps * 32, SMEM);
+  const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * C * B;
+  if (total > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many chunks");
+  long long grid = (total + kSsWarps - 1) / kSsWarps;
+  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (grid > cap) grid = cap;
+  kern<<<static_cast<int>(grid), kSsWarps * 32, SMEM, st>>>(static_cast<const T*>(proj), static_cast<T*>(y), ft, lhf,
+                                                             it, dec, lh, gs, B, C, L);
+  return check_launch("se_stream_kernel");
+}
+
 template <typename T>
 static int launch_se_dispatch(const void* proj, void* y, const float* ft, int lhf, const float* it,
                               const float* dec, int lh, int gs, int B, int C, int L, cudaStream_t st) {
+  const bool vec = (L % 8 == 0) && aligned16(proj) && aligned16(y);
+  if (vec && lhf == 7 && lh == 7) return launch_se_stream<T, 7, 7>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);
+  if (vec && lhf <= 8 && lh <= 8) return launch_se_stream<T, 8, 8>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);
   if (lhf == 7 && lh == 7) return launch_se<T, 7, 7>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);
   if (lhf <= 8 && lh <= 8) return launch_se<T, 8, 8>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);
   if (lhf <= 8) return launch_se<T, 8, 16>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run here, after gpurun brought the .ncu-rep back).
 
-    python scripts/ncu_summary.py gpurun_out/prof_mr.ncu-rep profiles/r01_mr_mixer_ncu.txt
+    python scripts/ncu_summary.py gpurun_out/prof_mr.ncu-rep profiles/r01_mr_mixer_ncu.txt mr
     python scripts/ncu_summary.py --launches gpurun_out/launches.csv profiles/r01_launches.txt
 """
 
@@ -50,7 +50,7 @@ def raw_metrics(rep: str) -> dict:
     return res
 
 
-def summarize_rep(rep: str, dst: str) -> None:
+def summarize_rep(rep: str, dst: str, workload: str | None = None) -> None:
     m = raw_metrics(rep)
     lines = [f"ncu --set full capture: {os.path.basename(rep)}", f"kernel: {m.pop('kernel')}", ""]
     lines += [f"{k:85s} {v}" for k, v in m.items()]
@@ -64,8 +64,10 @@ def summarize_rep(rep: str, dst: str) -> None:
     print("\n".join(lines))
     tj = os.path.join(os.path.dirname(dst), "ncu_traffic.json")
     d = json.load(open(tj)) if os.path.exists(tj) else {}
-    d[os.path.basename(dst)] = {"kernel": "two_stage_kernel" if "two_stage" in lines[1] else lines[1],
-                                "traffic_bytes": traffic}
+    ent = {"kernel": lines[1][len("kernel: "):], "traffic_bytes": traffic}
+    if workload:
+        ent["workload"] = workload
+    d[os.path.basename(dst)] = ent
     json.dump(d, open(tj, "w"), indent=1)
 
 
@@ -91,4 +93,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         summarize_launches(sys.argv[2], sys.argv[3])
     else:
-        summarize_rep(sys.argv[1], sys.argv[2])
+        summarize_rep(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)

@@ -219,7 +219,9 @@ def test_mr_mixer_tcgen05_vs_oracle(B, C, L, lhf, lh, gs):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("B,C,L,lhf,lh,gs", [(1, 4, 4096, 7, 7, 1), (2, 3, 1000, 14, 14, 3), (1, 2, 2049, 3, 16, 1)])
+@pytest.mark.parametrize("B,C,L,lhf,lh,gs", [(1, 4, 4096, 7, 7, 1), (2, 3, 1000, 14, 14, 3), (1, 2, 2049, 3, 16, 1),
+                                            (3, 5, 1000, 7, 7, 5), (2, 6, 2056, 8, 5, 2), (2, 64, 8192, 7, 7, 1),
+                                            (1, 8, 264, 4, 8, 4)])
 def test_se_mixer_vs_oracle(dtype, B, C, L, lhf, lh, gs):
     rng = np.random.default_rng(L + lh + lhf)
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
@@ -229,6 +231,23 @@ def test_se_mixer_vs_oracle(dtype, B, C, L, lhf, lh, gs):
     taps = rnd(rng.standard_normal((C // gs, lh)) / np.sqrt(lh))
     y = ops.hyena_mixer(dev(proj, tdt), dev(feat), dev(taps), gs, se_only=True).float().cpu().numpy()
     want = _mixer_oracle(np.asarray(dev(proj, tdt).double().cpu()), feat, explicit_bank_from_taps(taps, gs))
+    assert oracle.rel_err(y, want) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_se_mixer_decay_vs_oracle(dtype):
+    """Regularised inner taps (core.py:146): the decay 2^(-rate*log2(base)*t) applied in-kernel."""
+    B, C, L, lhf, lh = 2, 16, 6144, 7, 7
+    rng = np.random.default_rng(7)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    rnd = (lambda a: a) if dtype == "f32" else bf16_round
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    taps = rnd(rng.standard_normal((C, lh)) / np.sqrt(lh))
+    dec = np.linspace(0.01, 2.0, C).astype(np.float32)
+    y = ops.hyena_mixer(dev(proj, tdt), dev(feat), dev(taps), 1, decay=dev(dec), se_only=True).float().cpu().numpy()
+    eff = taps * np.exp2(-dec.astype(np.float64)[:, None] * np.arange(lh)[None, :])
+    want = _mixer_oracle(np.asarray(dev(proj, tdt).double().cpu()), feat, explicit_bank_from_taps(eff, 1))
     assert oracle.rel_err(y, want) < TOL[dtype]
 
 
