@@ -127,6 +127,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def operator_roofline(op_tf: float, peaks: dict, dtype: str, flops: int) -> dict:
+    """Whole operator step against the peak of the pipe its GEMMs run on: bf16 -> tensor cores
+    (MEASURED_PEAKS.json); fp32 -> CUDA-core FFMA (TF32 off for the 1e-5 parity bar), peak
+    derived as SMs x 128 lanes x 2 FLOP x max SM clock (not in MEASURED_PEAKS.json)."""
+    if dtype == "f32":
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        return {"bound": "fp32 cuda-core", "achieved": op_tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": op_tf / peak, "flops_per_step_per_rank": flops,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"}
+    return {"bound": "tensor", "achieved": op_tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": op_tf / peaks["bf16_tflops"], "flops_per_step_per_rank": flops}
+
+
 def ncu_traffic(workload: str):
     """dram read+write bytes per launch of the workload's dominant kernel, from the committed
     ncu --set full summaries (profiles/ncu_traffic.json, written by scripts/ncu_summary.py)."""
@@ -320,9 +333,7 @@ def run_ours(args, wl):
                         "input, forward, D2H of its result (copies of neighbouring steps overlap the forward)"},
         "roofline": dom,
         "roofline_kernels": kinfo,
-        "roofline_operator": {"bound": "tensor", "achieved": op_tf, "peak": peaks["bf16_tflops"],
-                              "unit": "TFLOP/s", "frac": op_tf / peaks["bf16_tflops"],
-                              "flops_per_step_per_rank": run.op_flops // ws},
+        "roofline_operator": operator_roofline(op_tf, peaks, wl["dtype"], run.op_flops // ws),
         "phases_ms": {"kernels": {k["label"]: k["launch_ms"] for k in kinfo},
                       "rest (cuBLAS GEMMs, comm, elementwise)": ms_step - sum(kern_ms)},
         "clocks": clocks,
