@@ -13,6 +13,7 @@ testing.random_*), so the inputs are bit-reproducible.
 
 from __future__ import annotations
 
+import dataclasses
 import os
 import sys
 
@@ -331,6 +332,134 @@ def gen_builders() -> None:
     save("builders", c)
 
 
+def grads_arrays(prefix: str, g: "hyena.HyenaGrads") -> dict:
+    """HyenaGrads -> flat arrays: dx, dense/factored projection grads, filter leaves stacked
+    over groups ({prefix}.f.{role}.{leaf} of shape (n_groups, ...))."""
+    out = {f"{prefix}.dx": g.dx}
+    for name in ("dw_q", "dw_k", "dw_v", "dw_out"):
+        val = getattr(g, name)
+        if isinstance(val, tuple):
+            out[f"{prefix}.{name}.left"], out[f"{prefix}.{name}.right"] = val
+        else:
+            out[f"{prefix}.{name}"] = val
+    for role, per_group in g.filters.items():
+        for leaf in per_group[0]:
+            out[f"{prefix}.f.{role}.{leaf}"] = np.stack([d[leaf] for d in per_group])
+    return out
+
+
+def gen_backward() -> None:
+    """Reference backward passes: conv adjoints (core.py:245-268), two-stage backward
+    (blockconv.py:223-264, incl. the hand example of pkg/tests/test_blockconv.py:154-160),
+    operator backward per variant/backend/dtype (hyena.py:250-284), layout backward
+    (hyena.py:409-417) and the sharded a2a backward (cpsim.py:440-446)."""
+    from convhybrid.core import causal_conv_input_grad, causal_conv_taps_grad
+    c = {}
+    rng = make_rng(1100)
+    n = 0
+    for d, gs, length, lh in ((3, 1, 40, 5), (4, 2, 50, 6), (2, 1, 3, 9), (6, 3, 300, 7), (4, 4, 257, 40),
+                              (2, 1, 1000, 129), (5, 5, 64, 1)):
+        g = random_explicit_groups(rng, d, gs, lh)
+        x = rng.standard_normal((d, length))
+        dy = rng.standard_normal((d, length))
+        c[f"cg{n}.x"], c[f"cg{n}.dy"], c[f"cg{n}.taps"], c[f"cg{n}.gs"] = x, dy, g.materialized(), gs
+        c[f"cg{n}.dx"] = causal_conv_input_grad(dy, g.taps_per_channel())
+        c[f"cg{n}.dtaps"] = causal_conv_taps_grad(dy, x, g)
+        n += 1
+    c["n_cg"] = n
+    # two-stage backward: hand example, then random gated / ungated
+    _, saved = bc.two_stage_forward_saved(SeqTensor([[1.0, 2.0, 3.0, 4.0]]), uniform_groups(1, [1.0, 1.0]), 2)
+    hg = bc.two_stage_backward(saved, np.ones((1, 4)))
+    c["hand.dtaps"], c["hand.dv"] = hg.dtaps, hg.dv
+    n = 0
+    for dtype in ("f64", "f32"):
+        for d, dg, length, lh, lb, gated in ((4, 2, 24, 5, 4, True), (6, 3, 70, 9, 8, False),
+                                              (4, 1, 300, 128, 128, True), (3, 3, 260, 129, 128, True),
+                                              (2, 1, 130, 7, 16, True)):
+            g = random_explicit_groups(rng, d, dg, lh)
+            v = random_seq(rng, d, length, dtype)
+            q = random_seq(rng, d, length, dtype) if gated else None
+            k = random_seq(rng, d, length, dtype) if gated else None
+            dy = rng.standard_normal((d, length))
+            _, saved = bc.two_stage_forward_saved(v, g, lb, q=q, k=k)
+            tg = bc.two_stage_backward(saved, dy)
+            c[f"tb{n}.v"], c[f"tb{n}.dy"] = v.data, dy
+            if gated:
+                c[f"tb{n}.q"], c[f"tb{n}.k"] = q.data, k.data
+                c[f"tb{n}.dq"], c[f"tb{n}.dk"] = tg.dq, tg.dk
+            c[f"tb{n}.taps"], c[f"tb{n}.gs"], c[f"tb{n}.lb"] = g.materialized(), dg, lb
+            c[f"tb{n}.dv"], c[f"tb{n}.dtaps"] = tg.dv, tg.dtaps
+            n += 1
+    c["n_tb"] = n
+    # operator backward
+    specs = [
+        ("SE", 8, 64, 1, None, 16, "blocked", "f64", False),
+        ("SE", 8, 96, 2, 9, 8, "direct", "f32", True),
+        ("SE", 4, 40, 1, None, 16, "fft", "f64", False),
+        ("MR", 8, 256, 1, 128, 128, "blocked", "f64", False),
+        ("MR", 8, 300, 2, 128, 128, "blocked", "f32", False),
+        ("MR", 4, 64, 1, 24, 8, "blocked", "f64", True),
+        ("MR", 8, 130, 1, 64, 16, "direct", "f32", False),
+        ("LI", 8, 64, 1, None, 16, "fft", "f64", False),
+        ("LI", 4, 48, 2, None, 16, "direct", "f32", False),
+        ("LI", 8, 256, 1, None, 16, "fft", "f64", True),
+    ]
+    n = 0
+    for variant, width, length, gs, inner_len, lb, backend, dtype, factored in specs:
+        rng = make_rng(1200 + n)
+        cfg = hyena.make_hyena_config(variant, width, rng, seq_len=length, group_size=gs,
+                                      inner_len=inner_len, block_size=lb, backend=backend)
+        if factored:
+            r = max(1, width // 2)
+            cfg = dataclasses.replace(cfg, w_v=(rng.standard_normal((width, r)), rng.standard_normal((r, width))))
+            c[f"hb{n}.cfg.w_v.left"], c[f"hb{n}.cfg.w_v.right"] = cfg.w_v
+        x = random_seq(make_rng(1300 + n), width, length, dtype)
+        dy = make_rng(1400 + n).standard_normal((width, length))
+        y, saved = hyena.hyena_forward_saved(x, cfg)
+        g = hyena.hyena_backward(saved, dy)
+        c.update(cfg_arrays(f"hb{n}.cfg", cfg))
+        c.update(grads_arrays(f"hb{n}.g", g))
+        c[f"hb{n}.x"], c[f"hb{n}.dy"], c[f"hb{n}.y"] = x.data, dy, y.data
+        c[f"hb{n}.args"] = np.array([variant, str(width), str(length), str(gs), str(inner_len), str(lb),
+                                     backend, dtype, str(factored)])
+        n += 1
+    c["n_hb"] = n
+    # layout backward (residual stack SE-MR-LI)
+    width, length = 8, 64
+    rng = make_rng(1500)
+    layers = (hyena.make_hyena_config("SE", width, rng, seq_len=length, block_size=16),
+              hyena.make_hyena_config("MR", width, rng, seq_len=length, inner_len=32, block_size=32),
+              hyena.make_hyena_config("LI", width, rng, seq_len=length, block_size=16))
+    stack = hyena.OperatorStack(layers, residual=True)
+    x = random_seq(make_rng(1501), width, length)
+    dy = make_rng(1502).standard_normal((width, length))
+    _, saveds = hyena.layout_forward_saved(x, stack)
+    dx, lg = hyena.layout_backward(stack, saveds, dy)
+    for i, cfg in enumerate(layers):
+        c.update(cfg_arrays(f"lay{i}", cfg))
+        c.update(grads_arrays(f"lg{i}", lg[i]))
+    c["lay.x"], c["lay.dy"], c["lay.dx"] = x.data, dy, dx
+    # sharded a2a backward
+    n = 0
+    for n_ranks, d, dg, length, lh, layout in ((2, 4, 1, 32, 3, "sequential"), (4, 8, 2, 64, 5, "zigzag"),
+                                               (4, 8, 1, 64, 5, "sequential")):
+        rng = make_rng(1600 + n)
+        groups = random_explicit_groups(rng, d, dg, lh)
+        x = random_seq(rng, d, length)
+        w = rng.standard_normal((d, length))
+        grp = cpsim.SimGroup(n_ranks)
+        _, asaved = cpsim.a2a_conv_saved(cpsim.shard(x, n_ranks, layout), groups, grp)
+        dxs = cpsim.a2a_conv_backward(asaved, cpsim.shard(SeqTensor(w), n_ranks, layout), grp)
+        c[f"ab{n}.args"] = np.array([str(n_ranks), str(d), str(dg), str(length), str(lh), layout])
+        c[f"ab{n}.x"], c[f"ab{n}.dy"], c[f"ab{n}.taps"] = x.data, w, groups.materialized()
+        c[f"ab{n}.dx"] = cpsim.gather(dxs).data
+        c[f"ab{n}.elements"] = grp.total_elements("a2a_conv")
+        c[f"ab{n}.messages"] = grp.total_messages("a2a_conv")
+        n += 1
+    c["n_ab"] = n
+    save("backward", c)
+
+
 if __name__ == "__main__":
     gen_direct()
     gen_blockconv()
@@ -340,3 +469,4 @@ if __name__ == "__main__":
     gen_layout()
     gen_cpsim()
     gen_builders()
+    gen_backward()

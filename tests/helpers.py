@@ -37,7 +37,9 @@ def oracle_cfg(z: dict, prefix: str) -> dict:
     cfg = {"variant": _s(z[f"{prefix}.variant"]), "width": int(z[f"{prefix}.width"]),
            "block_size": int(z[f"{prefix}.block_size"]), "backend": _s(z[f"{prefix}.backend"])}
     for name in ("w_q", "w_k", "w_v", "w_out"):
-        cfg[name] = z[f"{prefix}.{name}"]
+        # factored projections (hyena.py:48-65) are stored as .left / .right next to the dense
+        cfg[name] = ((z[f"{prefix}.{name}.left"], z[f"{prefix}.{name}.right"])
+                     if f"{prefix}.{name}.left" in z else z[f"{prefix}.{name}"])
     for name in ("q_feat", "k_feat", "v_feat", "inner"):
         cfg[name] = oracle_bank(z, f"{prefix}.{name}")
     return cfg
@@ -78,3 +80,21 @@ def product_groups_from_taps(taps: np.ndarray, gs: int):
     from paper_2503_01868_b200 import ExplicitFilter, GroupSpec
     taps = np.atleast_2d(np.asarray(taps, dtype=np.float64))
     return GroupSpec(taps.shape[0] * gs, gs, tuple(ExplicitFilter(t) for t in taps))
+
+
+def grads_from_golden(z: dict, prefix: str) -> dict:
+    """The flat arrays written by make_golden.grads_arrays, back in the oracle's grads form."""
+    out = {"dx": z[f"{prefix}.dx"], "filters": {}}
+    for name in ("dw_q", "dw_k", "dw_v", "dw_out"):
+        out[name] = ((z[f"{prefix}.{name}.left"], z[f"{prefix}.{name}.right"])
+                     if f"{prefix}.{name}.left" in z else z[f"{prefix}.{name}"])
+    for key in z:
+        if key.startswith(f"{prefix}.f."):
+            role, leaf = key[len(prefix) + 3:].split(".")
+            out["filters"].setdefault(role, {})[leaf] = z[key]
+    return out
+
+
+def stack_filter_grads(per_group: list) -> dict:
+    """[{leaf: grad} per group] -> {leaf: (n_groups, ...)}."""
+    return {leaf: np.stack([d[leaf] for d in per_group]) for leaf in per_group[0]}
