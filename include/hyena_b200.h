@@ -28,6 +28,11 @@
  *   hy_fft_conv_fwd         fft.py:128-145       fft_conv, fused with the k*v / q gates as used
  *                           hyena.py:183-186     by the LI operator (backend="fft")
  *   hy_halo_correction_fwd  cpsim.py:498-510     p2p_conv_overlapped's correction conv
+ *   hy_causal_conv_bwd      core.py:245-268      causal_conv_input_grad + causal_conv_taps_grad
+ *                           blockconv.py:223-264 two_stage_backward (transposed factors, two-pass dtaps)
+ *                           cpsim.py:440-446     a2a_conv_backward's slab step (_slab_backward)
+ *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
+ *                           core.py:255-268      the tap correlation it consumes
  */
 #ifndef HYENA_B200_H
 #define HYENA_B200_H
@@ -138,6 +143,30 @@ HY_API int hy_fft_conv_fwd(const void* q, const void* k, const void* v, void* y,
  * for t < H = lh - 1, where halo (B, C, H) holds the predecessor's last H steps. */
 HY_API int hy_halo_correction_fwd(const void* halo, void* y, const void* taps,
                            int B, int C, int L, int lh, int group_size, int dtype, void* stream);
+
+/* ---------------------------------------------------------------- backward
+ * Adjoints of the causal FIR (core.py:245-268), CUDA cores, fp32 / bf16 / fp64:
+ *   dx[b,c,t]    = sum_j taps[c/gs, j] * dy[b,c,t+j]                (causal_conv_input_grad)
+ *   dtaps[g, j]  = sum_{c in g} sum_{b,t} dy[b,c,t] * x[b,c,t-j]    (causal_conv_taps_grad)
+ * dx or dtaps may be NULL (not computed). dtaps is fp32 for HY_F32 / HY_BF16, fp64 for HY_F64,
+ * summed deterministically (per-CTA partials in ws, then a fixed-order fp64 reduce: the
+ * two-pass filter gradient of blockconv.py:246-262). lh <= 2048. Used for the SE / MR inner
+ * conv and the featurizers in two_stage_backward (blockconv.py:223-264) / hyena_backward
+ * (hyena.py:250-284), and for the slab step of a2a_conv_backward (cpsim.py:440-446). */
+HY_API size_t hy_causal_conv_bwd_workspace_size(int B, int C, int L, int lh, int dtype);
+HY_API int hy_causal_conv_bwd(const void* dy, const void* x, void* dx, void* dtaps, const void* taps,
+                              int B, int C, int L, int lh, int group_size, int dtype,
+                              void* ws, size_t ws_bytes, void* stream);
+/* Hyena-LI filter-parameter gradients for h_t = sum_n R_n lam_n^t (npoles <= 8) straight from
+ * dc (gradient at the conv output) and u (conv input), without the length-L tap gradient:
+ *   d_res[g,n]  = sum_{b, c in g} sum_s dc[s] S_n[s],     S_n[s] = lam_n S_n[s-1] + u[s]
+ *   d_pole[g,n] = R_n sum_{b, c in g} sum_s dc[s] P_n[s], P_n[s] = lam_n P_n[s-1] + S_n[s-1]
+ * = filter_param_grads(ImplicitFilter, causal_conv_taps_grad(dc, u)) (hyena.py:193-211).
+ * fp32 / bf16 activations; d_res, d_pole fp32 (n_groups, npoles). */
+HY_API size_t hy_li_param_grad_workspace_size(int B, int C);
+HY_API int hy_li_param_grad(const void* dc, const void* u, const float* residues, const float* poles, int npoles,
+                            int group_size, int B, int C, int L, int dtype, float* d_res, float* d_pole,
+                            void* ws, size_t ws_bytes, void* stream);
 
 /* Debug / tuning: CTA-0 per-tile timeline (clock64) of the last two-stage launch made
  * with HY_TS_TRACE=1 in the environment; n <= 4096 values, 8 events per tile. */

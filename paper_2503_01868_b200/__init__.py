@@ -6,15 +6,27 @@ C-ABI of include/hyena_b200.h; there is no CPU fallback.
 
 from . import cp, fft
 from .cp import CPGroup, ShardedSeq, a2a_conv, a2a_conv_pipelined, gather, p2p_conv, p2p_conv_overlapped, shard
+from .backward import (
+    DeviceGrads,
+    HyenaGrads,
+    filter_param_grads,
+    grad_for_path,
+    hyena_backward,
+    iter_params,
+    layout_backward,
+    operator_backward,
+)
 from .blockconv import (
     MultiplyCounter,
     ToeplitzFactors,
+    TwoStageGrads,
     TwoStageIneligibleError,
     assemble_toeplitz,
     block_conv,
     build_factors,
     chunk_parallel_forward,
     spill_count,
+    two_stage_backward,
     two_stage_flops,
     two_stage_forward,
     two_stage_forward_saved,
@@ -25,6 +37,8 @@ from .core import (
     ImplicitFilter,
     RegularizedFilter,
     SeqTensor,
+    causal_conv_input_grad,
+    causal_conv_taps_grad,
     direct_causal_conv,
     filter_length,
     full_toeplitz,

@@ -40,6 +40,10 @@ SIGNATURES = {
     "hy_li_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_li_conv_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_li_conv_segmented_fwd": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_longlong, _I, _P]),
+    "hy_causal_conv_bwd_workspace_size": (_SZ, [_I, _I, _I, _I, _I]),
+    "hy_causal_conv_bwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
+    "hy_li_param_grad_workspace_size": (_SZ, [_I, _I]),
+    "hy_li_param_grad": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 
 _lib = None

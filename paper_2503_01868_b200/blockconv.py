@@ -156,6 +156,44 @@ def two_stage_forward_saved(v: SeqTensor, groups: GroupSpec, block_size: int, q:
     return SeqTensor(y.cpu().numpy(), dtype=v.dtype), saved
 
 
+@dataclass
+class TwoStageGrads:
+    """(blockconv.py:152-157)."""
+
+    dv: np.ndarray
+    dq: np.ndarray | None
+    dk: np.ndarray | None
+    dtaps: np.ndarray  # (n_groups, filter_len)
+
+
+def two_stage_backward(saved: TwoStageSaved, dy) -> TwoStageGrads:
+    """Analytic gradients of the gated two-stage forward (blockconv.py:223-264) on the GPU, fp64:
+    dq = dy * conv_out, dc = dy * q, du = the transposed-factor (anti-causal) conv of dc, and the
+    filter gradient by the deterministic two-pass correlation (per-CTA partials, fixed-order
+    reduce) of hy_causal_conv_bwd; dk = du * v, dv = du * k."""
+    import torch
+
+    from .ops import causal_conv_bwd
+    if not isinstance(saved, TwoStageSaved):
+        raise ValueError("backward needs the TwoStageSaved context from two_stage_forward_saved")
+    dy = dy.data if isinstance(dy, SeqTensor) else np.asarray(dy, dtype=np.float64)
+    if dy.shape != saved.gated_input.shape:
+        raise ValueError(f"dy shape {dy.shape} does not match forward shape {saved.gated_input.shape}")
+    dev = device()
+    f64 = lambda a: torch.from_numpy(np.array(a, dtype=np.float64, copy=True)).to(dev)  # noqa: E731
+    dyd = f64(dy)
+    qd = None if saved.q is None else f64(saved.q.data)
+    dq = dyd * f64(saved.conv_out) if qd is not None else None
+    dc = dyd * qd if qd is not None else dyd
+    groups = saved.groups
+    du, dtaps = causal_conv_bwd(dc, f64(saved.gated_input), group_taps_device(groups, torch.float64),
+                                groups.group_size)
+    dk = du * f64(saved.v.data) if saved.k is not None else None
+    dv = du * f64(saved.k.data) if saved.k is not None else du
+    h = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+    return TwoStageGrads(dv=h(dv), dq=h(dq), dk=h(dk), dtaps=h(dtaps))
+
+
 def chunk_parallel_forward(v: SeqTensor, taps, block_size: int, counter: MultiplyCounter | None = None) -> SeqTensor:
     """One shared tap vector for every channel (blockconv.py:267-293)."""
     import torch

@@ -313,6 +313,40 @@ def a2a_conv(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str =
     return _a2a(local, groups, grp, 1, layout, "a2a_conv", conv_slab or _gpu_slab_conv)
 
 
+@dataclass
+class A2ASaved:
+    """Forward context of the all-to-all scheme (cpsim.py:421-425)."""
+
+    groups: GroupSpec
+    layout: str
+    n_ranks: int
+
+
+def a2a_conv_saved(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str = "sequential",
+                   conv_slab=None):
+    """(y shard, A2ASaved) (cpsim.py:433-437)."""
+    return a2a_conv(local, groups, grp, layout, conv_slab), A2ASaved(groups, layout, grp.n_ranks)
+
+
+def _gpu_slab_backward(natural: torch.Tensor, bank: GroupSpec) -> torch.Tensor:
+    """Input adjoint of the slab conv (cpsim.py:417-418): dx[t] = sum_j h[j] dy[t+j]."""
+    from .ops import causal_conv_bwd
+    dx, _ = causal_conv_bwd(natural.contiguous(), None, _taps_tensor(bank, natural), bank.group_size,
+                            want_dtaps=False)
+    return dx
+
+
+def a2a_conv_backward(saved: A2ASaved, dy_local: torch.Tensor, grp: CPGroup, layout: str | None = None,
+                      conv_slab=None) -> torch.Tensor:
+    """Input gradients via two more all-to-all rounds, the correlation on the channel slab
+    (cpsim.py:440-446); accounted under the forward's "a2a_conv" scheme like the reference."""
+    if not isinstance(saved, A2ASaved):
+        raise ValueError("backward needs the A2ASaved context from a2a_conv_saved")
+    if grp.n_ranks != saved.n_ranks or (layout is not None and layout != saved.layout):
+        raise ValueError("gradient sharding does not match the forward sharding")
+    return _a2a(dy_local, saved.groups, grp, 1, saved.layout, "a2a_conv", conv_slab or _gpu_slab_backward)
+
+
 def a2a_conv_pipelined(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int,
                        layout: str = "sequential", conv_slab=None) -> torch.Tensor:
     """The a2a scheme in n_pipe channel segments (cpsim.py:449-454)."""

@@ -269,3 +269,69 @@ def li_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, residues: torch.Tensor
                                    r.data_ptr(), p.data_ptr(), p.shape[1], group_size, B, C, L,
                                    _dtype_code(proj), _stream()), "li_mixer")
     return y
+
+
+# ---------------------------------------------------------------- backward
+
+
+def causal_conv_bwd(dy: torch.Tensor, x, taps, group_size: int = 1, want_dx: bool = True,
+                    want_dtaps: bool = True):
+    """Adjoints of y = h conv x (core.py:245-268): (dx, dtaps) with
+    dx[t] = sum_j h[j] dy[t+j] and dtaps[g, j] = sum_{c in g, b, t} dy[t] x[t-j].
+
+    dy, x: (B, C, L) or (C, L); taps: (G, lh). Either output may be skipped (None returned);
+    dtaps needs x and its length is taps.shape[-1] (or pass taps=None with want_dx=False and
+    an int lh via `taps`)."""
+    squeeze = dy.dim() == 2
+    dy3 = _as3(dy)
+    x3 = None if x is None else _as3(x)
+    _check_device(dy3, x3)
+    if x3 is not None and (x3.shape != dy3.shape or x3.dtype != dy3.dtype):
+        raise ValueError(f"x {tuple(x3.shape)}/{x3.dtype} does not match dy {tuple(dy3.shape)}/{dy3.dtype}")
+    B, C, L = dy3.shape
+    if isinstance(taps, int):
+        lh, tp = taps, None
+        if want_dx:
+            raise ValueError("dx needs the taps tensor")
+    else:
+        tp = _taps(taps, dy3)
+        lh = tp.shape[-1]
+    if C % group_size != 0:
+        raise ValueError(f"group_size {group_size} does not divide channel count {C}")
+    code = _dtype_code(dy3)
+    lib = _lib.load()
+    dx = torch.empty_like(dy3) if want_dx else None
+    dtaps = ws = None
+    if want_dtaps:
+        if x3 is None:
+            raise ValueError("dtaps needs x")
+        dtaps = torch.empty((C // group_size, lh), dtype=tap_dtype(dy3.dtype), device=dy3.device)
+        nbytes = int(lib.hy_causal_conv_bwd_workspace_size(B, C, L, lh, code))
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dy3.device)
+    _lib.check(lib.hy_causal_conv_bwd(dy3.data_ptr(), _ptr(x3), _ptr(dx), _ptr(dtaps), _ptr(tp), B, C, L, lh,
+                                      group_size, code, _ptr(ws), 0 if ws is None else ws.numel(), _stream()),
+               "causal_conv_bwd")
+    if dx is not None and squeeze:
+        dx = dx[0]
+    return dx, dtaps
+
+
+def li_param_grad(dc: torch.Tensor, u: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor,
+                  group_size: int = 1):
+    """(d_residues, d_poles), each (G, n_poles) fp32, of sum(dc * (h conv u)) for the implicit
+    filter h_t = sum_n R_n lam_n^t — filter_param_grads(ImplicitFilter, causal_conv_taps_grad(dc, u))
+    (hyena.py:193-211, core.py:255-268) by exact per-mode scans, no length-L tap gradient."""
+    dc3, u3 = _as3(dc), _as3(u)
+    _check_device(dc3, u3)
+    if dc3.shape != u3.shape or dc3.dtype != u3.dtype:
+        raise ValueError("dc and u must match in shape and dtype")
+    r, p = _modes(residues, poles, dc3.device)
+    B, C, L = dc3.shape
+    lib = _lib.load()
+    d_res = torch.empty_like(r)
+    d_pole = torch.empty_like(p)
+    ws = torch.empty(int(lib.hy_li_param_grad_workspace_size(B, C)), dtype=torch.uint8, device=dc3.device)
+    _lib.check(lib.hy_li_param_grad(dc3.data_ptr(), u3.data_ptr(), r.data_ptr(), p.data_ptr(), p.shape[1],
+                                    group_size, B, C, L, _dtype_code(dc3), d_res.data_ptr(), d_pole.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), _stream()), "li_param_grad")
+    return d_res, d_pole

@@ -140,3 +140,22 @@ def test_multiply_counter_model():
     counter.add_matmul(8, 8, 32)
     assert counter.multiplies == 2048
     assert oracle.two_stage_flops(64, 8, 4) == 2 * 8 * 8 * 4 * 8
+
+
+def test_backward_validation_before_device():
+    """Backward entry points reject bad contexts / shapes with the reference's ValueError before
+    any device work (blockconv.py:230-234, hyena.py:252-256), and the parameter traversal is
+    host logic (hyena.py:291-319)."""
+    with pytest.raises(ValueError):
+        hy.two_stage_backward(object(), np.ones((1, 4)))
+    with pytest.raises(ValueError):
+        hy.hyena_backward(object(), np.ones((1, 4)))
+    cfg = hy.make_hyena_config("LI", 4, hy.make_rng(3), seq_len=16, n_poles=2)
+    paths = [p for p, _ in hy.iter_params(cfg)]
+    assert paths[:4] == [("w_q",), ("w_k",), ("w_v",), ("w_out",)]
+    assert ("inner", 0, "residues") in paths and ("inner", 3, "poles") in paths
+    assert len(paths) == 4 + 3 * 4 + 2 * 4
+    g = hy.HyenaGrads(dx=None, dw_q=np.ones(1), dw_k=(np.zeros(1), np.ones(2)), dw_v=None, dw_out=None,
+                      filters={"inner": [{"residues": np.full(2, 3.0)}]})
+    assert hy.grad_for_path(g, ("w_k", "right")).shape == (2,)
+    assert hy.grad_for_path(g, ("inner", 0, "residues"))[0] == 3.0

@@ -119,3 +119,63 @@ def test_shard_gather_roundtrip_and_layouts():
         cp.shard(SeqTensor(np.zeros((2, 30))), 4)
     with pytest.raises(ValueError):
         cp.shard(SeqTensor(np.zeros((2, 12))), 4, "zigzag")
+
+
+def _bwd_worker(rank, world, port, case, q):
+    from oracle import backward as ob
+    from paper_2503_01868_b200 import SeqTensor, cp
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gs, layout = case["gs"], case["layout"]
+        groups = product_groups_from_taps(case["taps"], gs)
+        grp = cp.CPGroup()
+        xs = cp.shard(SeqTensor(case["x"]), world, layout)
+        dys = cp.shard(SeqTensor(case["dy"]), world, layout)
+
+        def conv_slab(natural, slab_groups):
+            b = explicit_bank_from_taps(slab_groups.materialized(), slab_groups.group_size)
+            return torch.from_numpy(__import__("oracle").direct_causal_conv(natural.numpy(), b))
+
+        def slab_bwd(natural, slab_groups):
+            tpc = np.repeat(slab_groups.materialized(), slab_groups.group_size, axis=0)
+            return torch.from_numpy(ob.causal_conv_input_grad(natural.numpy(), tpc))
+
+        _, saved = cp.a2a_conv_saved(torch.from_numpy(xs.shards[rank].copy()), groups, grp, layout,
+                                     conv_slab=conv_slab)
+        fwd_el = grp.total_elements("a2a_conv")
+        dx = cp.a2a_conv_backward(saved, torch.from_numpy(dys.shards[rank].copy()), grp, conv_slab=slab_bwd)
+        q.put((rank, dx.numpy(), grp.total_elements("a2a_conv") - fwd_el, grp.total_elements("a2a_conv"),
+               grp.total_messages("a2a_conv")))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("idx", range(3))
+def test_a2a_backward_matches_reference(idx):
+    """a2a_conv_backward (cpsim.py:440-446) on gloo vs the reference's sharded backward:
+    gathered dx, and the accounting (forward + backward both counted under a2a_conv)."""
+    from paper_2503_01868_b200 import SeqTensor, cp
+    z = load("backward")
+    n_ranks, d, dg, length, lh, layout = [str(a) for a in z[f"ab{idx}.args"]]
+    n_ranks = int(n_ranks)
+    case = dict(gs=int(dg), layout=layout, taps=z[f"ab{idx}.taps"], x=z[f"ab{idx}.x"], dy=z[f"ab{idx}.dy"])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bwd_worker, args=(r, n_ranks, port, case, q)) for r in range(n_ranks)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, dx, bwd_el, tot_el, tot_msg = q.get(timeout=180)
+        res[rank] = (dx, bwd_el, tot_el, tot_msg)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shards = [res[r][0] for r in range(n_ranks)]
+    got = cp.gather(cp.ShardedSeq(shards, layout)).data
+    assert np.max(np.abs(got - z[f"ab{idx}.dx"])) < 1e-12
+    assert res[0][2] == int(z[f"ab{idx}.elements"]) and res[0][3] == int(z[f"ab{idx}.messages"])
+    assert res[0][1] * 2 == res[0][2]  # the backward moves as much as the forward

@@ -1,0 +1,102 @@
+"""GPU parity of the backward kernels (hy_causal_conv_bwd, hy_li_param_grad) against the
+oracle restatement of the reference backward and the reference-generated golden vectors.
+
+Tolerances (rel_err, testing.py:57-62): fp64 1e-12; fp32 1e-5; bf16 1e-2 against the fp64
+oracle on bf16-representable inputs (north star)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import backward as ob
+from paper_2503_01868_b200 import ops
+
+from .helpers import load
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
+TDT = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).double().numpy()
+
+
+def dev(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def test_conv_bwd_golden_f64():
+    z = load("backward")
+    for n in range(int(z["n_cg"])):
+        p = f"cg{n}"
+        gs = int(z[f"{p}.gs"])
+        dx, dt = ops.causal_conv_bwd(dev(z[f"{p}.dy"]), dev(z[f"{p}.x"]), dev(z[f"{p}.taps"]), gs)
+        assert oracle.rel_err(dx.cpu().numpy(), z[f"{p}.dx"]) < TOL["f64"], p
+        assert oracle.rel_err(dt.cpu().numpy(), z[f"{p}.dtaps"]) < TOL["f64"], p
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+@pytest.mark.parametrize("B,C,L,lh,gs", [(1, 4, 4096, 7, 1), (3, 6, 1000, 5, 2), (2, 4, 8192, 128, 1),
+                                         (1, 3, 2051, 129, 3), (2, 2, 777, 1, 1), (1, 2, 3000, 2048, 2),
+                                         (4, 8, 64, 100, 4)])
+def test_conv_bwd_vs_oracle(dtype, B, C, L, lh, gs):
+    rng = np.random.default_rng(B * 1000 + L + lh)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: a)
+    dy = rnd(rng.standard_normal((B, C, L)))
+    x = rnd(rng.standard_normal((B, C, L)))
+    taps = rnd(rng.standard_normal((C // gs, lh)) / np.sqrt(lh))
+    if dtype == "f32":
+        dy, x = dy.astype(np.float32), x.astype(np.float32)
+    tt = torch.float64 if dtype == "f64" else torch.float32
+    dx, dt = ops.causal_conv_bwd(dev(dy, TDT[dtype]), dev(x, TDT[dtype]), dev(taps, tt), gs)
+    bank = oracle.explicit_bank(C, gs, taps)
+    want_dx = np.stack([ob.causal_conv_input_grad(dy[b], np.repeat(taps, gs, axis=0)) for b in range(B)])
+    want_dt = sum(ob.causal_conv_taps_grad(dy[b], x[b], bank) for b in range(B))
+    assert oracle.rel_err(dx.double().cpu().numpy(), want_dx) < TOL[dtype]
+    assert oracle.rel_err(dt.double().cpu().numpy(), want_dt) < TOL[dtype]
+
+
+def test_conv_bwd_partial_outputs_and_errors():
+    rng = np.random.default_rng(3)
+    dy = dev(rng.standard_normal((2, 4, 300)), torch.float32)
+    x = dev(rng.standard_normal((2, 4, 300)), torch.float32)
+    taps = dev(rng.standard_normal((4, 9)), torch.float32)
+    dx_only, none = ops.causal_conv_bwd(dy, None, taps, 1, want_dtaps=False)
+    assert none is None
+    dx_both, dt_both = ops.causal_conv_bwd(dy, x, taps, 1)
+    assert torch.equal(dx_only, dx_both)
+    none, dt_only = ops.causal_conv_bwd(dy, x, 9, 1, want_dx=False)
+    assert none is None and torch.equal(dt_only, dt_both)  # deterministic reduction
+    with pytest.raises(NotImplementedError):
+        ops.causal_conv_bwd(dy, x, dev(np.zeros((4, 2049)), torch.float32), 1)
+    with pytest.raises(ValueError):
+        ops.causal_conv_bwd(dy, x, taps, 3)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("B,C,L,npoles,gs,near_one", [(1, 4, 256, 8, 1, False), (2, 6, 1000, 3, 2, False),
+                                                      (1, 2, 4096, 8, 1, True), (3, 4, 77, 1, 4, False)])
+def test_li_param_grad_vs_oracle(dtype, B, C, L, npoles, gs, near_one):
+    rng = np.random.default_rng(L + npoles)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: np.asarray(a, dtype=np.float32).astype(np.float64))
+    dc = rnd(rng.standard_normal((B, C, L)))
+    u = rnd(rng.standard_normal((B, C, L)))
+    G = C // gs
+    res = rnd(rng.standard_normal((G, npoles)) / npoles)
+    poles = rnd(rng.uniform(0.99, 1.0, (G, npoles)) if near_one else rng.uniform(-0.95, 0.95, (G, npoles)))
+    poles[0, 0] = 0.0  # 0 ** 0 = 1 (core.py:147-151)
+    d_res, d_pole = ops.li_param_grad(dev(dc, TDT[dtype]), dev(u, TDT[dtype]), dev(res, torch.float32),
+                                      dev(poles, torch.float32), gs)
+    bank = {"channels": C, "group_size": gs, "filters": [("implicit", res[g], poles[g], L) for g in range(G)]}
+    dtaps = sum(ob.causal_conv_taps_grad(dc[b], u[b], bank) for b in range(B))
+    want = [ob.filter_param_grads(bank["filters"][g], dtaps[g]) for g in range(G)]
+    want_res = np.stack([w["residues"] for w in want])
+    want_pole = np.stack([w["poles"] for w in want])
+    tol = TOL[dtype] if not near_one else 5 * TOL[dtype]
+    assert oracle.rel_err(d_res.double().cpu().numpy(), want_res) < tol
+    assert oracle.rel_err(d_pole.double().cpu().numpy(), want_pole) < tol
