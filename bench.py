@@ -47,6 +47,10 @@ WORKLOADS = {
     "stripe": dict(kind="stripe", B=1, L=16384, D=4096, dtype="bf16",
                    desc="StripedHyena 2 stripe fwd (SE-MR-LI-MHA, residual), B=1, L=16384, D=4096, bf16"),
     # BASELINE.json configs[4]: L = 1M over N ranks (strong scaling), LI all-to-all
+    # backward: one training step of the C2 operator, forward + backward
+    "mr_train": dict(kind="train", variant="MR", B=4, L=8192, D=4096, inner_len=128, block_size=128, dtype="bf16",
+                     desc="Hyena-MR operator fwd+bwd (training step without optimizer), B=4, L=8192, D=4096, bf16",
+                     metric="Hyena-MR operator fwd+bwd tokens/s at D=4096 (backward: SURVEY 8(f) rank 1)"),
     "li_cp": dict(kind="cp", variant="LI", B=1, L=1 << 20, D=4096, inner_len=None, block_size=128,
                   dtype="bf16", desc="Context-parallel Hyena-LI operator fwd, L=1M, D=4096, bf16 "
                                      "(all-to-all sequence <-> channel sharding)"),
@@ -207,6 +211,31 @@ class Runner:
             self.kernels = [("MR", "MR", 4 * self.esize * D * B * L)]
             self.parallelism = f"cp{ws} (sequence sharded {L} tokens/rank, 144-step p2p history)"
             self.l_global = L * ws
+        elif kind == "train":  # forward + backward; the projections are kept for the backward
+            from paper_2503_01868_b200.backward import operator_backward
+            op = hy.HyenaOperator(build_config(wl), dt)
+            self.m = L
+            gdy = torch.Generator(device="cuda").manual_seed(7 + rank)
+            self.dy = torch.randn((B, D, L), device="cuda", dtype=dt, generator=gdy)
+
+            def train(x, ev=None):
+                proj = torch.matmul(op.w_qkv_t, x)
+                torch.matmul(op.w_out_t, op.mixer(proj))  # forward output (loss not needed)
+                evd = None if ev is None else {"inner_taps": ev[0], "featurizer_bwd": ev[1]}
+                dx, _ = operator_backward(op, x, self.dy, proj=proj, events=evd)
+                return dx
+
+            self.fwd = train
+            n = B * D * L
+            self.kernels = [
+                dict(label="inner_taps", kernel="causal_conv_bwd_kernel<DT> (hy_causal_conv_bwd: MR tap "
+                     "gradient, lag correlation of dc and u over 128 lags)", bound="fp32",
+                     work=2 * wl["inner_len"] * n, unit="TFLOP/s"),
+                dict(label="featurizer_bwd", kernel="feat_bwd_kernel (hy_featurizer_bwd: featurizers recomputed, "
+                     "gate products, anti-causal FIRs, tap gradients; 6 rows in, 3 out)", bound="hbm",
+                     work=9 * self.esize * n, unit="GB/s")]
+            self.parallelism = "single"
+            self.l_global = L
         elif kind == "stripe":
             cfgs = [build_config(dict(wl, inner_len=ln, block_size=128), variant=v)
                     for v, ln in (("SE", 7), ("MR", 128), ("LI", None))]
@@ -231,6 +260,8 @@ class Runner:
         self.x = torch.randn((B, D, self.m), device="cuda", dtype=dt, generator=gen)
         self.tokens_step = B * self.l_global
         self.op_flops = 8 * D * D * B * self.l_global * (3 if kind == "stripe" else 1)
+        if kind == "train":  # + backward GEMMs (dmixed, dW_out, dW_qkv, dx: 16 D^2 per token)
+            self.op_flops += 16 * D * D * B * L
         if kind == "stripe":
             self.op_flops += 8 * D * D * B * L // 2 + 2 * B * L * L * D  # MHA projections + causal attention
 
@@ -299,7 +330,20 @@ def run_ours(args, wl):
 
     peaks, peaks_kind = load_peaks()
     kinfo = []
-    for (label, variant, nbytes), ms in zip(run.kernels, kern_ms):
+    for kd, ms in zip(run.kernels, kern_ms):
+        if isinstance(kd, dict):  # explicit kernel description (train workloads)
+            if kd["bound"] == "hbm":
+                ach, peak = kd["work"] / (ms * 1e-3) / 1e9, peaks["hbm_gbs"]
+                extra = {"algorithmic_bytes_per_launch": kd["work"]}
+            else:
+                ach = kd["work"] / (ms * 1e-3) / 1e12
+                peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+                extra = {"algorithmic_flops_per_launch": kd["work"],
+                         "peak_source_note": "derived FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 x sm_max_mhz"}
+            kinfo.append({"kernel": kd["kernel"], "label": kd["label"], "bound": kd["bound"], "achieved": ach,
+                          "peak": peak, "unit": kd["unit"], "frac": ach / peak, **extra, "launch_ms": ms})
+            continue
+        label, variant, nbytes = kd
         ach = nbytes / (ms * 1e-3) / 1e9
         kinfo.append({"kernel": MIXER_KERNEL[variant] if wl["kind"] != "cp" else
                       "two_stage_kernel<IMPL> (hy_li_conv_fwd: implicit long conv of the rank's channel slab)",
@@ -310,7 +354,7 @@ def run_ours(args, wl):
     op_tf = run.op_flops / ws / (ms_step * 1e-3) / 1e12
     l2_bytes = run.x.numel() * run.esize * 3
     result = {
-        "metric": "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU",
+        "metric": wl.get("metric", "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU"),
         "value": run.tokens_step / (ms_step * 1e-3),
         "unit": "tokens/s",
         "n_gpus": ws,
@@ -329,7 +373,10 @@ def run_ours(args, wl):
         "e2e": {"value": run.tokens_step / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                 "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
-                "path": "streaming.HostPipeline over the public forward: per step H2D of its pinned host "
+                "path": ("streaming.HostPipeline over forward + operator_backward: per step H2D of its pinned "
+                         "host input, forward, backward, D2H of dx (copies of neighbouring steps overlap)")
+                if wl["kind"] == "train" else
+                        "streaming.HostPipeline over the public forward: per step H2D of its pinned host "
                         "input, forward, D2H of its result (copies of neighbouring steps overlap the forward)"},
         "roofline": dom,
         "roofline_kernels": kinfo,
@@ -360,6 +407,29 @@ def _time(fn, reps=1):
         fn()
         ts.append(time.perf_counter() - t)
     return statistics.median(ts)
+
+
+def cpu_seconds_train(variant, D, L, inner_len, block_size, sample_len=512):
+    """Oracle forward + backward (oracle/backward.py, restating hyena.py:162-284) on a (D, n) window,
+    scaled linearly to L. The reference's tap correlation (np.convolve, core.py:255-268) is O(n^2)
+    per channel, so linear scaling from a short window overstates the reference's speed."""
+    import oracle
+    from oracle import backward as ob
+    rng = oracle.make_rng(1, stream=0)
+    n = min(L, sample_len)
+    w0 = time.perf_counter()
+    cfg = _oracle_cfg(variant, D, L, inner_len, block_size)
+    x = rng.standard_normal((D, n))
+    dy = rng.standard_normal((D, n))
+
+    def step():
+        _, saved = ob.hyena_forward_saved(x, cfg)
+        ob.hyena_backward(saved, dy)
+
+    t = _time(step, 1)
+    return t * L / n, (f"oracle forward+backward (numpy f64, hyena.py:162-284) over a ({D}, {n}) token window, "
+                       f"scaled x{L / n:g} (linear; the reference's O(n^2) tap correlation makes this generous "
+                       f"to the reference)"), time.perf_counter() - w0
 
 
 def cpu_seconds_per_element(variant, D, L, inner_len=None, block_size=16, sample_len=2048, f32=False):
@@ -401,6 +471,9 @@ def _stripe_or_single(wl):
 def cpu_sample(wl, sample_len=2048):
     """Summed over the workload's Hyena layers: (tokens/s, description, wall seconds)."""
     D, L = wl["D"], wl["L"]
+    if wl["kind"] == "train":
+        sec, desc, wall = cpu_seconds_train(wl["variant"], D, L, wl.get("inner_len"), wl.get("block_size", 16))
+        return L / sec, desc, wall
     parts = [cpu_seconds_per_element(v, D, L, ln, 128 if wl["kind"] == "stripe" else wl.get("block_size", 16),
                                      sample_len=sample_len, f32=wl["dtype"] == "f32")
              for v, ln in _stripe_or_single(wl)]
@@ -414,6 +487,9 @@ def cpu_sample(wl, sample_len=2048):
 def run_cpu_baseline(wl):
     """Oracle (numpy, float64 like the reference) on a bounded sample of the workload."""
     value, desc, _ = cpu_sample(wl, sample_len=8192 if wl["kind"] == "op" and wl["variant"] == "MR" else 4096)
+    if wl["kind"] == "train":
+        return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"{desc}; OpenBLAS on all {os.cpu_count()} host cores"}
     return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{desc}; numpy float64 restatement of hyena.py:157-190, OpenBLAS on all "
                       f"{os.cpu_count()} host cores"}
@@ -436,7 +512,8 @@ def run_reference(args, wl):
     value = statistics.median(vals)
     sample = f"each step: {desc}; numpy float64 oracle port of hyena.py:157-190, OpenBLAS on all host cores"
     return {
-        "impl": "reference", "metric": "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU",
+        "impl": "reference",
+        "metric": wl.get("metric", "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU"),
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "f32" else "f64",

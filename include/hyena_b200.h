@@ -31,6 +31,10 @@
  *   hy_causal_conv_bwd      core.py:245-268      causal_conv_input_grad + causal_conv_taps_grad
  *                           blockconv.py:223-264 two_stage_backward (transposed factors, two-pass dtaps)
  *                           cpsim.py:440-446     a2a_conv_backward's slab step (_slab_backward)
+ *   hy_mixer_bwd_prep       hyena.py:262-270     gate products of hyena_backward (u, dc) fused with
+ *                                                the recomputed featurizers
+ *   hy_featurizer_bwd       hyena.py:234-247     _feat_backward for q, k, v fused with the gate
+ *                           hyena.py:262-270     products of hyena_backward (one HBM pass)
  *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
  *                           core.py:255-268      the tap correlation it consumes
  */
@@ -157,6 +161,34 @@ HY_API size_t hy_causal_conv_bwd_workspace_size(int B, int C, int L, int lh, int
 HY_API int hy_causal_conv_bwd(const void* dy, const void* x, void* dx, void* dtaps, const void* taps,
                               int B, int C, int L, int lh, int group_size, int dtype,
                               void* ws, size_t ws_bytes, void* stream);
+/* Backward prologue of the mixer (hyena.py:262-270), one stream over the projections:
+ *   u = (Fk conv pk) * (Fv conv pv),   dc = dmixed * (Fq conv pq)      (B, C, L) each
+ * (the featurizers recomputed with the TMA-fed stream of hy_se_mixer_fwd). lhf <= 8, fp32 / bf16,
+ * L % 8 == 0, 16-byte aligned. dc_rev (nullable) also receives dc time-reversed per row, so the
+ * anti-causal inner conv runs as the causal tcgen05 kernel without a flip pass. */
+HY_API int hy_mixer_bwd_prep(const void* proj, const void* dmixed, const float* feat_taps, int lhf, int B, int C,
+                             int L, int dtype, void* u, void* dc, void* dc_rev, void* stream);
+/* Fused featurizer backward of the mixer (hyena.py:234-247 for q, k, v with the gate products
+ * of hyena.py:262-270), one pass: from the projections proj (B, 3C, L) = [q; k; v] rows, the
+ * gradient at the mixer output dmixed (B, C, L), the inner conv output conv_out (B, C, L) and
+ * du (B, C, L) (gradient at u = k * v):
+ *   dfq = dmixed * conv_out, dfk = du * (Fv conv pv), dfv = du * (Fk conv pk)
+ *   dproj[x][t] = sum_j Fx[j] dfx[t + j],   dfeat[x][c][j] = sum_{b,t} dfx[t] px[t - j]
+ * feat_taps / dfeat: fp32 (3, C, lhf), lhf <= 8; fp32 / bf16 activations, L % 8 == 0,
+ * 16-byte aligned; ws: hy_featurizer_bwd_workspace_size bytes (fp64 accumulators).
+ * du_reversed != 0: du rows are stored time-reversed (the output of the causal conv run on the
+ * reversed dc), read back mirrored in shared memory. */
+HY_API size_t hy_featurizer_bwd_workspace_size(int C, int lhf);
+HY_API int hy_featurizer_bwd(const void* proj, const void* dmixed, const void* conv_out, const void* du,
+                             const float* feat_taps, int lhf, int B, int C, int L, int dtype, void* dproj,
+                             float* dfeat, void* ws, size_t ws_bytes, int du_reversed, void* stream);
+/* Two-stage filter gradient, pass 2 (blockconv.py:253-262): from the chunk-summed outer
+ * products P0 = sum_n dC_n U_n^T, P1 = sum_n dC_n U_{n-1}^T (fp32, (C, lb, lb) each; pass 1 is
+ * a tensor-core batched GEMM over the chunked rows) scatter the block diagonals onto the taps:
+ * dtaps[g, j] = sum_{c in g} (sum_{i-i'=j} P0[c,i,i'] + sum_{lb+i-i'=j} P1[c,i,i']), j < lh <= 2 lb.
+ * ws: C * lh fp32. */
+HY_API int hy_toeplitz_taps_reduce(const float* P0, const float* P1, float* dtaps, float* ws, size_t ws_bytes,
+                                   int C, int lb, int lh, int group_size, void* stream);
 /* Hyena-LI filter-parameter gradients for h_t = sum_n R_n lam_n^t (npoles <= 8) straight from
  * dc (gradient at the conv output) and u (conv input), without the length-L tap gradient:
  *   d_res[g,n]  = sum_{b, c in g} sum_s dc[s] S_n[s],     S_n[s] = lam_n S_n[s-1] + u[s]

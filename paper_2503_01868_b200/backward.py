@@ -178,19 +178,30 @@ class DeviceGrads:
 
 
 def _batched_outer(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """sum_b a[b] @ b[b]^T in fp32 (fp64 for fp64 inputs) for (B, M, L) x (B, N, L)."""
-    acc = torch.float64 if a.dtype == torch.float64 else torch.float32
-    out = None
-    for i in range(a.shape[0]):
-        part = torch.matmul(a[i], b[i].transpose(0, 1)).to(acc)
-        out = part if out is None else out.add_(part)
+    """sum_b a[b] @ b[b]^T for (B, M, L) x (B, N, L): cuBLAS GEMMs accumulating in an fp32 output
+    (fp64 for fp64 inputs) across the batch (beta = 1), no separate conversion / add passes."""
+    if a.dtype == torch.float64:
+        out = torch.matmul(a[0], b[0].transpose(0, 1))
+        for i in range(1, a.shape[0]):
+            out.addmm_(a[i], b[i].transpose(0, 1))
+        return out
+    kw = {} if a.dtype == torch.float32 else {"out_dtype": torch.float32}
+    out = torch.mm(a[0], b[0].transpose(0, 1), **kw)
+    for i in range(1, a.shape[0]):
+        torch.addmm(out, a[i], b[i].transpose(0, 1), out=out, **kw)
     return out
 
 
-def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor | None = None):
+def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor | None = None, events=None):
     """(dx, DeviceGrads) for y = op.forward(x) and upstream gradient dy, both (B, D, L) CUDA
     tensors of the operator's dtype. Recomputes the mixer intermediates from the projections
-    (pass `proj` = op.w_qkv_t @ x to skip that GEMM). Same chain rule as hyena.py:250-284."""
+    (pass `proj` = op.w_qkv_t @ x to skip that GEMM). Same chain rule as hyena.py:250-284.
+    events: optional {"inner_taps": (start, end), "featurizer_bwd": (start, end)} CUDA events
+    recorded around those kernels (bench accounting)."""
+
+    def mark(name, i):
+        if events is not None and name in events:
+            events[name][i].record()
     squeeze = x.dim() == 2
     x3 = x.unsqueeze(0) if squeeze else x
     dy3 = dy.unsqueeze(0) if squeeze else dy
@@ -200,9 +211,6 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
     B, _, L = x3.shape
     if proj is None:
         proj = torch.matmul(op.w_qkv_t, x3)
-    feats = ops.causal_conv(proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
-    q, k, v = feats[:, :D], feats[:, D:2 * D], feats[:, 2 * D:]
-    u = k * v
     inner = op.cfg.inner
     implicit = isinstance(inner.filters[0], ImplicitFilter)
     npoles = {f.poles.size for f in inner.filters} if implicit else set()
@@ -211,31 +219,72 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
     if scan:
         res = torch.tensor(np.stack([f.residues for f in inner.filters]), dtype=torch.float32, device=x3.device)
         poles = torch.tensor(np.stack([f.poles for f in inner.filters]), dtype=torch.float32, device=x3.device)
-    if modal:
-        c = ops.li_conv(u, res, poles, op.gs)
-    elif op.lh > 129 or op.cfg.variant == "LI":
-        c = ops.long_conv(u, op.materialized_inner, op.gs)
-    else:
-        c = ops.gated_conv(u, op.materialized_inner, op.gs)
-    mixed = q * c
+    ts_ok = op.dtype == torch.bfloat16 and op.lh <= 129 and L % 8 == 0 and op.inner_taps is not None \
+        and not implicit
+
+    def inner_conv(a):
+        if modal:
+            return ops.li_conv(a, res, poles, op.gs)
+        if ts_ok:
+            return ops.two_stage(a, op.inner_taps, op.gs, decay=op.decay)
+        if op.lh > 129 or op.cfg.variant == "LI":
+            return ops.long_conv(a, op.materialized_inner, op.gs)
+        return ops.gated_conv(a, op.materialized_inner, op.gs)
+
     dmixed = torch.matmul(op.w_out_t.transpose(0, 1), dy3)
+    fused = op.dtype != torch.float64 and op.lhf <= 8 and L % 8 == 0
+    rev = fused and (modal or ts_ok)  # du runs as the causal tcgen05 conv of the reversed dc
+    dc_rev = None
+    if fused:
+        # featurizers recomputed in-stream: u = fk * fv and dc = dmixed * fq, one pass
+        if rev:
+            u, dc, dc_rev = ops.mixer_bwd_prep(proj, dmixed, op.feat_taps, reversed_dc=True)
+        else:
+            u, dc = ops.mixer_bwd_prep(proj, dmixed, op.feat_taps)
+        c = inner_conv(u)
+        mixed = op.mixer(proj) if (modal or ts_ok) else None  # fused tcgen05 forward mixer
+        if mixed is None:
+            mixed = ops.causal_conv(proj[:, :D].contiguous(), op.feat_taps[0], 1) * c
+    else:
+        feats = ops.causal_conv(proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
+        q, k, v = feats[:, :D], feats[:, D:2 * D], feats[:, 2 * D:]
+        u = k * v
+        c = inner_conv(u)
+        mixed = q * c
+        dc = dmixed * q
     g_out = _batched_outer(dy3, mixed)
-    dfeats = torch.empty_like(feats)
-    torch.mul(dmixed, c, out=dfeats[:, :D])                      # dq
-    dc = dmixed * q
     inner_g = {}
+    du_rev = None  # du stored time-reversed (consumed mirrored by the featurizer backward)
     if scan:
         # du[t] = sum_{s >= t} h[s - t] dc[s]: the causal conv of the time-reversed dc
-        rdc = torch.flip(dc, dims=[-1]).contiguous()
-        rdu = ops.li_conv(rdc, res, poles, op.gs) if modal else ops.long_conv(rdc, op.materialized_inner, op.gs)
-        du = torch.flip(rdu, dims=[-1])
+        if rev:
+            du_rev = inner_conv(dc_rev)
+        else:
+            rdc = torch.flip(dc, dims=[-1]).contiguous()
+            rdu = ops.li_conv(rdc, res, poles, op.gs) if modal else ops.long_conv(rdc, op.materialized_inner, op.gs)
+            du = torch.flip(rdu, dims=[-1])
+        mark("inner_taps", 0)
         inner_g["residues"], inner_g["poles"] = ops.li_param_grad(dc, u, res, poles, op.gs)
+        mark("inner_taps", 1)
     else:
         taps = op.materialized_inner
         if taps.shape[-1] > 2048:
             raise NotImplementedError(f"device backward: inner filter of {taps.shape[-1]} taps > 2048 "
                                       "(implicit filters use the per-mode scans for fp32 / bf16)")
-        du, dtaps = ops.causal_conv_bwd(dc, u, taps, op.gs)
+        if ts_ok:
+            # du = anti-causal conv of dc = the causal two-stage conv (tcgen05, transposed
+            # factors become the forward factors) of the time-reversed dc
+            rdc = dc_rev if rev else torch.flip(dc, dims=[-1]).contiguous()
+            rdu = ops.two_stage(rdc, op.inner_taps, op.gs, decay=op.decay)
+            if rev:
+                du_rev = rdu
+            else:
+                du = torch.flip(rdu, dims=[-1])
+            mark("inner_taps", 0)
+            _, dtaps = ops.causal_conv_bwd(dc, u, op.lh, op.gs, want_dx=False)
+            mark("inner_taps", 1)
+        else:
+            du, dtaps = ops.causal_conv_bwd(dc, u, taps, op.gs)
         if implicit:  # fp64: pull the tap gradient back through h_t = sum_n R_n lam_n^t
             r64 = torch.tensor(np.stack([f.residues for f in inner.filters]), device=dtaps.device)
             p64 = torch.tensor(np.stack([f.poles for f in inner.filters]), device=dtaps.device)
@@ -256,9 +305,20 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             inner_g["taps_hat"] = dtaps * torch.pow(base[:, None], -rate[:, None] * t[None, :])
         else:
             inner_g["taps"] = dtaps
-    torch.mul(du, v, out=dfeats[:, D:2 * D])                     # dk
-    torch.mul(du, k, out=dfeats[:, 2 * D:])                      # dv
-    dproj, dfeat = ops.causal_conv_bwd(dfeats, proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
+    if fused:
+        # one pass: featurizers recomputed, gate products, anti-causal FIRs, tap gradients
+        mark("featurizer_bwd", 0)
+        if du_rev is not None:
+            dproj, dfeat = ops.featurizer_bwd(proj, dmixed, c, du_rev, op.feat_taps, du_reversed=True)
+        else:
+            dproj, dfeat = ops.featurizer_bwd(proj, dmixed, c, du.contiguous(), op.feat_taps)
+        mark("featurizer_bwd", 1)
+    else:
+        dfeats = torch.empty_like(feats)
+        torch.mul(dmixed, c, out=dfeats[:, :D])                  # dq
+        torch.mul(du, v, out=dfeats[:, D:2 * D])                 # dk
+        torch.mul(du, k, out=dfeats[:, 2 * D:])                  # dv
+        dproj, dfeat = ops.causal_conv_bwd(dfeats, proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
     g_qkv = _batched_outer(dproj, x3)
     dx = torch.matmul(op.w_qkv_t.transpose(0, 1), dproj)
     grads = DeviceGrads(w_qkv_t=g_qkv, w_out_t=g_out, feat_taps=dfeat.reshape(3, D, op.lhf), inner=inner_g)

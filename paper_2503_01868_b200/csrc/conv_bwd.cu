@@ -34,11 +34,16 @@ static int bwd_nsplit(int B, int C, int L) {
   return ns;
 }
 
+// dtaps work items are (8 consecutive lags) x (one time segment of a tile); nseg segments
+// per tile so that the items fill the CTA (segments are multiples of 8 steps).
 __host__ __device__ inline int bwd_nseg(int lh) {
-  const int nq = (lh + 3) / 4;
-  int ns = kBT / nq;
-  return ns < 4 ? 4 : ns;
+  const int no = (lh + 7) / 8;
+  int ns = kBT / no;
+  if (ns < 1) ns = 1;
+  while (kBTT % (8 * ns) != 0) --ns;
+  return ns;
 }
+__host__ __device__ inline int bwd_lhp(int lh) { return (lh + 7) / 8 * 8; }
 
 // xs[i] = row(s0 + i), zeros outside [0, L); s0, n multiples of VEC when vec.
 template <typename T>
@@ -69,6 +74,24 @@ __device__ __forceinline__ void stage(typename Elem<T>::A* xs, const T* __restri
   }
 }
 
+// r[0..N) = p[0..N) from 16-byte aligned shared memory with 16-byte loads.
+template <int N>
+__device__ __forceinline__ void lds_vec(float (&r)[N], const float* p) {
+#pragma unroll
+  for (int e = 0; e < N; e += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(p + e);
+    r[e] = v.x, r[e + 1] = v.y, r[e + 2] = v.z, r[e + 3] = v.w;
+  }
+}
+template <int N>
+__device__ __forceinline__ void lds_vec(double (&r)[N], const double* p) {
+#pragma unroll
+  for (int e = 0; e < N; e += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(p + e);
+    r[e] = v.x, r[e + 1] = v.y;
+  }
+}
+
 template <typename T, bool DX, bool DT>
 __global__ void __launch_bounds__(kBT)
 causal_conv_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, T* __restrict__ dx,
@@ -78,14 +101,13 @@ causal_conv_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, T* __r
   constexpr int VEC = Elem<T>::VEC;
   constexpr int AL = 16 / sizeof(A) * 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nseg = bwd_nseg(lh);
-  const int wdy = bceil_to(kBTT + lh + kBV, VEC);
-  const int wx = bceil_to(kBTT + lh + 2 * VEC, VEC);
-  A* hs = reinterpret_cast<A*>(smem_raw);        // [lh]
-  A* dys = hs + bceil_to(lh, AL);                // dy window
-  A* xs = dys + bceil_to(wdy, AL);               // x window
-  A* ps = xs + bceil_to(wx, AL);                 // [nseg][lh] item partials
-  A* dts = ps + bceil_to(nseg * lh, AL);         // [lh] CTA lag sums
+  const int nseg = bwd_nseg(lh), lhp = bwd_lhp(lh);
+  const int wdy = kBTT + lhp + 16;
+  const int wx = kBTT + lhp + 16;
+  A* hs = reinterpret_cast<A*>(smem_raw);        // [lhp], zero padded
+  A* dys = hs + bceil_to(lhp, AL);               // dy window: dys[i] = dy[t0 + i]
+  A* xs = dys + bceil_to(wdy, AL);               // x window:  xs[i] = x[sx + i], sx = t0 - lhp - 8
+  A* ps = xs + bceil_to(wx, AL);                 // [nseg][lhp] item partials, accumulated over tiles
 
   const int split = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
   const size_t row = (static_cast<size_t>(b) * C + c) * L;
@@ -93,31 +115,33 @@ causal_conv_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, T* __r
   const int tps = (ntiles + nsplit - 1) / nsplit;
   const int tile0 = split * tps, tile1 = min(ntiles, tile0 + tps);
   if (DX)
-    for (int i = threadIdx.x; i < lh; i += blockDim.x) hs[i] = taps[static_cast<size_t>(c / gs) * lh + i];
+    for (int i = threadIdx.x; i < lhp; i += blockDim.x)
+      hs[i] = i < lh ? taps[static_cast<size_t>(c / gs) * lh + i] : A(0);
+  const int no = lhp / 8;
+  const int seg_len = kBTT / nseg;
   if (DT)
-    for (int i = threadIdx.x; i < lh; i += blockDim.x) dts[i] = A(0);
-  const int nq = (lh + 3) / 4;
-  const int seg_len = (kBTT + nseg - 1) / nseg;
+    for (int i = threadIdx.x; i < nseg * lhp; i += blockDim.x) ps[i] = A(0);
 
   for (int tile = tile0; tile < tile1; ++tile) {
     const int t0 = tile * kBTT;
+    const int sx = t0 - lhp - 8;  // multiple of 8: 16-byte aligned 4-wide reads below
     stage<T>(dys, dy + row, t0, wdy, L, vec != 0);
-    const int sx = bfloor_to(t0 - lh + 1, VEC);
-    if (DT) stage<T>(xs, x + row, sx, bceil_to(t0 + kBTT - sx, VEC), L, vec != 0);
+    if (DT) stage<T>(xs, x + row, sx, wx, L, vec != 0);
     __syncthreads();
     if (DX) {
+      // dx[t0 + tl + v] = sum_j h[j] dy[t0 + tl + v + j], 8 taps per block from 16 window values
       const int tl = threadIdx.x * kBV;
-      A acc[kBV], r[kBV];
+      A acc[kBV];
 #pragma unroll
-      for (int v = 0; v < kBV; ++v) acc[v] = A(0), r[v] = dys[tl + v];
-#pragma unroll 4
-      for (int j = 0; j < lh; ++j) {
-        const A h = hs[j];
+      for (int v = 0; v < kBV; ++v) acc[v] = A(0);
+      for (int j0 = 0; j0 < lhp; j0 += 8) {
+        A r[16], h[8];
+        lds_vec(r, dys + tl + j0);
+        lds_vec(h, hs + j0);
 #pragma unroll
-        for (int v = 0; v < kBV; ++v) acc[v] = fma(h, r[v], acc[v]);
+        for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-        for (int v = 0; v < kBV - 1; ++v) r[v] = r[v + 1];
-        r[kBV - 1] = dys[tl + kBV + j];
+          for (int v = 0; v < kBV; ++v) acc[v] = fma(h[jj], r[v + jj], acc[v]);
       }
       const int t = t0 + tl;
       T* drow = dx + row;
@@ -131,42 +155,38 @@ causal_conv_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, T* __r
       }
     }
     if (DT) {
-      // item w = (lag quad jq, segment s): sum_{t in seg} dy[t] * x[t - j], j = 4 jq + m
-      for (int w = threadIdx.x; w < nq * nseg; w += blockDim.x) {
-        const int jq = w % nq, s = w / nq;
-        const int j0 = 4 * jq;
-        const int ta = s * seg_len, tb = min(kBTT, ta + seg_len);
-        A a4[4] = {A(0), A(0), A(0), A(0)};
-        if (ta < tb) {
-          const int xo = t0 - sx;  // x[t0 + i - j] = xs[xo + i - j]
-          A r[4];
+      // item (lag octet o, segment s): a[m] += sum_{i in seg} dy[t0+i] x[t0+i-8o-m], m < 8,
+      // 8 steps at a time from the aligned x values [i - 8o - 8, i - 8o + 8)
+      for (int w = threadIdx.x; w < no * nseg; w += blockDim.x) {
+        const int o = w % no, s = w / no;
+        const int ta = s * seg_len;
+        A a[8];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) r[m] = xs[xo + ta - j0 - m];
-          for (int i = ta; i < tb; ++i) {
-            const A d = dys[i];
+        for (int m = 0; m < 8; ++m) a[m] = A(0);
+        const int xo = t0 - sx - 8 * o;  // x[t0 + i - 8o + e] = xs[xo + i + e]
+        for (int i = ta; i < ta + seg_len; i += 8) {
+          A d[8], xw[16];
+          lds_vec(d, dys + i);
+          lds_vec(xw, xs + xo + i - 8);  // x[t0+i-8o-8 .. +8)
 #pragma unroll
-            for (int m = 0; m < 4; ++m) a4[m] = fma(d, r[m], a4[m]);
+          for (int e = 0; e < 8; ++e)
 #pragma unroll
-            for (int m = 3; m > 0; --m) r[m] = r[m - 1];
-            r[0] = xs[xo + i + 1 - j0];
-          }
+            for (int m = 0; m < 8; ++m) a[m] = fma(d[e], xw[8 + e - m], a[m]);
         }
+        A* pp = ps + s * lhp + 8 * o;
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (j0 + m < lh) ps[s * lh + j0 + m] = a4[m];
-      }
-      __syncthreads();
-      for (int j = threadIdx.x; j < lh; j += blockDim.x) {
-        A sum = dts[j];
-        for (int s = 0; s < nseg; ++s) sum += ps[s * lh + j];
-        dts[j] = sum;
+        for (int m = 0; m < 8; ++m) pp[m] += a[m];
       }
     }
     __syncthreads();
   }
   if (DT) {
     A* out = part + ((static_cast<size_t>(b) * nsplit + split) * C + c) * lh;
-    for (int j = threadIdx.x; j < lh; j += blockDim.x) out[j] = dts[j];
+    for (int j = threadIdx.x; j < lh; j += blockDim.x) {
+      A sum = A(0);
+      for (int s2 = 0; s2 < nseg; ++s2) sum += ps[s2 * lhp + j];
+      out[j] = sum;
+    }
   }
 }
 
@@ -185,10 +205,9 @@ __global__ void conv_taps_reduce_kernel(const A* __restrict__ part, A* __restric
 
 static size_t bwd_smem_bytes(int lh, size_t asz) {
   const int al = static_cast<int>(16 / asz * 2);
-  const int vec = static_cast<int>(16 / (asz == 8 ? 8 : 2));  // widest VEC over the storage types
-  const int wdy = bceil_to(kBTT + lh + kBV, vec), wx = bceil_to(kBTT + lh + 2 * vec, vec);
-  return (static_cast<size_t>(bceil_to(lh, al)) + bceil_to(wdy, al) + bceil_to(wx, al) +
-          bceil_to(bwd_nseg(lh) * lh, al) + bceil_to(lh, al)) * asz;
+  const int lhp = bwd_lhp(lh);
+  const int w = kBTT + lhp + 16;
+  return (static_cast<size_t>(bceil_to(lhp, al)) + 2 * bceil_to(w, al) + bceil_to(bwd_nseg(lh) * lhp, al)) * asz;
 }
 
 template <typename T, bool DX, bool DT>
@@ -261,3 +280,39 @@ int hy_causal_conv_bwd(const void* dy, const void* x, void* dx, void* dtaps, con
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- two-stage filter gradient, pass 2
+// Pass 1 (tensor-core batched GEMMs over the chunked rows, ops.two_stage_taps_grad) leaves per
+// channel the chunk-summed outer products P0 = sum_n dC_n U_n^T and P1 = sum_n dC_n U_{n-1}^T
+// (lb x lb, fp32). Pass 2 scatters their block diagonals onto the taps (blockconv.py:253-262):
+//   dtaps[g][j] = sum_{c in g} ( sum_{i-i'=j} P0[c][i][i'] + sum_{lb+i-i'=j} P1[c][i][i'] ),  j < lh.
+namespace hy {
+__global__ void toeplitz_diag_kernel(const float* __restrict__ P0, const float* __restrict__ P1,
+                                     float* __restrict__ part, int lb, int lh) {
+  const int c = blockIdx.x;
+  const size_t base = static_cast<size_t>(c) * lb * lb;
+  for (int j = threadIdx.x; j < lh; j += blockDim.x) {
+    double s = 0.0;
+    if (j < lb)
+      for (int i = j; i < lb; ++i) s += P0[base + static_cast<size_t>(i) * lb + (i - j)];
+    const int d = j - lb;  // i - i' = d for P1 (d in (-lb, 0] .. )
+    for (int i = max(0, d); i < lb && i - d < lb; ++i) s += P1[base + static_cast<size_t>(i) * lb + (i - d)];
+    part[static_cast<size_t>(c) * lh + j] = static_cast<float>(s);
+  }
+}
+}  // namespace hy
+
+extern "C" int hy_toeplitz_taps_reduce(const float* P0, const float* P1, float* dtaps, float* ws, size_t ws_bytes,
+                                       int C, int lb, int lh, int gs, void* stream) {
+  if (!P0 || !P1 || !dtaps || !ws) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (C < 1 || lb < 1 || lh < 1 || gs < 1 || C % gs) return fail(HY_ERR_INVALID, "bad sizes");
+  if (lh > 2 * lb) return fail(HY_ERR_INELIGIBLE, "filter length %d needs more than one spill factor", lh);
+  if (ws_bytes < static_cast<size_t>(C) * lh * sizeof(float)) return fail(HY_ERR_INVALID, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  toeplitz_diag_kernel<<<C, 128, 0, st>>>(P0, P1, ws, lb, lh);
+  int s = check_launch("toeplitz_diag_kernel");
+  if (s != HY_OK) return s;
+  dim3 grid((lh + 127) / 128, C / gs);
+  conv_taps_reduce_kernel<float><<<grid, 128, 0, st>>>(ws, dtaps, 1, C, lh, gs);
+  return check_launch("conv_taps_reduce_kernel");
+}

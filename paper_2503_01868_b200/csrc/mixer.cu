@@ -346,18 +346,22 @@ __device__ __forceinline__ void hist_shfl(float (&hist)[8], const float (&x)[8],
   }
 }
 
-template <typename T, int NF, int NI>
+// PREP: the backward's mixer prologue instead of the mixer: u = fk * fv into y and
+// dc = gmix * fq into dc_out (gmix = gradient at the mixer output), from the same stream.
+template <typename T, int NF, int NI, bool PREP = false>
 __global__ void __launch_bounds__(kSsWarps * 32, 2)
 se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __restrict__ feat_taps, int lhf,
                  const float* __restrict__ inner_taps, const float* __restrict__ decay, int lh, int gs, int B,
-                 int C, int L) {
+                 int C, int L, const T* __restrict__ gmix = nullptr, T* __restrict__ dc_out = nullptr,
+                 T* __restrict__ dc_rev = nullptr) {
   using namespace sm100;
   constexpr int ROWB = kSsChunk * static_cast<int>(sizeof(T));  // bytes per row per stage
   constexpr int NHF = NF - 1, NHI = NI - 1;  // history samples each FIR needs
   extern __shared__ __align__(128) unsigned char ss_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* ring = reinterpret_cast<T*>(ss_smem + warp * (kSsStages * 3 * ROWB));  // [stage][k, v, q][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ss_smem + kSsWarps * kSsStages * 3 * ROWB) + warp * kSsStages;
+  constexpr int NR = PREP ? 4 : 3;  // staged rows: k, v, q (+ gmix)
+  T* ring = reinterpret_cast<T*>(ss_smem + warp * (kSsStages * NR * ROWB));  // [stage][k, v, q, g][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ss_smem + kSsWarps * kSsStages * NR * ROWB) + warp * kSsStages;
 
   const int nch = (L + kSsChunk - 1) / kSsChunk;
   const long long total = static_cast<long long>(B) * C * nch;  // < 2^31 (host check)
@@ -384,21 +388,24 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
   // lane 0's issue cursor: the q row of the next entry to issue, its chunk, channel, stage
   const size_t CL = static_cast<size_t>(C) * L;
   const T* iss_q = proj + (static_cast<size_t>(start.row / C) * 3 * C + start.row % C) * L;
+  const T* iss_g = PREP ? gmix + static_cast<size_t>(start.row) * L : nullptr;
   int iss_k = start.k, iss_c = start.row % C, iss_st = 0, n_iss = 0;
   auto issue = [&]() {  // lane 0: entry n_iss into stage n_iss % S
     int t0 = iss_k * kSsChunk, cnt = min(kSsChunk, L - t0), off = 0;
     if (warm && n_iss == 0) off = kSsChunk - 16, t0 += kSsChunk - 16, cnt = 16;  // the 16 steps before i0
-    T* dst = ring + iss_st * 3 * kSsChunk + off;
+    T* dst = ring + iss_st * NR * kSsChunk + off;
     const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(T));
     const T* src = iss_q + t0;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&bars[iss_st], 3 * bytes);
+    mbar_arrive_expect_tx(&bars[iss_st], NR * bytes);
     bulk_g2s(dst, src + CL, bytes, &bars[iss_st]);                  // k
     bulk_g2s(dst + kSsChunk, src + 2 * CL, bytes, &bars[iss_st]);  // v
     bulk_g2s(dst + 2 * kSsChunk, src, bytes, &bars[iss_st]);       // q
+    if (PREP) bulk_g2s(dst + 3 * kSsChunk, iss_g + t0, bytes, &bars[iss_st]);  // gmix
     if (++iss_k == nch) {
       iss_k = 0;
       iss_q += L;
+      if (PREP) iss_g += L;
       if (++iss_c == C) iss_c = 0, iss_q += 2 * CL;
     }
     if (++iss_st == kSsStages) iss_st = 0;
@@ -431,14 +438,14 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
       }
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
-        float h = j < lh ? __ldg(inner_taps + static_cast<size_t>(g) * lh + j) : 0.f;
+        float h = (!PREP && j < lh) ? __ldg(inner_taps + static_cast<size_t>(g) * lh + j) : 0.f;
         if (decay) h *= exp2f(-dr * static_cast<float>(j));
         hi[j] = h;
       }
     }
     mbar_wait(&bars[st], parity);
-    const T* cur = ring + st * 3 * kSsChunk;
-    const T* prv = ring + prv_st * 3 * kSsChunk;
+    const T* cur = ring + st * NR * kSsChunk;
+    const T* prv = ring + prv_st * NR * kSsChunk;
     const bool row_start = (k == 0);
     float rk[8], rv[8], rq[8], pk[8], pv[8], pq[8];
     lds8<T>(rk, cur + 8 * lane);
@@ -447,6 +454,8 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
     lds8<T>(pk, prv + kSsChunk - 8);  // the previous chunk's last 8 steps (broadcast)
     lds8<T>(pv, prv + 2 * kSsChunk - 8);
     lds8<T>(pq, prv + 3 * kSsChunk - 8);
+    float gq[8];
+    if (PREP) lds8<T>(gq, cur + 3 * kSsChunk + 8 * lane);
     __syncwarp();
     // the stage read before this one is free now: refill it S - 1 entries ahead
     if (lane == 0 && n_iss < n_issue) issue();
@@ -464,6 +473,37 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
     fir_pairs<NF>(fv, rv, hist, hv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) u[e] = fk[e] * fv[e];
+    if constexpr (PREP) {
+      hist_shfl<NHF>(hist, rq, pq, lane);
+      fir_pairs<NF>(fq, rq, hist, hq);
+      const int t = k * kSsChunk + 8 * lane;
+      if (!(warm && n == 0) && t < L) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = gq[e] * fq[e];
+        T* up = y + static_cast<size_t>(row) * L + t;
+        T* dp = dc_out + static_cast<size_t>(row) * L + t;
+        if constexpr (sizeof(T) == 4) {
+          st_stream16(up, pack16<T>(u)), st_stream16(up + 4, pack16<T>(u + 4));
+          st_stream16(dp, pack16<T>(o)), st_stream16(dp + 4, pack16<T>(o + 4));
+        } else {
+          st_stream16(up, pack16<T>(u));
+          st_stream16(dp, pack16<T>(o));
+        }
+        if (dc_rev) {  // dc time-reversed (the anti-causal conv runs as a causal one on it)
+          float r[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) r[e] = o[7 - e];
+          T* rp = dc_rev + static_cast<size_t>(row) * L + (L - 8 - t);
+          if constexpr (sizeof(T) == 4) {
+            st_stream16(rp, pack16<T>(r)), st_stream16(rp + 4, pack16<T>(r + 4));
+          } else {
+            st_stream16(rp, pack16<T>(r));
+          }
+        }
+      }
+      continue;
+    }
     // u history: lane l - 1's u; lane 0 the previous chunk's lane 31 (carried)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -526,11 +566,12 @@ static int launch_se(const void* proj, void* y, const float* ft, int lhf, const 
   return check_launch("se_mixer_kernel");
 }
 
-template <typename T, int NF, int NI>
+template <typename T, int NF, int NI, bool PREP = false>
 static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf, const float* it, const float* dec,
-                            int lh, int gs, int B, int C, int L, cudaStream_t st) {
-  auto kern = se_stream_kernel<T, NF, NI>;
-  constexpr int SMEM = kSsWarps * kSsStages * (3 * kSsChunk * static_cast<int>(sizeof(T)) + 8);
+                            int lh, int gs, int B, int C, int L, cudaStream_t st, const void* gmix = nullptr,
+                            void* dc_out = nullptr, void* dc_rev = nullptr) {
+  auto kern = se_stream_kernel<T, NF, NI, PREP>;
+  constexpr int SMEM = kSsWarps * kSsStages * ((PREP ? 4 : 3) * kSsChunk * static_cast<int>(sizeof(T)) + 8);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -547,7 +588,8 @@ static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf,
   const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   kern<<<static_cast<int>(grid), kSsWarps * 32, SMEM, st>>>(static_cast<const T*>(proj), static_cast<T*>(y), ft, lhf,
-                                                             it, dec, lh, gs, B, C, L);
+                                                             it, dec, lh, gs, B, C, L, static_cast<const T*>(gmix),
+                                                             static_cast<T*>(dc_out), static_cast<T*>(dc_rev));
   return check_launch("se_stream_kernel");
 }
 
@@ -605,4 +647,28 @@ extern "C" int hy_se_mixer_fwd(const void* proj, void* y, const void* feat_taps,
   if (dtype == HY_BF16)
     return launch_se_dispatch<__nv_bfloat16>(proj, y, ft, lhf, it, inner_decay, lh, gs, B, C, L, st);
   return fail(HY_ERR_UNSUPPORTED, "SE mixer: fp32 / bf16 only");
+}
+
+// Backward prologue of the mixer (hyena.py:262-270): u = (Fk conv pk) * (Fv conv pv) and
+// dc = dmixed * (Fq conv pq) from the projections in one stream (se_stream_kernel<PREP>).
+extern "C" int hy_mixer_bwd_prep(const void* proj, const void* dmixed, const float* feat_taps, int lhf, int B, int C,
+                                 int L, int dtype, void* u, void* dc, void* dc_rev, void* stream) {
+  if (!proj || !dmixed || !feat_taps || !u || !dc) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (B < 1 || C < 1 || L < 1 || lhf < 1) return fail(HY_ERR_INVALID, "sizes must be >= 1");
+  if (lhf > 8) return fail(HY_ERR_UNSUPPORTED, "mixer backward prologue: lhf %d > 8", lhf);
+  if (L % 8 != 0 || !aligned16(proj) || !aligned16(dmixed) || !aligned16(u) || !aligned16(dc) ||
+      (dc_rev && !aligned16(dc_rev)))
+    return fail(HY_ERR_UNSUPPORTED, "mixer backward prologue needs L %% 8 == 0 and 16-byte aligned rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HY_BF16)
+    return lhf == 7 ? launch_se_stream<__nv_bfloat16, 7, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C,
+                                                                 L, st, dmixed, dc, dc_rev)
+                    : launch_se_stream<__nv_bfloat16, 8, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C,
+                                                                 L, st, dmixed, dc, dc_rev);
+  if (dtype == HY_F32)
+    return lhf == 7 ? launch_se_stream<float, 7, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C, L, st,
+                                                         dmixed, dc, dc_rev)
+                    : launch_se_stream<float, 8, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C, L, st,
+                                                         dmixed, dc, dc_rev);
+  return fail(HY_ERR_UNSUPPORTED, "mixer backward prologue: fp32 / bf16 only");
 }

@@ -335,3 +335,46 @@ def li_param_grad(dc: torch.Tensor, u: torch.Tensor, residues: torch.Tensor, pol
                                     group_size, B, C, L, _dtype_code(dc3), d_res.data_ptr(), d_pole.data_ptr(),
                                     ws.data_ptr(), ws.numel(), _stream()), "li_param_grad")
     return d_res, d_pole
+
+
+def featurizer_bwd(proj: torch.Tensor, dmixed: torch.Tensor, conv_out: torch.Tensor, du: torch.Tensor,
+                   feat_taps: torch.Tensor, du_reversed: bool = False):
+    """Fused featurizer backward (hy_featurizer_bwd): (dproj (B, 3C, L), dfeat (3, C, lhf) fp32)
+    from the projections, the mixer-output gradient, the inner conv output and du (stored
+    time-reversed per row when du_reversed)."""
+    _check_device(proj, dmixed, conv_out, du)
+    B, C3, L = proj.shape
+    C = C3 // 3
+    for name, t in (("dmixed", dmixed), ("conv_out", conv_out), ("du", du)):
+        if tuple(t.shape) != (B, C, L) or t.dtype != proj.dtype:
+            raise ValueError(f"{name} must be ({B}, {C}, {L}) {proj.dtype}, got {tuple(t.shape)} {t.dtype}")
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    lhf = ft.shape[-1]
+    lib = _lib.load()
+    dproj = torch.empty_like(proj)
+    dfeat = torch.empty((3, C, lhf), dtype=torch.float32, device=proj.device)
+    ws = torch.empty(int(lib.hy_featurizer_bwd_workspace_size(C, lhf)), dtype=torch.uint8, device=proj.device)
+    _lib.check(lib.hy_featurizer_bwd(proj.data_ptr(), dmixed.data_ptr(), conv_out.data_ptr(), du.data_ptr(),
+                                     ft.data_ptr(), lhf, B, C, L, _dtype_code(proj), dproj.data_ptr(),
+                                     dfeat.data_ptr(), ws.data_ptr(), ws.numel(), int(du_reversed), _stream()),
+               "featurizer_bwd")
+    return dproj, dfeat
+
+
+def mixer_bwd_prep(proj: torch.Tensor, dmixed: torch.Tensor, feat_taps: torch.Tensor, reversed_dc: bool = False):
+    """(u, dc[, dc_rev]) = ((Fk conv pk) * (Fv conv pv), dmixed * (Fq conv pq)[, dc time-reversed])
+    in one stream (hy_mixer_bwd_prep)."""
+    _check_device(proj, dmixed)
+    B, C3, L = proj.shape
+    C = C3 // 3
+    if tuple(dmixed.shape) != (B, C, L) or dmixed.dtype != proj.dtype:
+        raise ValueError("dmixed must be (B, C, L) of the projections' dtype")
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    u = torch.empty_like(dmixed)
+    dc = torch.empty_like(dmixed)
+    dc_rev = torch.empty_like(dmixed) if reversed_dc else None
+    lib = _lib.load()
+    _lib.check(lib.hy_mixer_bwd_prep(proj.data_ptr(), dmixed.data_ptr(), ft.data_ptr(), ft.shape[-1], B, C, L,
+                                     _dtype_code(proj), u.data_ptr(), dc.data_ptr(), _ptr(dc_rev), _stream()),
+               "mixer_bwd_prep")
+    return (u, dc, dc_rev) if reversed_dc else (u, dc)

@@ -100,3 +100,58 @@ def test_li_param_grad_vs_oracle(dtype, B, C, L, npoles, gs, near_one):
     tol = TOL[dtype] if not near_one else 5 * TOL[dtype]
     assert oracle.rel_err(d_res.double().cpu().numpy(), want_res) < tol
     assert oracle.rel_err(d_pole.double().cpu().numpy(), want_pole) < tol
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("B,C,L,lhf", [(2, 4, 4096, 7), (1, 3, 1000, 8), (3, 2, 248, 7), (1, 5, 256, 3),
+                                       (2, 2, 8, 7), (2, 64, 2056, 7), (1, 1, 504, 1)])
+def test_featurizer_bwd_vs_oracle(dtype, B, C, L, lhf):
+    """hy_featurizer_bwd = _feat_backward for q, k, v (hyena.py:234-247) with the gate products
+    dq = g * c, dk = du * fv, dv = du * fk (hyena.py:262-270)."""
+    rng = np.random.default_rng(L * 7 + lhf + C)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: np.asarray(a, dtype=np.float32).astype(np.float64))
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    g, cc, du = (rnd(rng.standard_normal((B, C, L))) for _ in range(3))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    dproj, dfeat = ops.featurizer_bwd(dev(proj, TDT[dtype]), dev(g, TDT[dtype]), dev(cc, TDT[dtype]),
+                                      dev(du, TDT[dtype]), dev(feat, torch.float32))
+    want_dp = np.empty_like(proj)
+    want_df = np.zeros((3, C, lhf))
+    for b in range(B):
+        pq, pk, pv = (proj[b, i * C:(i + 1) * C] for i in range(3))
+        fk = oracle.direct_causal_conv(pk, oracle.explicit_bank(C, 1, feat[1]))
+        fv = oracle.direct_causal_conv(pv, oracle.explicit_bank(C, 1, feat[2]))
+        for i, (dfx, px) in enumerate(((g[b] * cc[b], pq), (du[b] * fv, pk), (du[b] * fk, pv))):
+            want_dp[b, i * C:(i + 1) * C] = ob.causal_conv_input_grad(dfx, feat[i])
+            want_df[i] += ob.causal_conv_taps_grad(dfx, px, oracle.explicit_bank(C, 1, feat[i]))
+    tol = TOL[dtype]
+    assert oracle.rel_err(dproj.double().cpu().numpy(), want_dp) < tol
+    assert oracle.rel_err(dfeat.double().cpu().numpy(), want_df) < (1e-4 if dtype == "f32" else tol)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_mixer_bwd_prep_and_reversed_du(dtype):
+    """hy_mixer_bwd_prep (u = fk*fv, dc = g*fq, dc reversed) and hy_featurizer_bwd reading du
+    time-reversed equal the natural-order results."""
+    B, C, L, lhf = 2, 6, 2056, 7
+    rng = np.random.default_rng(11)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: np.asarray(a, dtype=np.float32).astype(np.float64))
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    g, cc, du = (rnd(rng.standard_normal((B, C, L))) for _ in range(3))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    t = TDT[dtype]
+    u, dc, dcr = ops.mixer_bwd_prep(dev(proj, t), dev(g, t), dev(feat, torch.float32), reversed_dc=True)
+    want_u = np.empty((B, C, L))
+    want_dc = np.empty((B, C, L))
+    for b in range(B):
+        fq, fk, fv = (oracle.direct_causal_conv(proj[b, i * C:(i + 1) * C], oracle.explicit_bank(C, 1, feat[i]))
+                      for i in range(3))
+        want_u[b], want_dc[b] = fk * fv, g[b] * fq
+    assert oracle.rel_err(u.double().cpu().numpy(), want_u) < TOL[dtype]
+    assert oracle.rel_err(dc.double().cpu().numpy(), want_dc) < TOL[dtype]
+    assert torch.equal(torch.flip(dc, dims=[-1]), dcr)
+    a = ops.featurizer_bwd(dev(proj, t), dev(g, t), dev(cc, t), dev(du, t), dev(feat, torch.float32))
+    r = ops.featurizer_bwd(dev(proj, t), dev(g, t), dev(cc, t), torch.flip(dev(du, t), dims=[-1]).contiguous(),
+                           dev(feat, torch.float32), du_reversed=True)
+    assert torch.equal(a[0], r[0])
+    assert torch.allclose(a[1], r[1], rtol=1e-6, atol=1e-6)
