@@ -228,9 +228,9 @@ class Runner:
             self.fwd = train
             n = B * D * L
             self.kernels = [
-                dict(label="inner_taps", kernel="causal_conv_bwd_kernel<DT> (hy_causal_conv_bwd: MR tap "
-                     "gradient, lag correlation of dc and u over 128 lags)", bound="fp32",
-                     work=2 * wl["inner_len"] * n, unit="TFLOP/s"),
+                dict(label="inner_taps", kernel="taps_grad_kernel (hy_two_stage_taps_grad: tcgen05 chunk outer "
+                     "products P0/P1 in TMEM + diagonal scatter; dc and u read once)", bound="hbm",
+                     work=2 * self.esize * n, unit="GB/s"),
                 dict(label="featurizer_bwd", kernel="feat_bwd_kernel (hy_featurizer_bwd: featurizers recomputed, "
                      "gate products, anti-causal FIRs, tap gradients; 6 rows in, 3 out)", bound="hbm",
                      work=9 * self.esize * n, unit="GB/s")]

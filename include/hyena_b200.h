@@ -35,6 +35,7 @@
  *                                                the recomputed featurizers
  *   hy_featurizer_bwd       hyena.py:234-247     _feat_backward for q, k, v fused with the gate
  *                           hyena.py:262-270     products of hyena_backward (one HBM pass)
+ *   hy_two_stage_taps_grad  blockconv.py:246-262 two_stage_backward's two-pass filter gradient (tcgen05)
  *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
  *                           core.py:255-268      the tap correlation it consumes
  */
@@ -182,6 +183,15 @@ HY_API size_t hy_featurizer_bwd_workspace_size(int C, int lhf);
 HY_API int hy_featurizer_bwd(const void* proj, const void* dmixed, const void* conv_out, const void* du,
                              const float* feat_taps, int lhf, int B, int C, int L, int dtype, void* dproj,
                              float* dfeat, void* ws, size_t ws_bytes, int du_reversed, void* stream);
+/* Two-stage filter gradient on tcgen05 (bf16, lh <= 129): both passes of blockconv.py:246-262
+ * in one kernel — per channel the chunk outer products P0 = sum_n dC_n U_n^T and
+ * P1 = sum_n dC_n U_{n-1}^T accumulate in TMEM (M = N = 128, K = chunks, summed over the
+ * batch), then their block diagonals are scattered onto the taps in the epilogue:
+ *   dtaps[g, j] = sum_{c in g} sum_{b,t} dc[b,c,t] * u[b,c,t-j]   (fp32 (G, lh))
+ * dc, u: (B, C, L) bf16, L % 8 == 0. ws: hy_two_stage_taps_grad_workspace_size bytes. */
+HY_API size_t hy_two_stage_taps_grad_workspace_size(int C, int lh);
+HY_API int hy_two_stage_taps_grad(const void* dc, const void* u, float* dtaps, int B, int C, int L, int lh,
+                                  int group_size, int dtype, void* ws, size_t ws_bytes, void* stream);
 /* Two-stage filter gradient, pass 2 (blockconv.py:253-262): from the chunk-summed outer
  * products P0 = sum_n dC_n U_n^T, P1 = sum_n dC_n U_{n-1}^T (fp32, (C, lb, lb) each; pass 1 is
  * a tensor-core batched GEMM over the chunked rows) scatter the block diagonals onto the taps:

@@ -45,6 +45,8 @@ SIGNATURES = {
     "hy_mixer_bwd_prep": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
     "hy_featurizer_bwd_workspace_size": (_SZ, [_I, _I]),
     "hy_featurizer_bwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _SZ, _I, _P]),
+    "hy_two_stage_taps_grad_workspace_size": (_SZ, [_I, _I]),
+    "hy_two_stage_taps_grad": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
     "hy_toeplitz_taps_reduce": (_I, [_P, _P, _P, _P, _SZ, _I, _I, _I, _I, _P]),
     "hy_li_param_grad_workspace_size": (_SZ, [_I, _I]),
     "hy_li_param_grad": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _SZ, _P]),

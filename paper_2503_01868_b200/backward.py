@@ -281,7 +281,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             else:
                 du = torch.flip(rdu, dims=[-1])
             mark("inner_taps", 0)
-            _, dtaps = ops.causal_conv_bwd(dc, u, op.lh, op.gs, want_dx=False)
+            dtaps = ops.two_stage_taps_grad(dc, u, op.lh, op.gs)  # tcgen05, both passes fused
             mark("inner_taps", 1)
         else:
             du, dtaps = ops.causal_conv_bwd(dc, u, taps, op.gs)

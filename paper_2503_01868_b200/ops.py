@@ -378,3 +378,21 @@ def mixer_bwd_prep(proj: torch.Tensor, dmixed: torch.Tensor, feat_taps: torch.Te
                                      _dtype_code(proj), u.data_ptr(), dc.data_ptr(), _ptr(dc_rev), _stream()),
                "mixer_bwd_prep")
     return (u, dc, dc_rev) if reversed_dc else (u, dc)
+
+
+def two_stage_taps_grad(dc: torch.Tensor, u: torch.Tensor, lh: int, group_size: int = 1) -> torch.Tensor:
+    """dtaps (G, lh) fp32 = sum_{c in g, b, t} dc[t] u[t-j] on tcgen05 (hy_two_stage_taps_grad;
+    the two-pass filter gradient of blockconv.py:246-262), bf16 dc / u, lh <= 129."""
+    dc3, u3 = _as3(dc), _as3(u)
+    _check_device(dc3, u3)
+    if dc3.shape != u3.shape or dc3.dtype != torch.bfloat16 or u3.dtype != torch.bfloat16:
+        raise ValueError("dc and u must be matching bfloat16 (B, C, L) tensors")
+    B, C, L = dc3.shape
+    if C % group_size:
+        raise ValueError(f"group_size {group_size} does not divide channel count {C}")
+    lib = _lib.load()
+    out = torch.empty((C // group_size, lh), dtype=torch.float32, device=dc3.device)
+    ws = torch.empty(int(lib.hy_two_stage_taps_grad_workspace_size(C, lh)), dtype=torch.uint8, device=dc3.device)
+    _lib.check(lib.hy_two_stage_taps_grad(dc3.data_ptr(), u3.data_ptr(), out.data_ptr(), B, C, L, lh, group_size,
+                                          _lib.HY_BF16, ws.data_ptr(), ws.numel(), _stream()), "two_stage_taps_grad")
+    return out

@@ -56,6 +56,10 @@ def main():
         esz = x.element_size()
         out = {"workload": key, "B": B, "L": L, "dtype": str(dt), "fwd_ms": round(fwd, 3), "bwd_ms": round(bwd, 3)}
         u = torch.randn((B, D, L), device="cuda", dtype=dt, generator=g)
+        if variant == "MR" and dt == torch.bfloat16:
+            ms = timeit(lambda: ops.two_stage_taps_grad(dy, u, 128, 1))
+            out["taps_grad_tcgen05_ms"] = round(ms, 3)
+            out["taps_grad_tcgen05_GBps"] = round(2 * B * D * L * esz / ms / 1e6, 1)
         if variant != "LI":
             taps = op.materialized_inner
             ms = timeit(lambda: ops.causal_conv_bwd(dy, u, taps, 1))

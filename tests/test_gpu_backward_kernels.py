@@ -155,3 +155,17 @@ def test_mixer_bwd_prep_and_reversed_du(dtype):
                            dev(feat, torch.float32), du_reversed=True)
     assert torch.equal(a[0], r[0])
     assert torch.allclose(a[1], r[1], rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("B,C,L,lh,gs", [(1, 4, 8192, 128, 1), (2, 3, 8192, 129, 3), (1, 2, 1000, 128, 1),
+                                         (3, 4, 16384 + 136, 100, 2), (1, 300, 256, 7, 1), (2, 2, 128, 128, 1)])
+def test_two_stage_taps_grad_tcgen05_vs_oracle(B, C, L, lh, gs):
+    """hy_two_stage_taps_grad (tcgen05 chunk outer products + diagonal scatter) equals the
+    reference's two-pass filter gradient (blockconv.py:246-262) = causal_conv_taps_grad."""
+    rng = np.random.default_rng(L + lh + C)
+    dc = bf16_round(rng.standard_normal((B, C, L)))
+    u = bf16_round(rng.standard_normal((B, C, L)))
+    got = ops.two_stage_taps_grad(dev(dc, torch.bfloat16), dev(u, torch.bfloat16), lh, gs)
+    bank = oracle.explicit_bank(C, gs, np.zeros((C // gs, lh)))
+    want = sum(ob.causal_conv_taps_grad(dc[b], u[b], bank) for b in range(B))
+    assert oracle.rel_err(got.double().cpu().numpy(), want) < 1e-5
