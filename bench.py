@@ -135,6 +135,12 @@ def operator_roofline(op_tf: float, peaks: dict, dtype: str, flops: int) -> dict
     """Whole operator step against the peak of the pipe its GEMMs run on: bf16 -> tensor cores
     (MEASURED_PEAKS.json); fp32 -> CUDA-core FFMA (TF32 off for the 1e-5 parity bar), peak
     derived as SMs x 128 lanes x 2 FLOP x max SM clock (not in MEASURED_PEAKS.json)."""
+    if dtype == "f32" and os.environ.get("HY_FP32_GEMM", "split3") == "split3":
+        # fp32 GEMMs as six bf16 tensor-core GEMMs on three-way bf16 splits (blas.py)
+        peak = peaks["bf16_tflops"] / 6
+        return {"bound": "tensor (fp32 = 6 bf16 GEMMs on 3-way splits)", "achieved": op_tf, "peak": peak,
+                "unit": "TFLOP/s (fp32-equivalent)", "frac": op_tf / peak, "flops_per_step_per_rank": flops,
+                "peak_source": "measured bf16 peak / 6"}
     if dtype == "f32":
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         return {"bound": "fp32 cuda-core", "achieved": op_tf, "peak": peak, "unit": "TFLOP/s",

@@ -210,7 +210,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         raise ValueError("x and dy must be (B, D, L) tensors of the operator's dtype")
     B, _, L = x3.shape
     if proj is None:
-        proj = torch.matmul(op.w_qkv_t, x3)
+        proj = op.project(x3)
     inner = op.cfg.inner
     implicit = isinstance(inner.filters[0], ImplicitFilter)
     npoles = {f.poles.size for f in inner.filters} if implicit else set()

@@ -389,9 +389,9 @@ class HyenaCP:
         if self._fused() and m >= _lib.MIXER_HISTORY:
             # the successor needs only the projections of the last 144 steps: compute those
             # first and start the send, so the transfer overlaps the full projection GEMM
-            tail = torch.matmul(op.w_qkv_t, x3[..., m - _lib.MIXER_HISTORY:])
+            tail = op.project(x3[..., m - _lib.MIXER_HISTORY:].contiguous())
             hist, reqs = _exchange_halo(tail, _lib.MIXER_HISTORY, grp, "cp_hist")
-            proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
+            proj = op.project(x3)  # (B, 3D, m): token-local
             for q in reqs:
                 q.wait()
             if events is not None:
@@ -401,7 +401,7 @@ class HyenaCP:
             if events is not None:
                 events[1].record()
         else:
-            proj = torch.matmul(op.w_qkv_t, x3)  # (B, 3D, m): token-local
+            proj = op.project(x3)  # (B, 3D, m): token-local
             # featurizers over the 3D projected rows with their (lhf-1)-step halo
             ft = op.feat_taps.reshape(3 * D, op.lhf)
             if getattr(self, "_feat_groups", None) is None:
@@ -426,7 +426,7 @@ class HyenaCP:
                                            conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
                                            correct=lambda h, y: _correct(h, y, taps, op.gs))
             mixed = q * conv
-        y = torch.matmul(op.w_out_t, mixed)
+        y = op.out_project(mixed)
         return y[0] if x_local.dim() == 2 else y
 
     __call__ = forward

@@ -12,7 +12,7 @@
 // its causal history straight from shared memory), and lane 31's steps are only the
 // anti-causal future of lane 30 (they are recomputed as lane 0 of the next chunk). So chunks
 // are independent: no carried state, no warm-up. Chunks stream in by 1-D bulk copies (TMA)
-// issued by one lane into a 3-stage per-warp ring with an mbarrier per stage. Tap gradients
+// issued by one lane into a 6-stage per-warp ring with an mbarrier per stage. Tap gradients
 // accumulate in registers per lane and leave by a warp reduction and fp64 atomics when the
 // warp moves to another channel.
 #include "common.cuh"
@@ -20,7 +20,7 @@
 
 namespace hy {
 
-constexpr int kFbStages = 3;
+constexpr int kFbStages = 6;
 constexpr int kFbStep = 248;   // output steps per chunk
 constexpr int kFbRaw = 264;    // staged raw steps per chunk: 8 history + 256
 constexpr int kFbGrad = 256;   // staged g / c / du steps per chunk

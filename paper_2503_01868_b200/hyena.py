@@ -15,6 +15,7 @@ packed once on the device); `hyena_forward` stages a SeqTensor through it.
 
 from __future__ import annotations
 
+import os
 import weakref
 from dataclasses import dataclass
 from typing import Union
@@ -22,7 +23,7 @@ from typing import Union
 import numpy as np
 import torch
 
-from . import ops
+from . import blas, ops
 from .blockconv import spill_count
 from .core import (
     ExplicitFilter,
@@ -151,6 +152,12 @@ class HyenaOperator:
         w = [projection_dense(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v")]
         self.w_qkv_t = torch.from_numpy(np.concatenate([m.T for m in w], axis=0)).to(self.dev, dtype).contiguous()
         self.w_out_t = torch.from_numpy(np.ascontiguousarray(projection_dense(cfg.w_out).T)).to(self.dev, dtype)
+        # fp32 projections on the tensor cores (blas.py: three-way bf16 split, six bf16 GEMMs);
+        # HY_FP32_GEMM=simt keeps cuBLAS's CUDA-core fp32 GEMM
+        self.split3 = dtype == torch.float32 and os.environ.get("HY_FP32_GEMM", "split3") == "split3"
+        if self.split3:
+            self.w_qkv_parts = blas.split3(self.w_qkv_t)
+            self.w_out_parts = blas.split3(self.w_out_t.contiguous())
         tdt = ops.tap_dtype(dtype)
         self.lhf = max(cfg.q_feat.filter_len, cfg.k_feat.filter_len, cfg.v_feat.filter_len)
         feat = np.zeros((3, D, self.lhf))
@@ -222,14 +229,26 @@ class HyenaOperator:
                 f"LI inner filter length {self.lh} must equal the sequence length {x3.shape[2]}")
         if x3.dtype != self.dtype:
             raise ValueError(f"operator packed for {self.dtype}, got {x3.dtype}")
-        proj = torch.matmul(self.w_qkv_t, x3)
+        proj = self.project(x3)
         if events is not None:
             events[0].record()
         mixed = self.mixer(proj)
         if events is not None:
             events[1].record()
-        y = torch.matmul(self.w_out_t, mixed)
+        y = self.out_project(mixed)
         return y[0] if squeeze else y
+
+    def project(self, x3: torch.Tensor) -> torch.Tensor:
+        """(B, 3D, L) = W_qkv^T x (hyena.py:122-124)."""
+        if self.split3:
+            return blas.matmul_split3(self.w_qkv_parts, blas.split3(x3))
+        return torch.matmul(self.w_qkv_t, x3)
+
+    def out_project(self, mixed: torch.Tensor) -> torch.Tensor:
+        """y = W_out^T mixed (hyena.py:188)."""
+        if self.split3:
+            return blas.matmul_split3(self.w_out_parts, blas.split3(mixed))
+        return torch.matmul(self.w_out_t, mixed)
 
     __call__ = forward
 
@@ -296,14 +315,14 @@ def hyena_forward_saved(x: SeqTensor, cfg: HyenaConfig):
     xd = to_device(x)
     op = operator_for(cfg, xd.dtype)
     D = cfg.width
-    proj = torch.matmul(op.w_qkv_t, xd)
+    proj = op.project(xd.unsqueeze(0))[0] if op.split3 else torch.matmul(op.w_qkv_t, xd)
     feats = ops.causal_conv(proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
     q, k, v = (feats[i * D:(i + 1) * D].contiguous() for i in range(3))
     gated = k * v
     conv_out = ops.long_conv(gated, op.materialized_inner, op.gs) if op.lh > 129 else \
         ops.gated_conv(gated, op.materialized_inner, op.gs)
     mixed = q * conv_out
-    y = torch.matmul(op.w_out_t, mixed)
+    y = op.out_project(mixed.unsqueeze(0))[0] if op.split3 else torch.matmul(op.w_out_t, mixed)
     h = lambda t: t.detach().cpu().numpy().astype(np.float64)  # noqa: E731
     saved = HyenaSaved(cfg, h(xd), h(proj[:D]), h(proj[D:2 * D]), h(proj[2 * D:]), h(q), h(k), h(v), h(gated),
                        h(conv_out), h(mixed), None, x.dtype)

@@ -151,3 +151,21 @@ def test_host_pipeline_matches_forward():
     torch.cuda.synchronize()
     for x, y in zip(xs, ys):
         assert torch.equal(y, op.forward(x.cuda()).cpu())
+
+
+def test_se_operator_fp32_full_width_parity():
+    """Config C1's width (D = 4096, the GEMM reduction length that sets the fp32 error) on a
+    short sequence: the fp32 operator (split-bf16 tensor-core projections, SE stream mixer)
+    against the oracle within the north-star fp32 bar 1e-5."""
+    D, L = 4096, 256
+    cfg = hy.make_hyena_config("SE", D, hy.make_rng(0), block_size=16)
+    x = hy.make_rng(1).standard_normal((D, L)).astype(np.float32)
+    y = hy.hyena_forward(hy.SeqTensor(x, "f32"), cfg).data
+    ocfg = {"variant": "SE", "width": D, "block_size": 16, "backend": "blocked",
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        g = getattr(cfg, n)
+        ocfg[n] = {"channels": g.channels, "group_size": g.group_size,
+                   "filters": [("explicit", f.taps) for f in g.filters]}
+    want = oracle.hyena_forward(x, ocfg)
+    assert oracle.rel_err(y, want) < 1e-5
