@@ -82,3 +82,56 @@ def test_hyena_cp_matches_single_gpu(variant):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert err < 2e-2, err
+
+
+def _a2a_bwd_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from oracle import backward as ob
+        D, L, lh = 16, 4096, 9
+        rng = np.random.default_rng(5)
+        taps = rng.standard_normal((D // 2, lh)) / 3
+        groups = hy.GroupSpec(D, 2, tuple(hy.ExplicitFilter(t) for t in taps))
+        x = rng.standard_normal((D, L))
+        dy = rng.standard_normal((D, L))
+        grp = hy.cp.CPGroup()
+        res = {}
+        for layout in ("sequential", "zigzag"):
+            xs = hy.cp.shard(hy.SeqTensor(x), world, layout)
+            dys = hy.cp.shard(hy.SeqTensor(dy), world, layout)
+            _, saved = hy.cp.a2a_conv_saved(torch.from_numpy(xs.shards[rank].copy()).cuda(), groups, grp, layout)
+            dx = hy.cp.a2a_conv_backward(saved, torch.from_numpy(dys.shards[rank].copy()).cuda(), grp)
+            parts = [torch.empty_like(dx) for _ in range(world)]
+            dist.all_gather(parts, dx)
+            if rank == 0:
+                got = hy.cp.gather(hy.cp.ShardedSeq([p.cpu().numpy() for p in parts], layout)).data
+                want = ob.causal_conv_input_grad(dy, np.repeat(taps, 2, axis=0))
+                res[layout] = float(np.abs(got - want).max() / max(1.0, np.abs(want).max()))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_a2a_backward_nccl_matches_oracle():
+    """a2a_conv_backward (cpsim.py:440-446) over NCCL, fp64 slab adjoint on the device, both
+    layouts, against the oracle's unsharded input adjoint (core.py:245-252)."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_bwd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for layout, err in res.items():
+        assert err < 1e-12, (layout, err)
