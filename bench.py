@@ -257,8 +257,10 @@ class Runner:
             mod = cp.HyenaCP(build_config(wl), dt)
             self.m = L // ws
             self.fwd = lambda x, ev=None: mod.forward(x, events=None if ev is None else ev[0])
-            # the slab long conv (ungated li_conv): D/ws channels x L tokens, in + out
-            self.kernels = [("LI slab conv", "LI", 2 * self.esize * (D // ws) * B * L)]
+            # the slab long conv (ungated li_conv): D/ws channels x L tokens, in + out; one rank
+            # runs the fused single-GPU operator (li_mixer: 3 projected rows in, 1 out)
+            self.kernels = [("LI slab conv", "LI", 2 * self.esize * (D // ws) * B * L)] if ws > 1 else \
+                [("LI mixer (one rank: fused operator)", "LI", 4 * self.esize * D * B * L)]
             self.parallelism = f"cp{ws} (sequence sharded, all-to-all to channel slabs for the long conv)"
             self.l_global = L
         self.B, self.D, self.dt = B, D, dt
@@ -351,7 +353,7 @@ def run_ours(args, wl):
             continue
         label, variant, nbytes = kd
         ach = nbytes / (ms * 1e-3) / 1e9
-        kinfo.append({"kernel": MIXER_KERNEL[variant] if wl["kind"] != "cp" else
+        kinfo.append({"kernel": MIXER_KERNEL[variant] if (wl["kind"] != "cp" or ws == 1) else
                       "two_stage_kernel<IMPL> (hy_li_conv_fwd: implicit long conv of the rank's channel slab)",
                       "label": label, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                       "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": nbytes, "launch_ms": ms})

@@ -31,6 +31,8 @@
  *   hy_causal_conv_bwd      core.py:245-268      causal_conv_input_grad + causal_conv_taps_grad
  *                           blockconv.py:223-264 two_stage_backward (transposed factors, two-pass dtaps)
  *                           cpsim.py:440-446     a2a_conv_backward's slab step (_slab_backward)
+ *   hy_featurize_fwd        hyena.py:122-126,184 _featurize(q, k, v) + gated = k * v (CP LI layer;
+ *                           cpsim.py:498-510     the featurizer halo as an explicit history)
  *   hy_mixer_bwd_prep       hyena.py:262-270     gate products of hyena_backward (u, dc) fused with
  *                                                the recomputed featurizers
  *   hy_featurizer_bwd       hyena.py:234-247     _feat_backward for q, k, v fused with the gate
@@ -162,6 +164,12 @@ HY_API size_t hy_causal_conv_bwd_workspace_size(int B, int C, int L, int lh, int
 HY_API int hy_causal_conv_bwd(const void* dy, const void* x, void* dx, void* dtaps, const void* taps,
                               int B, int C, int L, int lh, int group_size, int dtype,
                               void* ws, size_t ws_bytes, void* stream);
+/* Featurizers + k * v gate in one stream (forward; the context-parallel LI layer):
+ *   u = (Fk conv pk) * (Fv conv pv),  fq = Fq conv pq               (B, C, L) each
+ * rhist (nullable): (B, 3C, 8) raw projections of the 8 steps before t = 0 ([q; k; v] rows, the
+ * predecessor rank's), the featurizers' history instead of zeros. lhf <= 8, fp32 / bf16. */
+HY_API int hy_featurize_fwd(const void* proj, const void* rhist, const float* feat_taps, int lhf, int B, int C,
+                            int L, int dtype, void* u, void* fq, void* stream);
 /* Backward prologue of the mixer (hyena.py:262-270), one stream over the projections:
  *   u = (Fk conv pk) * (Fv conv pv),   dc = dmixed * (Fq conv pq)      (B, C, L) each
  * (the featurizers recomputed with the TMA-fed stream of hy_se_mixer_fwd). lhf <= 8, fp32 / bf16,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "hy_li_conv_segmented_fwd": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_longlong, _I, _P]),
     "hy_causal_conv_bwd_workspace_size": (_SZ, [_I, _I, _I, _I, _I]),
     "hy_causal_conv_bwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
+    "hy_featurize_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "hy_mixer_bwd_prep": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
     "hy_featurizer_bwd_workspace_size": (_SZ, [_I, _I]),
     "hy_featurizer_bwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _SZ, _I, _P]),

@@ -384,6 +384,8 @@ class HyenaCP:
         """events: optional (start, end) CUDA events recorded around the mixer / local conv."""
         from . import _lib, ops
         op, grp = self.op, self.grp
+        if grp.n_ranks == 1:  # one rank: the whole sequence is local, the fused operator applies
+            return op.forward(x_local, events=events)
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
         B, D, m = x3.shape
         if self._fused() and m >= _lib.MIXER_HISTORY:
@@ -400,6 +402,19 @@ class HyenaCP:
                                     packed=op.feat_packed, hist=hist if grp.rank > 0 else None)
             if events is not None:
                 events[1].record()
+        elif self.cfg.variant == "LI" and op.lhf <= 8 and m % 8 == 0 and m >= 8 and \
+                op.dtype in (torch.bfloat16, torch.float32):
+            # one stream for the featurizers and the k*v gate; their halo is the predecessor's
+            # last 8 raw projected steps, received as an explicit history (p2p, one round)
+            proj = op.project(x3)  # (B, 3D, m): token-local
+            hist, reqs = _exchange_halo(proj[..., m - 8:], 8, grp, "cp_feat_hist")
+            for q in reqs:
+                q.wait()
+            u, fq = ops.featurize(proj, op.feat_taps, rhist=hist if grp.rank > 0 else None)
+            slab_conv = _li_slab_conv(op, events) if (op.li_modes is not None and m % 4096 == 0) else None
+            conv = torch.stack([a2a_conv(u[b].contiguous(), self.cfg.inner, grp, conv_slab=slab_conv)
+                                for b in range(B)])
+            mixed = fq * conv
         else:
             proj = op.project(x3)  # (B, 3D, m): token-local
             # featurizers over the 3D projected rows with their (lhf-1)-step halo

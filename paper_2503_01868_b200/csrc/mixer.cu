@@ -346,14 +346,17 @@ __device__ __forceinline__ void hist_shfl(float (&hist)[8], const float (&x)[8],
   }
 }
 
-// PREP: the backward's mixer prologue instead of the mixer: u = fk * fv into y and
-// dc = gmix * fq into dc_out (gmix = gradient at the mixer output), from the same stream.
+// PREP: the featurizer / gate stream instead of the mixer: u = fk * fv into y and
+// dc = gmix * fq into dc_out (gmix = gradient at the mixer output: the backward's prologue),
+// or fq itself when gmix is null (the context-parallel LI forward). rhist (nullable,
+// (B, 3C, 8)): the 8 raw projected steps before t = 0 of every row (the predecessor rank's),
+// used instead of zeros as the featurizers' history.
 template <typename T, int NF, int NI, bool PREP = false>
 __global__ void __launch_bounds__(kSsWarps * 32, 2)
 se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __restrict__ feat_taps, int lhf,
                  const float* __restrict__ inner_taps, const float* __restrict__ decay, int lh, int gs, int B,
                  int C, int L, const T* __restrict__ gmix = nullptr, T* __restrict__ dc_out = nullptr,
-                 T* __restrict__ dc_rev = nullptr) {
+                 T* __restrict__ dc_rev = nullptr, const T* __restrict__ rhist = nullptr) {
   using namespace sm100;
   constexpr int ROWB = kSsChunk * static_cast<int>(sizeof(T));  // bytes per row per stage
   constexpr int NHF = NF - 1, NHI = NI - 1;  // history samples each FIR needs
@@ -388,7 +391,7 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
   // lane 0's issue cursor: the q row of the next entry to issue, its chunk, channel, stage
   const size_t CL = static_cast<size_t>(C) * L;
   const T* iss_q = proj + (static_cast<size_t>(start.row / C) * 3 * C + start.row % C) * L;
-  const T* iss_g = PREP ? gmix + static_cast<size_t>(start.row) * L : nullptr;
+  const T* iss_g = (PREP && gmix) ? gmix + static_cast<size_t>(start.row) * L : nullptr;
   int iss_k = start.k, iss_c = start.row % C, iss_st = 0, n_iss = 0;
   auto issue = [&]() {  // lane 0: entry n_iss into stage n_iss % S
     int t0 = iss_k * kSsChunk, cnt = min(kSsChunk, L - t0), off = 0;
@@ -397,15 +400,15 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
     const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(T));
     const T* src = iss_q + t0;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&bars[iss_st], NR * bytes);
+    mbar_arrive_expect_tx(&bars[iss_st], (PREP && !gmix ? 3 : NR) * bytes);
     bulk_g2s(dst, src + CL, bytes, &bars[iss_st]);                  // k
     bulk_g2s(dst + kSsChunk, src + 2 * CL, bytes, &bars[iss_st]);  // v
     bulk_g2s(dst + 2 * kSsChunk, src, bytes, &bars[iss_st]);       // q
-    if (PREP) bulk_g2s(dst + 3 * kSsChunk, iss_g + t0, bytes, &bars[iss_st]);  // gmix
+    if (PREP && gmix) bulk_g2s(dst + 3 * kSsChunk, iss_g + t0, bytes, &bars[iss_st]);  // gmix
     if (++iss_k == nch) {
       iss_k = 0;
       iss_q += L;
-      if (PREP) iss_g += L;
+      if (PREP && gmix) iss_g += L;
       if (++iss_c == C) iss_c = 0, iss_q += 2 * CL;
     }
     if (++iss_st == kSsStages) iss_st = 0;
@@ -455,7 +458,14 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
     lds8<T>(pv, prv + 2 * kSsChunk - 8);
     lds8<T>(pq, prv + 3 * kSsChunk - 8);
     float gq[8];
-    if (PREP) lds8<T>(gq, cur + 3 * kSsChunk + 8 * lane);
+    if (PREP) {
+      if (gmix) {
+        lds8<T>(gq, cur + 3 * kSsChunk + 8 * lane);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) gq[e] = 1.f;
+      }
+    }
     __syncwarp();
     // the stage read before this one is free now: refill it S - 1 entries ahead
     if (lane == 0 && n_iss < n_issue) issue();
@@ -465,6 +475,13 @@ se_stream_kernel(const T* __restrict__ proj, T* __restrict__ y, const float* __r
     if (row_start) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) pk[e] = pv[e] = pq[e] = ucarry[e] = 0.f;
+      if (PREP && rhist) {  // the predecessor's last 8 raw steps of this row's q / k / v
+        const int b = row / C, c = row - b * C;
+        const T* hq = rhist + (static_cast<size_t>(b) * 3 * C + c) * 8;
+        lds8<T>(pq, hq);
+        lds8<T>(pk, hq + static_cast<size_t>(C) * 8);
+        lds8<T>(pv, hq + 2 * static_cast<size_t>(C) * 8);
+      }
     }
     float hist[8], fk[8], fv[8], u[8], acc[8], fq[8];
     hist_shfl<NHF>(hist, rk, pk, lane);
@@ -569,7 +586,7 @@ static int launch_se(const void* proj, void* y, const float* ft, int lhf, const 
 template <typename T, int NF, int NI, bool PREP = false>
 static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf, const float* it, const float* dec,
                             int lh, int gs, int B, int C, int L, cudaStream_t st, const void* gmix = nullptr,
-                            void* dc_out = nullptr, void* dc_rev = nullptr) {
+                            void* dc_out = nullptr, void* dc_rev = nullptr, const void* rhist = nullptr) {
   auto kern = se_stream_kernel<T, NF, NI, PREP>;
   constexpr int SMEM = kSsWarps * kSsStages * ((PREP ? 4 : 3) * kSsChunk * static_cast<int>(sizeof(T)) + 8);
   static bool attr_set = false;
@@ -589,7 +606,8 @@ static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf,
   if (grid > cap) grid = cap;
   kern<<<static_cast<int>(grid), kSsWarps * 32, SMEM, st>>>(static_cast<const T*>(proj), static_cast<T*>(y), ft, lhf,
                                                              it, dec, lh, gs, B, C, L, static_cast<const T*>(gmix),
-                                                             static_cast<T*>(dc_out), static_cast<T*>(dc_rev));
+                                                             static_cast<T*>(dc_out), static_cast<T*>(dc_rev),
+                                                             static_cast<const T*>(rhist));
   return check_launch("se_stream_kernel");
 }
 
@@ -671,4 +689,28 @@ extern "C" int hy_mixer_bwd_prep(const void* proj, const void* dmixed, const flo
                     : launch_se_stream<float, 8, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C, L, st,
                                                          dmixed, dc, dc_rev);
   return fail(HY_ERR_UNSUPPORTED, "mixer backward prologue: fp32 / bf16 only");
+}
+
+// Featurizers + k*v gate from the projections in one stream (se_stream_kernel<PREP> without a
+// gradient input): u = (Fk conv pk) * (Fv conv pv) and fq = Fq conv pq, with the optional
+// (B, 3C, 8) raw history rhist in place of zeros before t = 0 (context parallel).
+extern "C" int hy_featurize_fwd(const void* proj, const void* rhist, const float* feat_taps, int lhf, int B, int C,
+                                int L, int dtype, void* u, void* fq, void* stream) {
+  if (!proj || !feat_taps || !u || !fq) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (B < 1 || C < 1 || L < 1 || lhf < 1) return fail(HY_ERR_INVALID, "sizes must be >= 1");
+  if (lhf > 8) return fail(HY_ERR_UNSUPPORTED, "featurize: lhf %d > 8", lhf);
+  if (L % 8 != 0 || !aligned16(proj) || !aligned16(u) || !aligned16(fq) || (rhist && !aligned16(rhist)))
+    return fail(HY_ERR_UNSUPPORTED, "featurize needs L %% 8 == 0 and 16-byte aligned rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HY_BF16)
+    return lhf == 7 ? launch_se_stream<__nv_bfloat16, 7, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C,
+                                                                 L, st, nullptr, fq, nullptr, rhist)
+                    : launch_se_stream<__nv_bfloat16, 8, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C,
+                                                                 L, st, nullptr, fq, nullptr, rhist);
+  if (dtype == HY_F32)
+    return lhf == 7 ? launch_se_stream<float, 7, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C, L, st,
+                                                         nullptr, fq, nullptr, rhist)
+                    : launch_se_stream<float, 8, 1, true>(proj, u, feat_taps, lhf, nullptr, nullptr, 1, 1, B, C, L, st,
+                                                         nullptr, fq, nullptr, rhist);
+  return fail(HY_ERR_UNSUPPORTED, "featurize: fp32 / bf16 only");
 }

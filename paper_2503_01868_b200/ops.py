@@ -396,3 +396,20 @@ def two_stage_taps_grad(dc: torch.Tensor, u: torch.Tensor, lh: int, group_size: 
     _lib.check(lib.hy_two_stage_taps_grad(dc3.data_ptr(), u3.data_ptr(), out.data_ptr(), B, C, L, lh, group_size,
                                           _lib.HY_BF16, ws.data_ptr(), ws.numel(), _stream()), "two_stage_taps_grad")
     return out
+
+
+def featurize(proj: torch.Tensor, feat_taps: torch.Tensor, rhist=None):
+    """(u, fq) = ((Fk conv pk) * (Fv conv pv), Fq conv pq) from the (B, 3C, L) projections in
+    one stream (hy_featurize_fwd); rhist: optional (B, 3C, 8) raw steps before t = 0."""
+    _check_device(proj, rhist)
+    B, C3, L = proj.shape
+    C = C3 // 3
+    if rhist is not None and (tuple(rhist.shape) != (B, C3, 8) or rhist.dtype != proj.dtype):
+        raise ValueError(f"rhist must be ({B}, {C3}, 8) {proj.dtype}")
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    u = torch.empty((B, C, L), dtype=proj.dtype, device=proj.device)
+    fq = torch.empty_like(u)
+    lib = _lib.load()
+    _lib.check(lib.hy_featurize_fwd(proj.data_ptr(), _ptr(rhist), ft.data_ptr(), ft.shape[-1], B, C, L,
+                                    _dtype_code(proj), u.data_ptr(), fq.data_ptr(), _stream()), "featurize")
+    return u, fq

@@ -356,3 +356,29 @@ def test_fft_conv_errors():
     v = torch.zeros((1, 2, 64), device="cuda")
     with pytest.raises(ValueError):
         ops.fft_conv(v, torch.zeros((2, 65), device="cuda"), 1)  # lh > L
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_featurize_fwd_with_history(dtype):
+    """hy_featurize_fwd: (u, fq) from the projections; with rhist = the 8 steps before t = 0 it
+    equals the second half of a full-sequence run (the context-parallel halo property)."""
+    B, C, L, lhf = 2, 6, 4096, 7
+    rng = np.random.default_rng(21)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: np.asarray(a, dtype=np.float32).astype(np.float64))
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    u, fq = ops.featurize(dev(proj, tdt), dev(feat))
+    want_u = np.empty((B, C, L))
+    want_q = np.empty((B, C, L))
+    for b in range(B):
+        fqq, fk, fv = (oracle.direct_causal_conv(proj[b, i * C:(i + 1) * C], explicit_bank_from_taps(feat[i], 1))
+                       for i in range(3))
+        want_u[b], want_q[b] = fk * fv, fqq
+    tol = TOL[dtype]
+    assert oracle.rel_err(u.double().cpu().numpy(), want_u) < tol
+    assert oracle.rel_err(fq.double().cpu().numpy(), want_q) < tol
+    pd = dev(proj, tdt)
+    for cut in (2048, 1000, 256):
+        u2, fq2 = ops.featurize(pd[..., cut:].contiguous(), dev(feat), rhist=pd[..., cut - 8:cut].contiguous())
+        assert torch.equal(u2, u[..., cut:]) and torch.equal(fq2, fq[..., cut:]), cut
