@@ -327,6 +327,11 @@ def li_param_grad(dc: torch.Tensor, u: torch.Tensor, residues: torch.Tensor, pol
         raise ValueError("dc and u must match in shape and dtype")
     r, p = _modes(residues, poles, dc3.device)
     B, C, L = dc3.shape
+    if L % 8:  # the kernel streams 16-byte rows; zero steps after L contribute nothing
+        pad = 8 - L % 8
+        dc3 = torch.nn.functional.pad(dc3, (0, pad)).contiguous()
+        u3 = torch.nn.functional.pad(u3, (0, pad)).contiguous()
+        L += pad
     lib = _lib.load()
     d_res = torch.empty_like(r)
     d_pole = torch.empty_like(p)
