@@ -21,12 +21,15 @@ u = k*v to channel slabs with all-to-all for the long convolution.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import blas
 from .core import GroupSpec, SeqTensor
 
 LAYOUTS = ("sequential", "zigzag")
@@ -371,14 +374,119 @@ class HyenaCP:
       or, for LI, by the two all-to-all rounds to channel slabs and back.
     """
 
-    def __init__(self, cfg, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None):
+    def __init__(self, cfg, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None, n_pipe: int | None = None):
         from .hyena import HyenaOperator
         self.op = HyenaOperator(cfg, dtype)
         self.cfg = cfg
         self.grp = grp or CPGroup()
+        # LI: channel segments pipelined through the all-to-all
+        self.n_pipe = n_pipe if n_pipe is not None else int(os.environ.get("HY_CP_NPIPE", "4"))
 
     def _fused(self) -> bool:
         return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
+
+    def _li_pipelined(self, m: int) -> bool:
+        op, n = self.op, self.grp.n_ranks
+        return (self.cfg.variant == "LI" and op.li_modes is not None and op.lhf <= 8 and m % 4096 == 0
+                and self.n_pipe >= 1 and self.cfg.width % (self.n_pipe * n) == 0
+                and (self.cfg.width // (self.n_pipe * n)) % self.cfg.inner.group_size == 0)
+
+    def _li_segments(self):
+        """Per channel segment: the [q; k; v] rows of W_qkv^T, the featurizer taps and the
+        (residues, poles) of every rank's slab, reordered once."""
+        if getattr(self, "_segs", None) is not None:
+            return self._segs
+        op, n = self.op, self.grp.n_ranks
+        D = self.cfg.width
+        seg = D // self.n_pipe
+        segs = []
+        for s in range(self.n_pipe):
+            rows = torch.cat([torch.arange(i * D + s * seg, i * D + (s + 1) * seg) for i in range(3)]).to(op.dev)
+            w = op.w_qkv_t.index_select(0, rows).contiguous()
+            wp = tuple(p.index_select(0, rows).contiguous() for p in op.w_qkv_parts) if op.split3 else None
+            ft = op.feat_taps[:, s * seg:(s + 1) * seg].contiguous()
+            g0 = (s * seg + self.grp.rank * (seg // n)) // op.gs
+            ng = (seg // n) // op.gs
+            res, poles = (t[g0:g0 + ng].contiguous() for t in op.li_modes)
+            segs.append((rows, w, wp, ft, res, poles))
+        self._segs = segs
+        return segs
+
+    def _li_pipeline(self, x3: torch.Tensor, events=None) -> torch.Tensor:
+        """LI layer in n_pipe channel segments (the reference's a2a_conv_pipelined, cpsim.py:449-454,
+        taken up to the projections): segment s's projection GEMM and featurizer stream run on the
+        compute stream while segment s-1's all-to-all rounds and slab conv run on a side stream, so
+        the NVLink traffic hides behind the GEMMs. The all-to-all rounds are copy-engine copies into
+        the peers' symmetric buffers over NVLink (p2p.PeerAllToAll; HY_CP_P2P=0 selects NCCL's
+        all_to_all_single). The featurizer halo (the predecessor's last 8
+        raw projected steps of every row) comes first from a small GEMM on the last 8 input steps
+        and one p2p round."""
+        from . import ops
+        op, grp = self.op, self.grp
+        n, r = grp.n_ranks, grp.rank
+        B, D, m = x3.shape
+        seg = D // self.n_pipe
+        slab = seg // n
+        segs = self._li_segments()
+        comp = torch.cuda.current_stream()
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream(device=x3.device)
+        comm = self._comm
+        peer = None
+        if os.environ.get("HY_CP_P2P", "1") != "0":
+            key = (slab, m, x3.dtype)
+            if getattr(self, "_peer_key", None) != key:
+                from .p2p import PeerAllToAll
+                self._peer = (PeerAllToAll(grp.group, (slab, m), x3.dtype), PeerAllToAll(grp.group, (slab, m), x3.dtype))
+                self._peer_key = key
+            peer = self._peer
+        tail = op.project(x3[..., m - 8:].contiguous())  # (B, 3D, 8)
+        hist, reqs = _exchange_halo(tail, 8, grp, "cp_feat_hist")
+        for q in reqs:
+            q.wait()
+        mixed = torch.empty((B, D, m), dtype=x3.dtype, device=x3.device)
+        pending = []
+        for s, (rows, w, wp, ft, res, poles) in enumerate(segs):
+            proj_s = blas.matmul_split3(wp, blas.split3(x3)) if op.split3 else torch.matmul(w, x3)
+            rh = hist.index_select(1, rows).contiguous() if r > 0 else None
+            u_s, fq_s = ops.featurize(proj_s, ft, rhist=rh)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ev)
+                for b in range(B):
+                    for src in range(n):  # the reference's accounting: scatter + return rounds
+                        for dst in range(n):
+                            if dst != src:
+                                grp._send("a2a_conv_pipelined", src, dst, 2 * slab * m)
+                    if peer is not None:  # copy engines over NVLink peer memory
+                        k = (s * B + b) % 2
+                        recv = peer[0].exchange(u_s[b].view(n, slab, m), k)
+                    else:
+                        recv = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
+                        dist.all_to_all_single(recv, u_s[b], group=grp.group)
+                    if events is not None and s == 0 and b == 0:
+                        events[0].record(comm)
+                    y_slab = ops.li_conv_segmented(recv, res, poles, op.gs)
+                    if events is not None and s == 0 and b == 0:
+                        events[1].record(comm)
+                    if peer is not None:
+                        peer[0].release(k)
+                        back = peer[1].exchange(y_slab, k)
+                    else:
+                        back = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
+                        dist.all_to_all_single(back, y_slab, group=grp.group)
+                    torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
+                    if peer is not None:
+                        peer[1].release(k)
+                u_s.record_stream(comm)
+                fq_s.record_stream(comm)
+            pending.append(u_s)
+        for r_ in range(n):
+            grp.filter_elements[r_] = self.cfg.inner.n_groups // n * self.cfg.inner.filter_len
+        grp.count_rounds("a2a_conv_pipelined", 2 * self.n_pipe * B)
+        comp.wait_stream(comm)
+        return mixed
 
     def forward(self, x_local: torch.Tensor, events=None) -> torch.Tensor:
         """events: optional (start, end) CUDA events recorded around the mixer / local conv."""
@@ -402,19 +510,8 @@ class HyenaCP:
                                     packed=op.feat_packed, hist=hist if grp.rank > 0 else None)
             if events is not None:
                 events[1].record()
-        elif self.cfg.variant == "LI" and op.lhf <= 8 and m % 8 == 0 and m >= 8 and \
-                op.dtype in (torch.bfloat16, torch.float32):
-            # one stream for the featurizers and the k*v gate; their halo is the predecessor's
-            # last 8 raw projected steps, received as an explicit history (p2p, one round)
-            proj = op.project(x3)  # (B, 3D, m): token-local
-            hist, reqs = _exchange_halo(proj[..., m - 8:], 8, grp, "cp_feat_hist")
-            for q in reqs:
-                q.wait()
-            u, fq = ops.featurize(proj, op.feat_taps, rhist=hist if grp.rank > 0 else None)
-            slab_conv = _li_slab_conv(op, events) if (op.li_modes is not None and m % 4096 == 0) else None
-            conv = torch.stack([a2a_conv(u[b].contiguous(), self.cfg.inner, grp, conv_slab=slab_conv)
-                                for b in range(B)])
-            mixed = fq * conv
+        elif self._li_pipelined(m):
+            mixed = self._li_pipeline(x3, events)
         else:
             proj = op.project(x3)  # (B, 3D, m): token-local
             # featurizers over the 3D projected rows with their (lhf-1)-step halo

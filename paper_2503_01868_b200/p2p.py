@@ -1,0 +1,146 @@
+"""All-to-all over NVLink peer memory for the context-parallel LI layer (no NCCL kernels).
+
+Every rank owns a symmetric receive buffer of `nslots` slots, each (n_ranks, chunk) bytes,
+allocated with cudaMalloc and mapped into every peer by CUDA IPC (cudaIpcOpenMemHandle with
+lazy peer access: the peer's pages are addressed directly over NVLink / NVSwitch). A
+transfer is a set of stream-ordered copy-engine copies (cudaMemcpyAsync on peer pointers, one
+side stream per destination so the copies run on separate engines and links) followed by a
+32-bit flag write into the receiver (cuStreamWriteValue32, with its default memory barrier);
+the receiver's stream waits on the flags (cuStreamWaitValue32). The copies take no SMs, so
+they overlap the projection GEMMs fully — NCCL's all-to-all kernels would share the SMs.
+
+Flow control per slot: a use counter u. The sender, before writing slot k of rank d for use
+u, waits until d has released use u-1 of that slot (d writes u-1 into the sender's `free`
+flag after its consumer is enqueued); the receiver waits until every sender's `arrive` flag
+reaches u. Nothing is ever host-synchronised.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+try:
+    from cuda.bindings import driver as _cu
+    from cuda.bindings import runtime as _rt
+except ImportError:  # pragma: no cover - cuda-python is part of the image
+    _cu = _rt = None
+
+_GEQ = 0  # CU_STREAM_WAIT_VALUE_GEQ
+_WDEF = 0  # CU_STREAM_WRITE_VALUE_DEFAULT (fenced)
+_D2D = 3  # cudaMemcpyDeviceToDevice
+
+
+def _ck(res):
+    err = res[0] if isinstance(res, tuple) else res
+    if int(err) != 0:
+        raise RuntimeError(f"CUDA call failed: {err}")
+    return res[1] if isinstance(res, tuple) and len(res) == 2 else res
+
+
+class _RawArray:
+    """A cudaMalloc'd region viewed as a torch tensor through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, shape, dtype: torch.dtype):
+        typestr = {torch.bfloat16: "<V2", torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self.dtype = dtype
+
+    def tensor(self) -> torch.Tensor:
+        if self.dtype == torch.bfloat16:  # no bf16 typestr: view 2-byte words as int16 then reinterpret
+            iface = dict(self.__cuda_array_interface__, typestr="<i2")
+            holder = type("H", (), {"__cuda_array_interface__": iface})()
+            return torch.as_tensor(holder, device="cuda").view(torch.bfloat16)
+        return torch.as_tensor(self, device="cuda")
+
+
+class PeerAllToAll:
+    """Symmetric-buffer all-to-all among the ranks of `group` (one process per GPU, one node)."""
+
+    def __init__(self, group, chunk_shape, dtype: torch.dtype, nslots: int = 2):
+        if _rt is None:
+            raise RuntimeError("cuda-python is required for the peer-memory all-to-all")
+        self.group = group
+        self.n = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.nslots = nslots
+        self.chunk_shape = tuple(chunk_shape)
+        self.dtype = dtype
+        esz = torch.empty((), dtype=dtype).element_size()
+        self.chunk = int(esz * torch.Size(chunk_shape).numel())
+        self.slot = self.n * self.chunk
+        dev = torch.cuda.current_device()
+        self.data = int(_ck(_rt.cudaMalloc(nslots * self.slot)))
+        self.flags = int(_ck(_rt.cudaMalloc(2 * nslots * self.n * 4)))  # arrive[k][src], free[k][dst]
+        _ck(_rt.cudaMemset(self.flags, 0, 2 * nslots * self.n * 4))
+        _ck(_rt.cudaDeviceSynchronize())
+        mine = (bytes(_ck(_rt.cudaIpcGetMemHandle(self.data)).reserved),
+                bytes(_ck(_rt.cudaIpcGetMemHandle(self.flags)).reserved), dev)
+        allh = [None] * self.n
+        dist.all_gather_object(allh, mine, group=group)
+        self.peer_data, self.peer_flags = [0] * self.n, [0] * self.n
+        for p in range(self.n):
+            if p == self.r:
+                self.peer_data[p], self.peer_flags[p] = self.data, self.flags
+                continue
+            hd, hf = _rt.cudaIpcMemHandle_t(), _rt.cudaIpcMemHandle_t()
+            hd.reserved, hf.reserved = allh[p][0], allh[p][1]
+            self.peer_data[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hd, _rt.cudaIpcMemLazyEnablePeerAccess)))
+            self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
+        self.use = [0] * nslots
+        self.streams = [torch.cuda.Stream() for _ in range(self.n)]
+        dist.barrier(group=group)
+
+    # flag addresses: arrive[k][src] at (k * n + src), free[k][dst] at (nslots * n + k * n + dst)
+    def _arrive(self, base: int, k: int, src: int) -> int:
+        return base + 4 * (k * self.n + src)
+
+    def _free(self, base: int, k: int, dst: int) -> int:
+        return base + 4 * (self.nslots * self.n + k * self.n + dst)
+
+    def recv_tensor(self, k: int) -> torch.Tensor:
+        """Slot k of this rank's receive buffer as (n, *chunk_shape): [src] = what src sent."""
+        return _RawArray(self.data + k * self.slot, (self.n,) + self.chunk_shape, self.dtype).tensor()
+
+    def exchange(self, send: torch.Tensor, k: int) -> torch.Tensor:
+        """send: (n, *chunk_shape) contiguous on this rank, [dst] goes to rank dst. Enqueued on
+        the current stream; returns slot k of the receive buffer (valid on that stream)."""
+        if tuple(send.shape) != (self.n,) + self.chunk_shape or send.dtype != self.dtype or not send.is_contiguous():
+            raise ValueError("send must be a contiguous (n_ranks, *chunk_shape) tensor of the exchange dtype")
+        cur = torch.cuda.current_stream()
+        u = self.use[k] + 1
+        self.use[k] = u
+        src_base = send.data_ptr()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        done = []
+        for d in range(self.n):
+            st = self.streams[d]
+            st.wait_event(ev)
+            h = st.cuda_stream
+            if d != self.r:  # d has consumed use u-1 of its slot k
+                _ck(_cu.cuStreamWaitValue32(h, self._free(self.flags, k, d), u - 1, _GEQ))
+            dst = self.peer_data[d] + k * self.slot + self.r * self.chunk
+            _ck(_rt.cudaMemcpyAsync(dst, src_base + d * self.chunk, self.chunk, _D2D, h))
+            if d != self.r:
+                _ck(_cu.cuStreamWriteValue32(h, self._arrive(self.peer_flags[d], k, self.r), u, _WDEF))
+            e = torch.cuda.Event()
+            e.record(st)
+            done.append(e)
+        send.record_stream(cur)
+        for e in done:
+            cur.wait_event(e)
+        h = cur.cuda_stream
+        for s in range(self.n):
+            if s != self.r:
+                _ck(_cu.cuStreamWaitValue32(h, self._arrive(self.flags, k, s), u, _GEQ))
+        return self.recv_tensor(k)
+
+    def release(self, k: int) -> None:
+        """Enqueue on the current stream (after the last reader of slot k): tell every sender
+        that this rank is done with slot k's current use."""
+        h = torch.cuda.current_stream().cuda_stream
+        for s in range(self.n):
+            if s != self.r:
+                _ck(_cu.cuStreamWriteValue32(h, self._free(self.peer_flags[s], k, self.r), self.use[k], _WDEF))
