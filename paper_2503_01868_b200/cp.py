@@ -382,6 +382,18 @@ class HyenaCP:
         # LI: channel segments pipelined through the all-to-all
         self.n_pipe = n_pipe if n_pipe is not None else int(os.environ.get("HY_CP_NPIPE", "4"))
 
+    def _halo_peer(self, tail: torch.Tensor):
+        """PeerHalo for this tail shape (created once per shape; CUDA devices only)."""
+        if not tail.is_cuda:
+            return None
+        key = (tuple(tail.shape), tail.dtype)
+        if getattr(self, "_halo_key", None) != key:
+            from .p2p import PeerHalo
+            self._halo = PeerHalo(self.grp.group, tail.shape, tail.dtype)
+            self._halo_key = key
+            self._halo_step = 0
+        return self._halo
+
     def _fused(self) -> bool:
         return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
 
@@ -441,9 +453,18 @@ class HyenaCP:
                 self._peer_key = key
             peer = self._peer
         tail = op.project(x3[..., m - 8:].contiguous())  # (B, 3D, 8)
-        hist, reqs = _exchange_halo(tail, 8, grp, "cp_feat_hist")
-        for q in reqs:
-            q.wait()
+        hpeer = self._halo_peer(tail) if peer is not None else None
+        if hpeer is not None:
+            hk = self._halo_step % 2
+            self._halo_step += 1
+            for src in range(n - 1):
+                grp._send("cp_feat_hist", src, src + 1, tail.numel())
+            hist = hpeer.send(tail, hk)
+            hpeer.wait(hk)
+        else:
+            hist, reqs = _exchange_halo(tail, 8, grp, "cp_feat_hist")
+            for q in reqs:
+                q.wait()
         mixed = torch.empty((B, D, m), dtype=x3.dtype, device=x3.device)
         pending = []
         for s, (rows, w, wp, ft, res, poles) in enumerate(segs):
@@ -485,6 +506,8 @@ class HyenaCP:
         for r_ in range(n):
             grp.filter_elements[r_] = self.cfg.inner.n_groups // n * self.cfg.inner.filter_len
         grp.count_rounds("a2a_conv_pipelined", 2 * self.n_pipe * B)
+        if hpeer is not None:  # every segment's featurizer stream has read the history
+            hpeer.release(hk)
         comp.wait_stream(comm)
         return mixed
 
@@ -500,14 +523,26 @@ class HyenaCP:
             # the successor needs only the projections of the last 144 steps: compute those
             # first and start the send, so the transfer overlaps the full projection GEMM
             tail = op.project(x3[..., m - _lib.MIXER_HISTORY:].contiguous())
-            hist, reqs = _exchange_halo(tail, _lib.MIXER_HISTORY, grp, "cp_hist")
-            proj = op.project(x3)  # (B, 3D, m): token-local
-            for q in reqs:
-                q.wait()
+            peer = self._halo_peer(tail) if os.environ.get("HY_CP_P2P", "1") != "0" else None
+            if peer is not None:  # copy engine into rank r+1's symmetric slot (no SMs, no NCCL)
+                k = self._halo_step % 2
+                self._halo_step += 1
+                for src in range(grp.n_ranks - 1):
+                    grp._send("cp_hist", src, src + 1, tail.numel() // tail.shape[-1] * _lib.MIXER_HISTORY)
+                hist = peer.send(tail, k)
+                proj = op.project(x3)  # (B, 3D, m): token-local
+                peer.wait(k)
+            else:
+                hist, reqs = _exchange_halo(tail, _lib.MIXER_HISTORY, grp, "cp_hist")
+                proj = op.project(x3)  # (B, 3D, m): token-local
+                for q in reqs:
+                    q.wait()
             if events is not None:
                 events[0].record()
             mixed = ops.hyena_mixer(proj, op.feat_taps, op.inner_taps, op.gs, decay=op.decay,
                                     packed=op.feat_packed, hist=hist if grp.rank > 0 else None)
+            if peer is not None:
+                peer.release(k)
             if events is not None:
                 events[1].record()
         elif self._li_pipelined(m):

@@ -1,4 +1,6 @@
-"""All-to-all over NVLink peer memory for the context-parallel LI layer (no NCCL kernels).
+"""All-to-all and causal halo over NVLink peer memory for the context-parallel layer (no
+NCCL kernels): PeerAllToAll for the LI sequence <-> channel swaps, PeerHalo for the SE/MR
+point-to-point history.
 
 Every rank owns a symmetric receive buffer of `nslots` slots, each (n_ranks, chunk) bytes,
 allocated with cudaMalloc and mapped into every peer by CUDA IPC (cudaIpcOpenMemHandle with
@@ -55,25 +57,22 @@ class _RawArray:
         return torch.as_tensor(self, device="cuda")
 
 
-class PeerAllToAll:
-    """Symmetric-buffer all-to-all among the ranks of `group` (one process per GPU, one node)."""
+class _Symmetric:
+    """`nslots` data slots of `slot` bytes plus `nflags` 32-bit flags per rank, cudaMalloc'd
+    and mapped into every peer of `group` by CUDA IPC (lazy peer access over NVLink)."""
 
-    def __init__(self, group, chunk_shape, dtype: torch.dtype, nslots: int = 2):
+    def __init__(self, group, slot: int, nslots: int, nflags: int):
         if _rt is None:
-            raise RuntimeError("cuda-python is required for the peer-memory all-to-all")
+            raise RuntimeError("cuda-python is required for the peer-memory transfers")
         self.group = group
         self.n = dist.get_world_size(group)
         self.r = dist.get_rank(group)
         self.nslots = nslots
-        self.chunk_shape = tuple(chunk_shape)
-        self.dtype = dtype
-        esz = torch.empty((), dtype=dtype).element_size()
-        self.chunk = int(esz * torch.Size(chunk_shape).numel())
-        self.slot = self.n * self.chunk
+        self.slot = slot
         dev = torch.cuda.current_device()
-        self.data = int(_ck(_rt.cudaMalloc(nslots * self.slot)))
-        self.flags = int(_ck(_rt.cudaMalloc(2 * nslots * self.n * 4)))  # arrive[k][src], free[k][dst]
-        _ck(_rt.cudaMemset(self.flags, 0, 2 * nslots * self.n * 4))
+        self.data = int(_ck(_rt.cudaMalloc(nslots * slot)))
+        self.flags = int(_ck(_rt.cudaMalloc(nflags * 4)))
+        _ck(_rt.cudaMemset(self.flags, 0, nflags * 4))
         _ck(_rt.cudaDeviceSynchronize())
         mine = (bytes(_ck(_rt.cudaIpcGetMemHandle(self.data)).reserved),
                 bytes(_ck(_rt.cudaIpcGetMemHandle(self.flags)).reserved), dev)
@@ -89,6 +88,18 @@ class PeerAllToAll:
             self.peer_data[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hd, _rt.cudaIpcMemLazyEnablePeerAccess)))
             self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
         self.use = [0] * nslots
+
+
+class PeerAllToAll(_Symmetric):
+    """Symmetric-buffer all-to-all among the ranks of `group` (one process per GPU, one node)."""
+
+    def __init__(self, group, chunk_shape, dtype: torch.dtype, nslots: int = 2):
+        n = dist.get_world_size(group)
+        esz = torch.empty((), dtype=dtype).element_size()
+        self.chunk_shape = tuple(chunk_shape)
+        self.dtype = dtype
+        self.chunk = int(esz * torch.Size(chunk_shape).numel())
+        super().__init__(group, n * self.chunk, nslots, 2 * nslots * n)  # arrive[k][src], free[k][dst]
         self.streams = [torch.cuda.Stream() for _ in range(self.n)]
         dist.barrier(group=group)
 
@@ -144,3 +155,56 @@ class PeerAllToAll:
         for s in range(self.n):
             if s != self.r:
                 _ck(_cu.cuStreamWriteValue32(h, self._free(self.peer_flags[s], k, self.r), self.use[k], _WDEF))
+
+
+class PeerHalo(_Symmetric):
+    """Causal halo to the next rank (the p2p scheme's one message per boundary, cpsim.py:475-485)
+    as one copy-engine copy into rank r+1's symmetric slot plus a fenced flag write: no NCCL
+    kernel, no SMs, so the transfer hides behind the projection GEMM that follows it.
+
+    Flags: arrive[k] (written by r-1), free[k] (written by r+1). Per-slot use counters give
+    the same flow control as PeerAllToAll."""
+
+    def __init__(self, group, shape, dtype: torch.dtype, nslots: int = 2):
+        self.shape = tuple(shape)
+        self.dtype = dtype
+        nbytes = int(torch.empty((), dtype=dtype).element_size() * torch.Size(shape).numel())
+        super().__init__(group, nbytes, nslots, 2 * nslots)
+        self.side = torch.cuda.Stream()
+        dist.barrier(group=group)
+
+    def send(self, tail: torch.Tensor, k: int):
+        """Enqueue (after the current stream's work) the copy of `tail` into rank r+1's slot k;
+        returns slot k of this rank's buffer (rank r-1's halo; None on rank 0). Call wait(k)
+        on the consuming stream before reading it."""
+        if tuple(tail.shape) != self.shape or tail.dtype != self.dtype or not tail.is_contiguous():
+            raise ValueError("halo must be a contiguous tensor of the exchange shape and dtype")
+        u = self.use[k] + 1
+        self.use[k] = u
+        if self.r < self.n - 1:
+            cur = torch.cuda.current_stream()
+            self.side.wait_stream(cur)
+            h = self.side.cuda_stream
+            d = self.r + 1
+            _ck(_cu.cuStreamWaitValue32(h, self.flags + 4 * (self.nslots + k), u - 1, _GEQ))
+            _ck(_rt.cudaMemcpyAsync(self.peer_data[d] + k * self.slot, tail.data_ptr(), self.slot, _D2D, h))
+            _ck(_cu.cuStreamWriteValue32(h, self.peer_flags[d] + 4 * k, u, _WDEF))
+            tail.record_stream(self.side)
+        if self.r == 0:
+            return None
+        if not hasattr(self, "_views"):
+            self._views = [_RawArray(self.data + j * self.slot, self.shape, self.dtype).tensor()
+                           for j in range(self.nslots)]
+        return self._views[k]
+
+    def wait(self, k: int) -> None:
+        """Current stream waits until rank r-1's halo for slot k's current use has landed."""
+        if self.r > 0:
+            _ck(_cu.cuStreamWaitValue32(torch.cuda.current_stream().cuda_stream, self.flags + 4 * k,
+                                        self.use[k], _GEQ))
+
+    def release(self, k: int) -> None:
+        """Enqueue after the last reader of slot k: rank r-1 may overwrite it."""
+        if self.r > 0:
+            _ck(_cu.cuStreamWriteValue32(torch.cuda.current_stream().cuda_stream,
+                                         self.peer_flags[self.r - 1] + 4 * (self.nslots + k), self.use[k], _WDEF))

@@ -40,8 +40,9 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _cp_worker(rank, world, port, variant, q):
+def _cp_worker(rank, world, port, variant, q, p2p="1"):
     import torch.distributed as dist
+    os.environ["HY_CP_P2P"] = p2p
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -53,7 +54,9 @@ def _cp_worker(rank, world, port, variant, q):
         gen = torch.Generator(device="cuda").manual_seed(7)
         x = torch.randn((1, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
         m = L // world
-        y_local = hy.cp.HyenaCP(cfg, torch.bfloat16).forward(x[..., rank * m:(rank + 1) * m].contiguous())
+        cpop = hy.cp.HyenaCP(cfg, torch.bfloat16)
+        for _ in range(3):  # repeated steps exercise the slot flow control of the peer transfers
+            y_local = cpop.forward(x[..., rank * m:(rank + 1) * m].contiguous())
         if rank == 0:
             y_ref = hy.HyenaOperator(cfg, torch.bfloat16).forward(x)
         parts = [torch.empty_like(y_local) for _ in range(world)]
@@ -67,14 +70,16 @@ def _cp_worker(rank, world, port, variant, q):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("p2p", ["1", "0"], ids=["peer", "nccl"])
 @pytest.mark.parametrize("variant", ["MR", "SE", "LI"])
-def test_hyena_cp_matches_single_gpu(variant):
+def test_hyena_cp_matches_single_gpu(variant, p2p):
+    """HyenaCP's halo / all-to-all over copy-engine peer transfers (default) and over NCCL."""
     import torch.multiprocessing as mp
     world = min(torch.cuda.device_count(), 4)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, variant, q)) for r in range(world)]
+    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, variant, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     err = q.get(timeout=600)
