@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   uint64_t* qempty = qfull + NBUF;       // [NBUF] epilogue warps -> converter
   uint64_t* efull = qempty + NBUF;       // [2] IMPL: MMA commit -> scan warp (E in TMEM)
   uint64_t* eempty = efull + 2;          // [2] IMPL: scan warp -> MMA (E drained)
-  uint64_t* sready = eempty + 2;         // [NBUF] IMPL: scan warp -> MMA (S_prev in SMEM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -275,7 +274,6 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       mbar_init(&qempty[i], N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
-      mbar_init(&sready[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&efull[i], 1);
@@ -421,29 +419,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const uint32_t t0a = tmem_base + TM_T0, t1a = tmem_base + TM_T1;
     if (IMPL) {
       // per tile j: T0 . U and E = Lam . U (one commit -> scan warp); the inter-chunk term
-      // P . S_prev of tile j waits for the scan and is issued after tile j+1's MMAs (or
-      // before them when tile j+1 starts a new group, whose factors wait on it)
-      constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
-      const uint32_t pa = smem_u32(smem + LY::OFF_P);
+      // P . S_prev of tile j is issued by the scan warp itself once the states are in SMEM
+      // (its efull wait orders it after this tile's T0 . U), keeping this loop short
       const uint32_t la = smem_u32(smem + LY::OFF_L);
-      int pend = -1;
-      bool pend_last = false;
-      auto finish = [&](int jj, bool lst) {
-        const int uu = jj % NBUF;
-        if (lane == 0) trace(p, jj, 19);
-        mbar_wait(&sready[uu], (jj / NBUF) & 1);
-        if (lane == 0) trace(p, jj, 20);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + LY::OFF_S + uu * NCH * NPOLE * 4);
-        if (elect_one()) {
-          mma_tf32(tmem_base + TM_ACC + uu * NCH, desc_noswz(pa, 128, 256), desc_noswz(sa, 128, 256), idesc_tf32,
-                   1u);
-          if (lst) mma_commit(&tfree[1]);
-          mma_commit(&tfull[uu]);
-        }
-        if (lane == 0) trace(p, jj, 8);
-        __syncwarp();
-      };
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -459,10 +437,6 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         if (lane == 0) trace(p, j, 16);
         mbar_wait(&tempty[u], ph ^ 1);
         if (lane == 0) trace(p, j, 17);
-        if (first && pend >= 0) {
-          finish(pend, pend_last);
-          pend = -1;
-        }
         if (lane == 0) trace(p, j, 4);
         if (first) mbar_wait(&tready[0], gi & 1);
         mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
@@ -489,11 +463,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           trace(p, j, 7);
         }
         __syncwarp();
-        if (pend >= 0) finish(pend, pend_last);
-        pend = j;
-        pend_last = last;
       }
-      if (pend >= 0) finish(pend, pend_last);
     } else {
       int gi = -1, g_prev = -1;
       Tile t;
@@ -699,7 +669,10 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     // as the tf32 B operand S_prev[c][n] (element (c, n) at (c%8)*16 + (c/8)*256 + (n%4)*4 +
     // (n/4)*128 bytes) and carried to the next tile of the channel
     float lam128 = 0.f, carry = 0.f;
-    auto scan = [&](int j, const Tile& tl) {
+    // after the states: D += P . S_prev (tf32 MMA, issued here; the epilogue waits on its commit)
+    constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
+    const uint32_t pa_s = smem_u32(smem + LY::OFF_P);
+    auto scan = [&](int j, const Tile& tl, bool lst) {
       const int eb = j & 1;
       mbar_wait(&efull[eb], (j >> 1) & 1);
       if (lane == 0) trace(p, j, 9);
@@ -719,8 +692,17 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       carry = st;
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sready[j % NBUF]);
       if (lane == 0) trace(p, j, 10);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sa = smem_u32(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
+        mma_tf32(tmem_base + TM_ACC + (j % NBUF) * NCH, desc_noswz(pa_s, 128, 256), desc_noswz(sa, 128, 256),
+                 idesc_tf32, 1u);
+        if (lst) mma_commit(&tfree[1]);
+        mma_commit(&tfull[j % NBUF]);
+        trace(p, j, 8);
+      }
+      __syncwarp();
     };
     int gi = 0, g_prev = -1;
     Tile t;
@@ -729,8 +711,10 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     if (ntiles > 0) prefetch(t.c / p.gs);
     for (int j = 0; j < ntiles; ++j, t.next(p)) {
       const int g = t.c / p.gs;
+      // last tile of its group with a successor tile: its tf32 MMA commit frees P
+      const bool lst = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
       if (g == g_prev) {
-        if (IMPL && warp == W_TB0) scan(j, t);
+        if (IMPL && warp == W_TB0) scan(j, t, lst);
         continue;
       }
       g_prev = g;
@@ -771,7 +755,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         build(0);
         if (g < g_end) prefetch(g + 1);
         ++gi;
-        if (warp == W_TB0) scan(j, t);
+        if (warp == W_TB0) scan(j, t, lst);
         continue;
       }
 #pragma unroll

@@ -34,7 +34,7 @@ tr -= tr[0, 0]
 EV = {0: "P_got_empty", 11: "P_issued", 1: "C_ffull", 2: "C_uempty", 3: "C_done", 4: "M_start", 7: "M_E_commit",
       8: "M_tf32", 9: "S_efull", 10: "S_done", 5: "E_tfull", 6: "E_done", 16: "M_ufull", 17: "M_tempty",
       18: "M_eempty", 19: "F_start", 20: "F_sready"}
-order = [0, 11, 1, 2, 3, 16, 17, 4, 18, 7, 9, 10, 19, 20, 8, 5, 6]
+order = [0, 11, 1, 2, 3, 16, 17, 4, 18, 7, 9, 10, 8, 5, 6]
 print("tiles 40..44 (cycles):")
 for it in range(40, 45):
     print(it, " ".join(f"{EV[e]}={tr[it, e]:8.0f}" for e in order))
@@ -45,11 +45,7 @@ def st(a, b):
     d = tr[20:n, b] - tr[20:n, a]
     print(f"{EV[a]:>12s} -> {EV[b]:12s} median {np.median(d):7.0f} p90 {np.percentile(d, 90):7.0f}")
 for a, b in [(0, 11), (11, 1), (1, 2), (2, 3), (3, 4), (4, 7), (7, 9), (9, 10), (10, 8), (8, 5), (5, 6),
-             (16, 17), (17, 4), (4, 18), (18, 7), (19, 20), (20, 8)]:
+             (16, 17), (17, 4), (4, 18), (18, 7)]:
     st(a, b)
-# MMA-warp loop, tile j: M_ufull(j) .. E_commit(j), then finish(j-1) (events 19/20/8 are
-# indexed by the finished tile), then M_ufull(j+1)
-d = tr[20:n - 1, 19] - tr[21:n, 7]
-print(f"{'E_commit(j) -> F_start(j-1)':30s} median {np.median(d):7.0f}")
-d = tr[22:n, 16] - tr[21:n - 1, 8]
-print(f"{'F_done(j-1) -> M_ufull(j+1)':30s} median {np.median(d):7.0f}")
+d = tr[21:n, 16] - tr[20:n - 1, 7]
+print(f"{'E_commit(j) -> M_ufull(j+1)':30s} median {np.median(d):7.0f}")
