@@ -29,6 +29,8 @@
 //   warps 12-15 T builder: Toeplitz factors T0 / T1 of the next filter group, each
 //                          rebuilt as soon as the last MMA reading the old one retires
 //                          (tcgen05.commit after that tile's T0 / T1 MMAs)
+//   (IMPL)      scan     : per-mode state recurrence over each tile's chunks + the P . S_prev
+//                          tf32 MMA (one extra warp; the ids below shift by one)
 //   warp 16     feat MMA : one lane issues the featurizer MMAs of each tile, then frees
 //                          the stage (tcgen05.commit -> empty barrier)
 //   warp 17     MMA      : TMEM alloc (512 cols); one lane issues the 16 main MMAs per tile
@@ -69,8 +71,14 @@ constexpr int N_CONV_WARPS = 8, N_EPI_WARPS = 4, N_TB_WARPS = 4;
 constexpr int W_CONV0 = 0, W_EPI0 = W_CONV0 + N_CONV_WARPS, W_TB0 = W_EPI0 + N_EPI_WARPS;
 // Two producer warps alternate tiles (each owns every other stage of the ring).
 constexpr int N_PROD_WARPS = 2;
-constexpr int W_FMMA = W_TB0 + N_TB_WARPS, W_MMA = W_FMMA + 1, W_PROD = W_MMA + 1;
-constexpr int THREADS = (W_PROD + N_PROD_WARPS) * 32;
+// IMPL adds one warp for the per-mode state scan (21 warps, <= 80 registers); the explicit
+// modes keep 20 warps and their 96-register budget
+template <bool IMPL>
+struct Warps {
+  static constexpr int SCAN = IMPL ? W_TB0 + N_TB_WARPS : -1;
+  static constexpr int FMMA = W_TB0 + N_TB_WARPS + (IMPL ? 1 : 0), MMA = FMMA + 1, PROD = MMA + 1;
+  static constexpr int THREADS = (PROD + N_PROD_WARPS) * 32;
+};
 constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
 constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
 
@@ -85,7 +93,9 @@ constexpr uint32_t TM_ACC = 0, TM_T0 = NBUF * NCH, TM_T1 = TM_T0 + 64, TM_FEAT =
 constexpr uint32_t TM_K = 0, TM_V = 16 * KV_MB, TM_Q = 32 * KV_MB;
 // implicit mode has no T1: its columns hold the mode-input accumulators E[2] x 32
 constexpr uint32_t TM_E = TM_T1;
-static_assert(TM_FEAT + TM_Q + 16 * Q_MB <= 512, "TMEM budget");
+// implicit mode double-buffers its group factors: T0 of odd groups in the last 64 columns
+constexpr uint32_t TM_T0B = 448;
+static_assert(TM_FEAT + TM_Q + 16 * Q_MB <= TM_T0B && TM_T0B + 64 <= 512, "TMEM budget");
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
 constexpr int KV_BYTES = round_up(KV_LEN * 2, 128);
@@ -110,6 +120,10 @@ struct Layout {
   // E[n][chunk] = Lam . U (SW128 K-major, 8 rows, two 64-element K atoms; the descriptor's
   // zero group stride lets the M = 128 MMA re-read these rows for every 8-row group)
   static constexpr int OFF_L = round_up(OFF_S + NBUF * NCH * NPOLE * 4, 1024);
+  // implicit mode keeps two sets (P, Lam) for group double-buffering in the U_prev region,
+  // which it does not use: P[b] at OFF_UP + 4096 b, Lam[b] at OFF_UP + 8192 + 2048 b
+  static constexpr int OFF_P2 = OFF_UP, OFF_L2 = OFF_UP + 8192;
+  static_assert(OFF_L2 % 1024 == 0 && OFF_L2 + 4096 <= OFF_FQ, "implicit factor buffers");
   static constexpr int OFF_BAR = OFF_L + 2048;
   static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
@@ -224,8 +238,10 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // s_n[t] = lam_n s_n[t-1] + u[t] carried chunk to chunk (E = per-chunk mode inputs,
 // S_prev = state entering each chunk) and applied by one tf32 MMA, P . S_prev.
 template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL>
-__global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
+__global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(const Params p) {
   using LY = Layout<KS>;
+  constexpr int W_SCAN = Warps<IMPL>::SCAN, W_FMMA = Warps<IMPL>::FMMA, W_MMA = Warps<IMPL>::MMA,
+                W_PROD = Warps<IMPL>::PROD;
   constexpr int STAGES = LY::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // keep the pointer in the shared window (offset arithmetic, not an integer round trip)
@@ -245,6 +261,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
   uint64_t* qempty = qfull + NBUF;       // [NBUF] epilogue warps -> converter
   uint64_t* efull = qempty + NBUF;       // [2] IMPL: MMA commit -> scan warp (E in TMEM)
   uint64_t* eempty = efull + 2;          // [2] IMPL: scan warp -> MMA (E drained)
+  // IMPL factor buffers b = 0 / 1: tfree[b] (MMA warp: last T0 . U / Lam . U of buffer b
+  // retired), tfreep[b] (scan warp: last P . S_prev of buffer b retired), tready[b]
+  uint64_t* tfreep = eempty + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -278,6 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&efull[i], 1);
       mbar_init(&eempty[i], 1);
+      mbar_init(&tfreep[i], 1);
     }
     fence_mbar_init();
   }
@@ -421,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       // per tile j: T0 . U and E = Lam . U (one commit -> scan warp); the inter-chunk term
       // P . S_prev of tile j is issued by the scan warp itself once the states are in SMEM
       // (its efull wait orders it after this tile's T0 . U), keeping this loop short
-      const uint32_t la = smem_u32(smem + LY::OFF_L);
+      const uint32_t la0 = smem_u32(smem + LY::OFF_L2);
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -438,18 +458,21 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
         mbar_wait(&tempty[u], ph ^ 1);
         if (lane == 0) trace(p, j, 17);
         if (lane == 0) trace(p, j, 4);
-        if (first) mbar_wait(&tready[0], gi & 1);
+        const int fb = gi & 1;  // this group's factor buffer
+        if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
         mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
         if (lane == 0) trace(p, j, 18);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
         const uint32_t de = tmem_base + TM_E + (j & 1) * NCH;
         const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
+        const uint32_t ta = tmem_base + (fb ? TM_T0B : TM_T0);
+        const uint32_t la = la0 + fb * 2048;
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+            mma_bf16_ts(d, ta + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           }
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
@@ -459,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           }
           mma_commit(&efull[j & 1]);
           mma_commit(&uempty[u]);
-          if (last) mma_commit(&tfree[0]);
+          if (last) mma_commit(&tfree[fb]);
           trace(p, j, 7);
         }
         __syncwarp();
@@ -618,7 +641,69 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       if (lane == 0) mbar_arrive(&qempty[a]);
       if (quarter == 0 && lane == 0) trace(p, it, 6);
     }
-  } else if (warp >= W_TB0 && warp < W_FMMA) {
+  } else if (warp == W_SCAN) {
+    // ------------------------------------------------------------ IMPL state scan
+    // (lane n < NPOLE = mode n): E[n][chunk] from TMEM, then the sequential state
+    // recurrence over the tile's chunks; the state entering chunk c is written as the tf32
+    // B operand S_prev[c][n] (element (c, n) at (c%8)*16 + (c/8)*256 + (n%4)*4 + (n/4)*128
+    // bytes) and carried to the next tile of the sequence. Then D += P . S_prev (tf32 MMA,
+    // issued here: the efull wait orders it after the tile's T0 . U; the epilogue waits on
+    // its commit). A warp of its own, so the factor builds never stall it.
+    if (IMPL) {
+      constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
+      const uint32_t pa_s = smem_u32(smem + LY::OFF_P2);
+      float lam128 = 0.f, carry = 0.f;
+      const int g_end = ntiles > 0 ? ((te - 1) / (p.tiles_per_seq * p.B)) / p.gs : -1;
+      auto pole = [&](int g) {
+        return (lane < NPOLE && lane < p.npoles) ? p.poles[static_cast<size_t>(g) * p.npoles + lane] : 0.f;
+      };
+      int gi = -1, g_prev = -1;
+      Tile t;
+      t.init(tb, p);
+      float pf = ntiles > 0 ? pole(t.c / p.gs) : 0.f;
+      for (int j = 0; j < ntiles; ++j, t.next(p)) {
+        const int g = t.c / p.gs;
+        const bool lst = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
+        if (g != g_prev) {
+          g_prev = g;
+          ++gi;
+          lam128 = powf(pf, 128.f);
+          if (g < g_end) pf = pole(g + 1);
+        }
+        const int fb = gi & 1;
+        const int eb = j & 1;
+        mbar_wait(&efull[eb], (j >> 1) & 1);
+        if (lane == 0) trace(p, j, 9);
+        tc_fence_after();
+        float ev[NCH];
+        tmem_ld_32x32b_x32(tmem_base + TM_E + eb * NCH, ev);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&eempty[eb]);
+        float* sp = reinterpret_cast<float*>(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
+        float st = t.t0 == 0 ? 0.f : carry;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          if (lane < NPOLE) sp[((c & 7) * 16 + (c >> 3) * 256 + (lane & 3) * 4 + (lane >> 2) * 128) / 4] = st;
+          st = fmaf(lam128, st, ev[c]);
+        }
+        carry = st;
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) trace(p, j, 10);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
+          mma_tf32(tmem_base + TM_ACC + (j % NBUF) * NCH, desc_noswz(pa_s + fb * 4096, 128, 256),
+                   desc_noswz(sa, 128, 256), idesc_tf32, 1u);
+          if (lst) mma_commit(&tfreep[fb]);
+          mma_commit(&tfull[j % NBUF]);
+          trace(p, j, 8);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= W_TB0 && warp < W_TB0 + N_TB_WARPS) {
     // ------------------------------------------------------------ Toeplitz factor builder
     const int bt = threadIdx.x - W_TB0 * 32;
     constexpr int PER = 512 / TB_THREADS;  // hpad entries per thread
@@ -647,7 +732,7 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-    auto build = [&](int fct) {
+    auto build = [&](int fct, uint32_t tcol, uint64_t* rdy) {
       const unsigned short* hp = reinterpret_cast<const unsigned short*>(hpad) + 128 + fct * 128 + mrow;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -657,105 +742,69 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
           const int cc = half * 32 + c;
           w[c] = static_cast<uint32_t>(hp[-2 * cc]) | (static_cast<uint32_t>(hp[-2 * cc - 1]) << 16);
         }
-        tmem_st_32x32b_x32(trow + (fct ? TM_T1 : TM_T0) + half * 32, w);
+        tmem_st_32x32b_x32(trow + tcol + half * 32, w);
       }
       tmem_wait_st();
       tc_fence_before();
       named_bar_sync(BAR_TB, TB_THREADS);
-      if (bt == 0) mbar_arrive(&tready[fct]);
+      if (bt == 0) mbar_arrive(rdy);
     };
-    // IMPL scan (warp W_TB0, lane n < NPOLE = mode n): E[n][chunk] from TMEM, then the
-    // sequential state recurrence over the tile's chunks; the state entering chunk c is written
-    // as the tf32 B operand S_prev[c][n] (element (c, n) at (c%8)*16 + (c/8)*256 + (n%4)*4 +
-    // (n/4)*128 bytes) and carried to the next tile of the channel
-    float lam128 = 0.f, carry = 0.f;
-    // after the states: D += P . S_prev (tf32 MMA, issued here; the epilogue waits on its commit)
-    constexpr uint32_t idesc_tf32 = idesc_tf32_f32<LB, NCH>();
-    const uint32_t pa_s = smem_u32(smem + LY::OFF_P);
-    auto scan = [&](int j, const Tile& tl, bool lst) {
-      const int eb = j & 1;
-      mbar_wait(&efull[eb], (j >> 1) & 1);
-      if (lane == 0) trace(p, j, 9);
-      tc_fence_after();
-      float ev[NCH];
-      tmem_ld_32x32b_x32(tmem_base + TM_E + eb * NCH, ev);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&eempty[eb]);
-      float* sp = reinterpret_cast<float*>(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
-      float st = tl.t0 == 0 ? 0.f : carry;
+    // IMPL: group gb's factors into buffer gb & 1 (T0 in TMEM, P / Lam in SMEM), built one
+    // group ahead from the prefetched modes once group gb - 2's last readers retired:
+    // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states),
+    // P[m][n] = R_n lam_n^(m+1) as the tf32 A operand (element (m, n) at
+    // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes) and Lam[n][t] = lam_n^(127 - t)
+    auto build_impl = [&](int gb) {
+      const int b = gb & 1;
+      if (gb >= 2) {
+        mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);   // T0 / Lam of buffer b: last readers retired
+        mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);  // P of buffer b
+      }
+      float hv = 0.f, pm[NPOLE];
+      unsigned char* lrow = smem + LY::OFF_L2 + b * 2048 + (bt >> 6) * 1024 + (bt & 7) * 2;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (lane < NPOLE) sp[((c & 7) * 16 + (c >> 3) * 256 + (lane & 3) * 4 + (lane >> 2) * 128) / 4] = st;
-        st = fmaf(lam128, st, ev[c]);
+      for (int n = 0; n < NPOLE; ++n) {
+        const float lt = powf(pf_pole[n], static_cast<float>(bt));
+        hv = fmaf(pf_res[n], lt, hv);
+        pm[n] = pf_res[n] * lt * pf_pole[n];
+        const int jj = (bt >> 3) & 7;
+        *reinterpret_cast<bf16*>(lrow + n * 128 + ((jj ^ n) << 4)) =
+            __float2bfloat16_rn(powf(pf_pole[n], static_cast<float>(127 - bt)));
       }
-      carry = st;
+      hpad[bt] = __float2bfloat16_rn(0.f);
+      hpad[128 + bt] = __float2bfloat16_rn(hv);
+      hpad[256 + bt] = __float2bfloat16_rn(0.f);
+      hpad[384 + bt] = __float2bfloat16_rn(0.f);
+      float* pa = reinterpret_cast<float*>(smem + LY::OFF_P2 + b * 4096 + (bt & 7) * 16 + (bt >> 3) * 256);
+      *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
+      *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
       fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) trace(p, j, 10);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sa = smem_u32(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
-        mma_tf32(tmem_base + TM_ACC + (j % NBUF) * NCH, desc_noswz(pa_s, 128, 256), desc_noswz(sa, 128, 256),
-                 idesc_tf32, 1u);
-        if (lst) mma_commit(&tfree[1]);
-        mma_commit(&tfull[j % NBUF]);
-        trace(p, j, 8);
-      }
-      __syncwarp();
+      named_bar_sync(BAR_TB, TB_THREADS);
+      build(0, b ? TM_T0B : TM_T0, &tready[b]);
     };
     int gi = 0, g_prev = -1;
     Tile t;
     t.init(tb, p);
     const int g_end = ntiles > 0 ? ((te - 1) / (p.tiles_per_seq * p.B)) / p.gs : -1;  // last group
-    if (ntiles > 0) prefetch(t.c / p.gs);
+    if (ntiles > 0) {
+      prefetch(t.c / p.gs);
+      if (IMPL) {
+        build_impl(0);
+        if (t.c / p.gs < g_end) prefetch(t.c / p.gs + 1);
+      }
+    }
     for (int j = 0; j < ntiles; ++j, t.next(p)) {
       const int g = t.c / p.gs;
-      // last tile of its group with a successor tile: its tf32 MMA commit frees P
-      const bool lst = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
-      if (g == g_prev) {
-        if (IMPL && warp == W_TB0) scan(j, t, lst);
-        continue;
-      }
+      if (g == g_prev) continue;
       g_prev = g;
       if (IMPL) {
-        // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states),
-        // P[m][n] = R_n lam_n^(m+1) as the tf32 A operand (element (m, n) at
-        // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes) and Lam[n][t] = lam_n^(127 - t)
-        if (gi > 0) {
-          mbar_wait(&tfree[0], (gi - 1) & 1);  // T0 / Lam: last T0 . U and Lam . U retired
-          mbar_wait(&tfree[1], (gi - 1) & 1);  // P: last P . S_prev retired
+        // group gi starts: its factors were built one group ahead; build group gi + 1 into
+        // the other buffer
+        if (g < g_end) {
+          build_impl(gi + 1);
+          if (g + 1 < g_end) prefetch(g + 2);
         }
-        float hv = 0.f, pm[NPOLE];
-        unsigned char* lrow = smem + LY::OFF_L + (bt >> 6) * 1024 + (bt & 7) * 2;
-#pragma unroll
-        for (int n = 0; n < NPOLE; ++n) {
-          const float lt = powf(pf_pole[n], static_cast<float>(bt));
-          hv = fmaf(pf_res[n], lt, hv);
-          pm[n] = pf_res[n] * lt * pf_pole[n];
-          const int jj = (bt >> 3) & 7;
-          *reinterpret_cast<bf16*>(lrow + n * 128 + ((jj ^ n) << 4)) =
-              __float2bfloat16_rn(powf(pf_pole[n], static_cast<float>(127 - bt)));
-        }
-        if (warp == W_TB0) {
-          lam128 = 0.f;
-#pragma unroll
-          for (int n = 0; n < NPOLE; ++n)
-            if (n == lane) lam128 = powf(pf_pole[n], 128.f);
-        }
-        hpad[bt] = __float2bfloat16_rn(0.f);
-        hpad[128 + bt] = __float2bfloat16_rn(hv);
-        hpad[256 + bt] = __float2bfloat16_rn(0.f);
-        hpad[384 + bt] = __float2bfloat16_rn(0.f);
-        float* pa = reinterpret_cast<float*>(smem + LY::OFF_P + (bt & 7) * 16 + (bt >> 3) * 256);
-        *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
-        *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
-        fence_proxy_async();
-        named_bar_sync(BAR_TB, TB_THREADS);
-        build(0);
-        if (g < g_end) prefetch(g + 1);
         ++gi;
-        if (warp == W_TB0) scan(j, t, lst);
         continue;
       }
 #pragma unroll
@@ -766,9 +815,9 @@ __global__ void __launch_bounds__(THREADS, 1) two_stage_kernel(const Params p) {
       }
       named_bar_sync(BAR_TB, TB_THREADS);
       if (gi > 0) mbar_wait(&tfree[0], (gi - 1) & 1);
-      build(0);
+      build(0, TM_T0, &tready[0]);
       if (gi > 0) mbar_wait(&tfree[1], (gi - 1) & 1);
-      build(1);
+      build(1, TM_T1, &tready[1]);
       if (g < g_end) prefetch(g + 1);  // next group's taps load during this group
       ++gi;
     }
@@ -795,7 +844,7 @@ static int launch_ks(const Params& p, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = IMPL ? p.total_tiles / p.tiles_per_seq : p.total_tiles;  // IMPL: whole sequences
   const int grid = units < sms ? units : sms;
-  kern<<<grid, THREADS, smem, st>>>(p);
+  kern<<<grid, Warps<IMPL>::THREADS, smem, st>>>(p);
   return check_launch("two_stage_kernel");
 }
 

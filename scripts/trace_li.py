@@ -35,9 +35,11 @@ EV = {0: "P_got_empty", 11: "P_issued", 1: "C_ffull", 2: "C_uempty", 3: "C_done"
       8: "M_tf32", 9: "S_efull", 10: "S_done", 5: "E_tfull", 6: "E_done", 16: "M_ufull", 17: "M_tempty",
       18: "M_eempty", 19: "F_start", 20: "F_sready"}
 order = [0, 11, 1, 2, 3, 16, 17, 4, 18, 7, 9, 10, 8, 5, 6]
-print("tiles 40..44 (cycles):")
-for it in range(40, 45):
+print("tiles 30..34 and 40..44 (cycles):")
+for it in list(range(30, 35)) + list(range(40, 45)):
     print(it, " ".join(f"{EV[e]}={tr[it, e]:8.0f}" for e in order))
+big = np.diff(tr[20:n, 6])
+print("E_done gaps > 2x median at tiles:", [(i + 21, int(v)) for i, v in enumerate(big) if v > 2 * np.median(big)])
 for e in order:
     d = np.diff(tr[20:n, e])
     print(f"period {EV[e]:12s} median {np.median(d):7.0f} mean {d.mean():7.0f}")
