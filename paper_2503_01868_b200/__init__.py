@@ -5,7 +5,7 @@ C-ABI of include/hyena_b200.h; there is no CPU fallback.
 """
 
 from . import cp, fft
-from .cp import CPGroup, ShardedSeq, a2a_conv, a2a_conv_pipelined, gather, p2p_conv, p2p_conv_overlapped, shard
+from .cp import CPGroup, LayoutCP, ShardedSeq, a2a_conv, a2a_conv_pipelined, gather, layout_forward_cp, p2p_conv, p2p_conv_overlapped, shard
 from .backward import (
     DeviceGrads,
     HyenaGrads,

@@ -12,6 +12,9 @@ output, and tally the same accounting as the reference's SimGroup (cpsim.py:69-1
   a2a_conv             two all_to_all_single rounds swap time shards <-> channel slabs,
                        conv over the full sequence on the slab (cpsim.py:325-447)
   a2a_conv_pipelined   the same in n_pipe channel segments (cpsim.py:449-454)
+  p2p_fft_conv         distributed FFT: log2(N) cross-rank DiF stages (one partner
+                       exchange each), local FFT, bit-reversed bin ownership, spectrum
+                       product, inverse (cpsim.py:540-659)
 
 `HyenaCP` composes them into the context-parallel Hyena operator:
 projections and gates are token-local; SE/MR receive the last 144 steps of the
@@ -45,6 +48,24 @@ class CPGroup:
     scheme_rounds: dict = field(default_factory=dict)
     filter_elements: dict = field(default_factory=dict)
     message_log: list = field(default_factory=list)
+    # symmetric peer buffers (p2p.PeerHalo / PeerAllToAll) shared by every CP layer on this
+    # group, keyed by (kind, shape, dtype): a deep stack maps one set, not one per layer
+    peers: dict = field(default_factory=dict, repr=False)
+    max_resident: dict = field(default_factory=dict)  # rank -> max sequence samples held (dfft)
+
+    def note_resident(self, rank: int, samples: int) -> None:
+        self.max_resident[rank] = max(self.max_resident.get(rank, 0), samples)
+
+    def peer(self, kind: str, shape, dtype):
+        key = (kind, tuple(shape), dtype)
+        if key not in self.peers:
+            from . import p2p
+            if kind == "halo":
+                self.peers[key] = p2p.PeerHalo(self.group, shape, dtype)
+            else:  # the LI all-to-all: a scatter and a return exchanger
+                self.peers[key] = (p2p.PeerAllToAll(self.group, shape, dtype),
+                                   p2p.PeerAllToAll(self.group, shape, dtype))
+        return self.peers[key]
 
     def __post_init__(self):
         n = self.n_ranks
@@ -361,6 +382,135 @@ def a2a_conv_pipelined(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_p
 # ---------------------------------------------------------------- context-parallel Hyena operator
 
 
+# ---------------------------------------------------------------- distributed FFT (cpsim.py:537-659)
+
+
+def _partner_exchange(x: torch.Tensor, partner: int, grp: CPGroup) -> torch.Tensor:
+    """Swap a complex tensor with one partner rank (both send, both receive)."""
+    xr = torch.view_as_real(x).contiguous()
+    out = torch.empty_like(xr)
+    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, xr, partner, grp.group),
+                                   dist.P2POp(dist.irecv, out, partner, grp.group)])
+    for q in reqs:
+        q.wait()
+    return torch.view_as_complex(out)
+
+
+def _dfft_check(local: torch.Tensor, grp: CPGroup) -> int:
+    from .fft import require_pow2
+    require_pow2(local.shape[-1])
+    return local.shape[-1]
+
+
+def _complex(local: torch.Tensor) -> torch.Tensor:
+    if local.is_complex():
+        return local
+    return local.to(torch.complex128 if local.dtype == torch.float64 else torch.complex64)
+
+
+def _stage_twiddle(g: int, half: int, m: int, length: int, sign: float, like: torch.Tensor) -> torch.Tensor:
+    pos = torch.arange(m, dtype=torch.float64) + (g if g < half else g - half) * m
+    ang = sign * 2.0 * np.pi * pos / length
+    return torch.polar(torch.ones_like(ang), ang).to(like.device, like.dtype)
+
+
+def p2p_fft_forward(local: torch.Tensor, grp: CPGroup, scheme: str = "p2p_fft_conv") -> torch.Tensor:
+    """This rank's spectrum slice of the sequentially sharded signal (cpsim.py:547-566, 596-604):
+    stage s pairs rank r with r +- half inside groups of N >> (s-1) ranks; the low half keeps
+    x + other, the high half (other - x) * W^pos; then a local FFT. Rank r ends up owning the
+    bins congruent to bitrev(r) mod N."""
+    m = _dfft_check(local, grp)
+    n, r = grp.n_ranks, grp.rank
+    total = m * n
+    x = _complex(local)
+    elems = int(x.numel())
+    grp.note_resident(r, m)
+    stages = int(np.log2(n))
+    for stage in range(1, stages + 1):
+        group, length = n >> (stage - 1), total >> (stage - 1)
+        half = group // 2
+        g = r % group
+        for src in range(n):  # every rank tallies every message
+            gs_ = src % group
+            grp._send(scheme, src, src + half if gs_ < half else src - half, elems)
+        partner = r + half if g < half else r - half
+        other = _partner_exchange(x, partner, grp)
+        if g < half:
+            x = x + other
+        else:
+            x = (other - x) * _stage_twiddle(g, half, m, length, -1.0, x)
+        grp.note_resident(r, m)
+    grp.count_rounds(scheme, stages)
+    return torch.fft.fft(x)
+
+
+def p2p_fft_inverse(spec: torch.Tensor, grp: CPGroup, scheme: str = "p2p_fft_conv") -> torch.Tensor:
+    """Inverse of p2p_fft_forward (cpsim.py:569-590, 607-615): local inverse FFT, then the
+    stages in reverse with conjugate twiddles and a factor 1/2; restores the sequential shard."""
+    n, r = grp.n_ranks, grp.rank
+    x = torch.fft.ifft(spec)
+    m = x.shape[-1]
+    total = m * n
+    elems = int(x.numel())
+    grp.note_resident(r, m)
+    stages = int(np.log2(n))
+    for stage in range(stages, 0, -1):
+        group, length = n >> (stage - 1), total >> (stage - 1)
+        half = group // 2
+        g = r % group
+        for src in range(n):
+            gs_ = src % group
+            grp._send(scheme, src, src + half if gs_ < half else src - half, elems)
+        partner = r + half if g < half else r - half
+        other = _partner_exchange(x, partner, grp)
+        w_inv = _stage_twiddle(g, half, m, length, 1.0, x)
+        x = 0.5 * (x + w_inv * other) if g < half else 0.5 * (other - w_inv * x)
+        grp.note_resident(r, m)
+    grp.count_rounds(scheme, stages)
+    return x
+
+
+def p2p_fft_conv(local_x: torch.Tensor, local_h: torch.Tensor, grp: CPGroup) -> torch.Tensor:
+    """Circular convolution with both operands sharded along time (cpsim.py:618-631)."""
+    _dfft_check(local_x, grp)
+    _dfft_check(local_h, grp)
+    if tuple(local_h.shape) != tuple(local_x.shape):
+        raise ValueError("filter must be sharded identically to the input")
+    for r in range(grp.n_ranks):
+        grp.filter_elements[r] = int(local_h.numel())
+    prod = p2p_fft_forward(local_x, grp) * p2p_fft_forward(local_h, grp)
+    return p2p_fft_inverse(prod, grp).real.contiguous()
+
+
+def p2p_fft_causal_wrapper(x: SeqTensor, h_taps, grp: CPGroup | None = None, device=None) -> SeqTensor:
+    """Causal linear convolution on the distributed circular core (cpsim.py:634-659): pad to
+    2 * next_pow2(L), each rank takes its sequential shard of the padded signal and filter,
+    runs p2p_fft_conv, and the shards are gathered and truncated. Every rank returns y."""
+    from .fft import next_pow2
+    grp = grp or CPGroup()
+    taps = np.asarray(h_taps, dtype=np.float64)
+    if taps.ndim == 1:
+        taps = np.broadcast_to(taps, (x.channels, taps.size))
+    if taps.shape[0] != x.channels:
+        raise ValueError(f"taps cover {taps.shape[0]} channels, input has {x.channels}")
+    taps = taps[:, : x.length]
+    size = 2 * next_pow2(x.length)
+    n, r = grp.n_ranks, grp.rank
+    m = size // n
+    dev = device if device is not None else ("cuda" if dist.get_backend(grp.group) == "nccl" else "cpu")
+    xp = np.zeros((x.channels, size))
+    xp[:, : x.length] = x.data
+    hp = np.zeros((x.channels, size))
+    hp[:, : taps.shape[1]] = taps
+    lx = torch.from_numpy(np.ascontiguousarray(xp[:, r * m:(r + 1) * m])).to(dev)
+    lh = torch.from_numpy(np.ascontiguousarray(hp[:, r * m:(r + 1) * m])).to(dev)
+    y_local = p2p_fft_conv(lx, lh, grp)
+    parts = [torch.empty_like(y_local) for _ in range(n)]
+    dist.all_gather(parts, y_local, group=grp.group)
+    y = torch.cat(parts, dim=-1)[:, : x.length].cpu().numpy()
+    return SeqTensor(y, dtype=x.dtype)
+
+
 class HyenaCP:
     """Context-parallel Hyena operator: each rank holds the (B, D, L/N) time
     shard of x (sequential layout) and returns its shard of y.
@@ -383,16 +533,8 @@ class HyenaCP:
         self.n_pipe = n_pipe if n_pipe is not None else int(os.environ.get("HY_CP_NPIPE", "4"))
 
     def _halo_peer(self, tail: torch.Tensor):
-        """PeerHalo for this tail shape (created once per shape; CUDA devices only)."""
-        if not tail.is_cuda:
-            return None
-        key = (tuple(tail.shape), tail.dtype)
-        if getattr(self, "_halo_key", None) != key:
-            from .p2p import PeerHalo
-            self._halo = PeerHalo(self.grp.group, tail.shape, tail.dtype)
-            self._halo_key = key
-            self._halo_step = 0
-        return self._halo
+        """The group's PeerHalo for this tail shape (CUDA devices only)."""
+        return self.grp.peer("halo", tail.shape, tail.dtype) if tail.is_cuda else None
 
     def _fused(self) -> bool:
         return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
@@ -446,17 +588,11 @@ class HyenaCP:
         comm = self._comm
         peer = None
         if os.environ.get("HY_CP_P2P", "1") != "0":
-            key = (slab, m, x3.dtype)
-            if getattr(self, "_peer_key", None) != key:
-                from .p2p import PeerAllToAll
-                self._peer = (PeerAllToAll(grp.group, (slab, m), x3.dtype), PeerAllToAll(grp.group, (slab, m), x3.dtype))
-                self._peer_key = key
-            peer = self._peer
+            peer = grp.peer("a2a", (slab, m), x3.dtype)
         tail = op.project(x3[..., m - 8:].contiguous())  # (B, 3D, 8)
         hpeer = self._halo_peer(tail) if peer is not None else None
         if hpeer is not None:
-            hk = self._halo_step % 2
-            self._halo_step += 1
+            hk = hpeer.next_slot()
             for src in range(n - 1):
                 grp._send("cp_feat_hist", src, src + 1, tail.numel())
             hist = hpeer.send(tail, hk)
@@ -481,7 +617,7 @@ class HyenaCP:
                             if dst != src:
                                 grp._send("a2a_conv_pipelined", src, dst, 2 * slab * m)
                     if peer is not None:  # copy engines over NVLink peer memory
-                        k = (s * B + b) % 2
+                        k = peer[0].next_slot()
                         recv = peer[0].exchange(u_s[b].view(n, slab, m), k)
                     else:
                         recv = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
@@ -525,8 +661,7 @@ class HyenaCP:
             tail = op.project(x3[..., m - _lib.MIXER_HISTORY:].contiguous())
             peer = self._halo_peer(tail) if os.environ.get("HY_CP_P2P", "1") != "0" else None
             if peer is not None:  # copy engine into rank r+1's symmetric slot (no SMs, no NCCL)
-                k = self._halo_step % 2
-                self._halo_step += 1
+                k = peer.next_slot()
                 for src in range(grp.n_ranks - 1):
                     grp._send("cp_hist", src, src + 1, tail.numel() // tail.shape[-1] * _lib.MIXER_HISTORY)
                 hist = peer.send(tail, k)
@@ -618,3 +753,30 @@ def _per_channel_groups(taps: torch.Tensor) -> GroupSpec:
     from .core import ExplicitFilter
     t = taps.detach().double().cpu().numpy()
     return GroupSpec(t.shape[0], 1, tuple(ExplicitFilter(r) for r in t))
+
+
+class LayoutCP:
+    """Multi-layer context-parallel stack (hyena.py:377-392 over cpsim's
+    sequential sharding): the sequence is sharded once, every layer runs as HyenaCP on the
+    rank's (B, D, L/N) shard and the residual add is token-local, so activations stay sharded
+    from the first layer to the last. Layers share the group's peer buffers (CPGroup.peer)."""
+
+    def __init__(self, stack, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None,
+                 n_pipe: int | None = None):
+        self.grp = grp or CPGroup()
+        self.layers = [HyenaCP(cfg, dtype, self.grp, n_pipe) for cfg in stack.layers]
+        self.residual = stack.residual
+
+    def forward(self, x_local: torch.Tensor) -> torch.Tensor:
+        cur = x_local
+        for layer in self.layers:
+            out = layer.forward(cur)
+            cur = cur + out if self.residual else out
+        return cur
+
+    __call__ = forward
+
+
+def layout_forward_cp(x_local: torch.Tensor, stack, grp: CPGroup | None = None) -> torch.Tensor:
+    """layout_forward (hyena.py:386) on this rank's sequential shard of x."""
+    return LayoutCP(stack, x_local.dtype, grp).forward(x_local)

@@ -88,6 +88,13 @@ class _Symmetric:
             self.peer_data[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hd, _rt.cudaIpcMemLazyEnablePeerAccess)))
             self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
         self.use = [0] * nslots
+        self.step = 0
+
+    def next_slot(self) -> int:
+        """Slots are taken round robin; every rank calls this in the same order."""
+        k = self.step % self.nslots
+        self.step += 1
+        return k
 
 
 class PeerAllToAll(_Symmetric):

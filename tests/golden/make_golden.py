@@ -319,6 +319,44 @@ def gen_cpsim() -> None:
     save("cpsim", c)
 
 
+def gen_dfft() -> None:
+    """Distributed FFT scheme (cpsim.py:537-659), cases of pkg/tests/test_cpsim.py:324-412."""
+    c = {}
+    for n_ranks, seed, length in ((2, 111, 16), (4, 112, 32)):
+        rng = make_rng(seed)
+        x = rng.standard_normal((1, length))
+        spectra = cpsim.p2p_fft_forward(cpsim.shard(SeqTensor(x), n_ranks), cpsim.SimGroup(n_ranks))
+        c[f"own{n_ranks}.x"] = x
+        for r in range(n_ranks):
+            c[f"own{n_ranks}.spec{r}"] = spectra[r]
+    for n_ranks in (2, 4, 8):
+        rng = make_rng(114)
+        x = rng.standard_normal((2, 64))
+        h = rng.standard_normal((2, 64))
+        grp = cpsim.SimGroup(n_ranks)
+        ys = cpsim.p2p_fft_conv(cpsim.shard(SeqTensor(x), n_ranks), cpsim.shard(SeqTensor(h), n_ranks), grp)
+        c[f"conv{n_ranks}.x"] = x
+        c[f"conv{n_ranks}.h"] = h
+        c[f"conv{n_ranks}.y"] = cpsim.gather(ys).data
+        c[f"conv{n_ranks}.elements"] = grp.total_elements("p2p_fft_conv")
+        c[f"conv{n_ranks}.messages"] = grp.total_messages("p2p_fft_conv")
+        c[f"conv{n_ranks}.rounds"] = grp.scheme_rounds.get("p2p_fft_conv", 0)
+        c[f"conv{n_ranks}.max_resident"] = max(grp.max_resident.values())
+    rng = make_rng(118)
+    taps = rng.standard_normal(24) / np.sqrt(24)
+    x = random_seq(rng, 2, 96)
+    c["causal.taps"] = taps
+    c["causal.x"] = x.data
+    c["causal.y"] = cpsim.p2p_fft_causal_wrapper(x, taps, 4, cpsim.SimGroup(4)).data
+    rng = make_rng(119)
+    taps = rng.standard_normal(40)
+    x = random_seq(rng, 1, 32)
+    c["trunc.taps"] = taps
+    c["trunc.x"] = x.data
+    c["trunc.y"] = cpsim.p2p_fft_causal_wrapper(x, taps, 2, cpsim.SimGroup(2)).data
+    save("dfft", c)
+
+
 def gen_builders() -> None:
     """Raw make_hyena_config draws, to pin the product's seeded builders."""
     c = {}
@@ -468,5 +506,6 @@ if __name__ == "__main__":
     gen_hyena()
     gen_layout()
     gen_cpsim()
+    gen_dfft()
     gen_builders()
     gen_backward()

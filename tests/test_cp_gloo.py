@@ -179,3 +179,68 @@ def test_a2a_backward_matches_reference(idx):
     assert np.max(np.abs(got - z[f"ab{idx}.dx"])) < 1e-12
     assert res[0][2] == int(z[f"ab{idx}.elements"]) and res[0][3] == int(z[f"ab{idx}.messages"])
     assert res[0][1] * 2 == res[0][2]  # the backward moves as much as the forward
+
+
+def _dfft_worker(rank, world, port, q):
+    from paper_2503_01868_b200 import SeqTensor, cp
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        z = load("dfft")
+        out = {}
+        if f"own{world}.x" in z:  # bin ownership of the forward transform
+            grp = cp.CPGroup()
+            x = z[f"own{world}.x"]
+            m = x.shape[-1] // world
+            spec = cp.p2p_fft_forward(torch.from_numpy(x[:, rank * m:(rank + 1) * m].copy()), grp)
+            out["own"] = float(np.max(np.abs(spec.numpy() - z[f"own{world}.spec{rank}"])))
+        grp = cp.CPGroup()
+        x, h = z[f"conv{world}.x"], z[f"conv{world}.h"]
+        m = x.shape[-1] // world
+        lx = torch.from_numpy(x[:, rank * m:(rank + 1) * m].copy())
+        lh = torch.from_numpy(h[:, rank * m:(rank + 1) * m].copy())
+        y = cp.p2p_fft_conv(lx, lh, grp)
+        out["conv"] = float(np.max(np.abs(y.numpy() - z[f"conv{world}.y"][:, rank * m:(rank + 1) * m])))
+        out["acct"] = (grp.total_elements("p2p_fft_conv"), grp.total_messages("p2p_fft_conv"),
+                       grp.scheme_rounds.get("p2p_fft_conv", 0), max(grp.max_resident.values()))
+        out["want_acct"] = (int(z[f"conv{world}.elements"]), int(z[f"conv{world}.messages"]),
+                            int(z[f"conv{world}.rounds"]), int(z[f"conv{world}.max_resident"]))
+        for case, n in (("causal", 4), ("trunc", 2)):
+            if n == world:
+                yc = cp.p2p_fft_causal_wrapper(SeqTensor(z[f"{case}.x"]), z[f"{case}.taps"], cp.CPGroup())
+                out[case] = float(np.max(np.abs(yc.data - z[f"{case}.y"])))
+        if world == 2:  # the reference's argument checks (test_cpsim.py:391-402)
+            for bad in (lambda: cp.p2p_fft_forward(torch.zeros((1, 12), dtype=torch.float64), cp.CPGroup()),
+                        lambda: cp.p2p_fft_conv(torch.zeros((2, 16), dtype=torch.float64),
+                                                torch.zeros((1, 16), dtype=torch.float64), cp.CPGroup())):
+                try:
+                    bad()
+                    out["raises"] = False
+                except ValueError:
+                    out.setdefault("raises", True)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_p2p_fft_matches_reference_simulator(world):
+    """Distributed FFT over gloo (cpsim.py:537-659) against the reference simulator's outputs:
+    bit-reversed bin ownership, circular conv, accounting, causal wrapper, argument checks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dfft_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, out in res.items():
+        assert out.get("own", 0.0) < 1e-10, (r, out)
+        assert out["conv"] < 1e-10, (r, out)
+        assert out["acct"] == out["want_acct"], (r, out)
+        assert out.get("causal", 0.0) < 1e-10 and out.get("trunc", 0.0) < 1e-10, (r, out)
+        assert out.get("raises", True), (r, out)

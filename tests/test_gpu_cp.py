@@ -140,3 +140,92 @@ def test_a2a_backward_nccl_matches_oracle():
         assert p.exitcode == 0
     for layout, err in res.items():
         assert err < 1e-12, (layout, err)
+
+
+def _layout_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        D, L = 64, 8192 * world
+        rng = hy.make_rng(4)
+        layers = (hy.make_hyena_config("SE", D, rng, seq_len=L),
+                  hy.make_hyena_config("MR", D, rng, inner_len=128, block_size=128),
+                  hy.make_hyena_config("LI", D, rng, seq_len=L),
+                  hy.make_hyena_config("MR", D, rng, inner_len=128, block_size=128))
+        stack = hy.build_layout(hy.LayoutSpec(("SE", "MR", "LI", "MR"), 1, layers), residual=True)
+        gen = torch.Generator(device="cuda").manual_seed(9)
+        x = torch.randn((1, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
+        m = L // world
+        lcp = hy.LayoutCP(stack, torch.bfloat16)
+        for _ in range(2):
+            y_local = lcp.forward(x[..., rank * m:(rank + 1) * m].contiguous())
+        parts = [torch.empty_like(y_local) for _ in range(world)]
+        dist.all_gather(parts, y_local)
+        if rank == 0:
+            y_ref = hy.layout_forward_device(x, stack).float()
+            y = torch.cat(parts, dim=-1).float()
+            q.put(float((y - y_ref).abs().max() / max(1.0, float(y_ref.abs().max()))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_layout_cp_matches_single_gpu():
+    """SE-MR-LI-MR residual stack sharded once across ranks (LayoutCP) equals the single-GPU
+    layout forward; the layers share the group's peer buffers."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert err < 2e-2, err
+
+
+def _dfft_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import oracle
+        rng = np.random.default_rng(21)
+        C, L, lh = 4, 3000, 700
+        x = rng.standard_normal((C, L))
+        taps = rng.standard_normal((C, lh)) / np.sqrt(lh)
+        y = hy.cp.p2p_fft_causal_wrapper(hy.SeqTensor(x), taps, hy.cp.CPGroup())
+        if rank == 0:
+            want = oracle.direct_causal_conv(x, {"channels": C, "group_size": 1,
+                                                 "filters": [("explicit", t) for t in taps]})
+            q.put(float(np.abs(y.data - want).max() / max(1.0, np.abs(want).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_p2p_fft_causal_nccl_matches_oracle():
+    """Distributed FFT conv (cpsim.py:634-659) over NCCL on the devices, float64 (cuFFT local
+    transforms), against the oracle's direct causal conv."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dfft_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert err < 1e-10, err
