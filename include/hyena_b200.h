@@ -146,6 +146,19 @@ HY_API int hy_fft_conv_fwd(const void* q, const void* k, const void* v, void* y,
                     int B, int C, int L, int lh, int group_size, int dtype,
                     void* ws, size_t ws_bytes, void* stream);
 
+/* Cached filter spectra for the register four-step path (2^14 <= N <= 2^18, N =
+ * next_pow2(L + lh - 1)): hy_fft_spectrum() writes the spectrum of every group's zero-padded
+ * taps (G, lh) fp32 into spec (hy_fft_spectrum_size() bytes; 0 = size not covered) once per
+ * filter bank — the FFT(pad(h)) half of fft.py:128-145 as a parameter transform; ws:
+ * hy_fft_conv_workspace_size(1, G, L, lh, 1, HY_F32) bytes. hy_fft_conv_spec_fwd() is
+ * hy_fft_conv_fwd() reading those spectra instead of transforming the taps. */
+HY_API size_t hy_fft_spectrum_size(int n_groups, int L, int lh);
+HY_API int hy_fft_spectrum(const void* taps, int n_groups, int L, int lh, void* spec, void* ws,
+                           size_t ws_bytes, void* stream);
+HY_API int hy_fft_conv_spec_fwd(const void* q, const void* k, const void* v, void* y, const void* spec,
+                                int B, int C, int L, int lh, int group_size, int dtype,
+                                void* ws, size_t ws_bytes, void* stream);
+
 /* Overlapped-p2p correction: y[:, t] += sum_{j > t} taps[j] * halo[:, H + t - j]
  * for t < H = lh - 1, where halo (B, C, H) holds the predecessor's last H steps. */
 HY_API int hy_halo_correction_fwd(const void* halo, void* y, const void* taps,

@@ -35,6 +35,9 @@ SIGNATURES = {
     "hy_se_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_fft_conv_workspace_size": (_SZ, [_I, _I, _I, _I, _I, _I]),
     "hy_fft_conv_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
+    "hy_fft_spectrum_size": (_SZ, [_I, _I, _I]),
+    "hy_fft_spectrum": (_I, [_P, _I, _I, _I, _P, _P, _SZ, _P]),
+    "hy_fft_conv_spec_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P]),
     "hy_halo_correction_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_debug_two_stage_trace": (_I, [_P, _I]),
     "hy_li_mixer_fwd": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),

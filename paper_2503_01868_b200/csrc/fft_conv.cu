@@ -22,8 +22,10 @@
 // double precision. Workspace: the table, the spectra of one channel block's groups and
 // the transforms of one block of rows (hy_fft_conv_workspace_size).
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "internal.h"
 
 namespace hy {
 namespace fft {
@@ -327,6 +329,10 @@ int run(const void* q, const void* k, const void* v, void* y, const float* taps,
   float2* tw = reinterpret_cast<float2*>(base + ly.tw);
   float2* Hf = reinterpret_cast<float2*>(base + ly.hf);
   float2* X = reinterpret_cast<float2*>(base + ly.x);
+  if (fft_fast_supported(pl.N) && !getenv("HY_FFT_RADIX4")) {
+    const int dt = sizeof(T) == 4 ? HY_F32 : HY_BF16;
+    return fft_fast_run(q, k, v, y, taps, B, C, L, lh, gs, dt, pl.N, ROW_BLOCK, tw, Hf, X, st);
+  }
   twiddle_kernel<<<(pl.N + 255) / 256, 256, 0, st>>>(tw, pl.N);
   // widest column block that fits: N1 x COLS <= 8192 points, COLS <= N2
   if (pl.N1 <= 128 && pl.N2 >= 64) return run_cols<T, 64>(q, k, v, y, taps, B, C, L, lh, gs, pl, tw, Hf, X, st);
@@ -366,4 +372,48 @@ extern "C" HY_API int hy_fft_conv_fwd(const void* q, const void* k, const void* 
   const float* h = static_cast<const float*>(taps);
   if (dtype == HY_F32) return fft::run<float>(q, k, v, y, h, B, C, L, lh, gs, ws, st);
   return fft::run<__nv_bfloat16>(q, k, v, y, h, B, C, L, lh, gs, ws, st);
+}
+
+// ---------------------------------------------------------------- cached filter spectra
+// (register four-step path: 2^14 <= N <= 2^18). The spectrum of each group's zero-padded taps
+// is a parameter transform: computed once per filter bank, read by every later call.
+
+extern "C" HY_API size_t hy_fft_spectrum_size(int G, int L, int lh) {
+  if (G < 1 || L < 1 || lh < 1 || lh > L) return 0;
+  const fft::Plan pl = fft::make_plan(L, lh);
+  if (!fft_fast_supported(pl.N)) return 0;
+  return static_cast<size_t>(G) * pl.N * 8;
+}
+
+extern "C" HY_API int hy_fft_spectrum(const void* taps, int G, int L, int lh, void* spec, void* ws, size_t ws_bytes,
+                                      void* stream) {
+  if (!taps || !spec) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (G < 1 || L < 1 || lh < 1) return fail(HY_ERR_INVALID, "sizes must be >= 1 (G=%d L=%d lh=%d)", G, L, lh);
+  if (lh > L) return fail(HY_ERR_INVALID, "filter length %d exceeds the sequence length %d", lh, L);
+  const fft::Plan pl = fft::make_plan(L, lh);
+  if (!fft_fast_supported(pl.N))
+    return fail(HY_ERR_UNSUPPORTED, "cached FFT spectra need 2^14 <= N <= 2^18, got N = %d", pl.N);
+  const size_t need = static_cast<size_t>(pl.N / 64 + 64) * 8;
+  if (!ws || ws_bytes < need) return fail(HY_ERR_INVALID, "workspace %zu bytes, need %zu", ws_bytes, need);
+  return fft_fast_spectrum(static_cast<const float*>(taps), G, lh, pl.N, spec, ws, stream);
+}
+
+extern "C" HY_API int hy_fft_conv_spec_fwd(const void* q, const void* k, const void* v, void* y, const void* spec,
+                                           int B, int C, int L, int lh, int gs, int dtype, void* ws,
+                                           size_t ws_bytes, void* stream) {
+  if (!v || !y || !spec) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (B < 1 || C < 1 || L < 1 || lh < 1 || gs < 1)
+    return fail(HY_ERR_INVALID, "sizes must be >= 1 (B=%d C=%d L=%d lh=%d gs=%d)", B, C, L, lh, gs);
+  if (C % gs != 0) return fail(HY_ERR_INVALID, "group_size %d does not divide channel count %d", gs, C);
+  if (lh > L) return fail(HY_ERR_INVALID, "filter length %d exceeds the sequence length %d", lh, L);
+  if (dtype != HY_F32 && dtype != HY_BF16)
+    return fail(HY_ERR_UNSUPPORTED, "hy_fft_conv_spec_fwd: fp32 / bf16 activations");
+  const fft::Plan pl = fft::make_plan(L, lh);
+  if (!fft_fast_supported(pl.N))
+    return fail(HY_ERR_UNSUPPORTED, "cached FFT spectra need 2^14 <= N <= 2^18, got N = %d", pl.N);
+  const fft::Layout ly = fft::ws_layout(pl, C, gs);
+  if (!ws || ws_bytes < ly.total) return fail(HY_ERR_INVALID, "workspace %zu bytes, need %zu", ws_bytes, ly.total);
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  return fft_fast_conv_spec(q, k, v, y, spec, B, C, L, gs, dtype, pl.N, fft::ROW_BLOCK, base + ly.tw, base + ly.x,
+                            stream);
 }

@@ -5,4 +5,11 @@ namespace hy {
 int mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const void* feat_pack, const void* hist,
                  int lhf, const float* taps_hat, const float* decay, int lh, int gs, int B, int C, int L,
                  void* stream);
+// register-blocked four-step FFT conv (fft_fast.cu) for 2^14 <= N <= 2^18
+bool fft_fast_supported(int N);
+int fft_fast_run(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L,
+                 int lh, int gs, int dtype, int N, int row_block, void* tw, void* hf, void* x, void* stream);
+int fft_fast_spectrum(const float* taps, int G, int lh, int N, void* spec, void* tw, void* stream);
+int fft_fast_conv_spec(const void* q, const void* k, const void* v, void* y, const void* spec, int B, int C, int L,
+                       int gs, int dtype, int N, int row_block, void* tw, void* x, void* stream);
 }  // namespace hy

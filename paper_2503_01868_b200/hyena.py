@@ -215,7 +215,12 @@ class HyenaOperator:
         feats = ops.causal_conv(proj, self.feat_taps.reshape(3 * D, self.lhf), 1)
         q, k, v = (feats[:, i * D:(i + 1) * D].contiguous() for i in range(3))
         if self.lh > 129 or self.cfg.variant == "LI":
-            return ops.long_conv(v, self.materialized_inner, self.gs, q=q, k=k)
+            if self.dtype != torch.float64 and getattr(self, "_spec_L", None) != L:
+                # the filter half of the FFT conv is a parameter transform: once per length
+                self._spec = ops.fft_spectrum(self.materialized_inner, L)
+                self._spec_L = L
+            return ops.long_conv(v, self.materialized_inner, self.gs, q=q, k=k,
+                                 spectrum=self._spec if self.dtype != torch.float64 else None)
         return ops.gated_conv(v, self.materialized_inner, self.gs, q=q, k=k)
 
     def forward(self, x: torch.Tensor, events=None) -> torch.Tensor:

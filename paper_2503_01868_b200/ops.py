@@ -181,28 +181,69 @@ def halo_correction(halo: torch.Tensor, y: torch.Tensor, taps: torch.Tensor, gro
                "halo_correction")
 
 
-def fft_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None) -> torch.Tensor:
-    """y = q * (h conv (k * v)) through the FFT kernel (fft.py:128-145, hyena.py:183-186)."""
+class FFTSpectrum:
+    """Cached spectra of a filter bank's zero-padded taps (hy_fft_spectrum): `data` is a
+    (G, N, 2) float32 device tensor in the register four-step path's own order, valid for
+    sequence length L and filter length lh."""
+
+    def __init__(self, data: torch.Tensor, L: int, lh: int):
+        self.data, self.L, self.lh = data, L, lh
+
+
+def fft_spectrum(taps: torch.Tensor, L: int):
+    """Spectra of (G, lh) taps for sequences of length L, or None where the cached path does not
+    cover N = next_pow2(L + lh - 1) (2^14 <= N <= 2^18)."""
+    if not taps.is_cuda:
+        raise ValueError("paper_2503_01868_b200 ops need CUDA tensors (there is no CPU path)")
+    taps = taps.to(torch.float32).contiguous()
+    G, lh = taps.shape
+    lib = _lib.load()
+    nbytes = int(lib.hy_fft_spectrum_size(G, L, lh))
+    if nbytes == 0:
+        return None
+    spec = torch.empty((nbytes // 4,), dtype=torch.float32, device=taps.device).view(G, -1, 2)
+    ws_bytes = int(lib.hy_fft_conv_workspace_size(1, G, L, lh, 1, _lib.HY_F32))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=taps.device)
+    _lib.check(lib.hy_fft_spectrum(taps.data_ptr(), G, L, lh, spec.data_ptr(), ws.data_ptr(), ws_bytes, _stream()),
+               "fft_spectrum")
+    return FFTSpectrum(spec, L, lh)
+
+
+def fft_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None,
+             spectrum: FFTSpectrum | None = None) -> torch.Tensor:
+    """y = q * (h conv (k * v)) through the FFT kernel (fft.py:128-145, hyena.py:183-186);
+    `spectrum` (from fft_spectrum(taps, L)) skips the filter transform."""
     squeeze = v.dim() == 2
     v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
     _check_device(v3, q3, k3)
-    taps = _taps(taps, v3)
     B, C, L = v3.shape
-    lh = taps.shape[-1]
     lib = _lib.load()
     code = _dtype_code(v3)
+    y = torch.empty_like(v3)
+    if spectrum is not None:
+        if spectrum.L != L:
+            raise ValueError(f"spectrum computed for L={spectrum.L}, input has L={L}")
+        lh = spectrum.lh
+        ws_bytes = lib.hy_fft_conv_workspace_size(B, C, L, lh, group_size, code)
+        ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=v3.device)
+        _lib.check(lib.hy_fft_conv_spec_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), spectrum.data.data_ptr(),
+                                            B, C, L, lh, group_size, code, ws.data_ptr(), int(ws_bytes), _stream()),
+                   "fft_conv")
+        return y[0] if squeeze else y
+    taps = _taps(taps, v3)
+    lh = taps.shape[-1]
     ws_bytes = lib.hy_fft_conv_workspace_size(B, C, L, lh, group_size, code)
     ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=v3.device)
-    y = torch.empty_like(v3)
     _lib.check(lib.hy_fft_conv_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), taps.data_ptr(), B, C, L,
                                    lh, group_size, code, ws.data_ptr(), int(ws_bytes), _stream()), "fft_conv")
     return y[0] if squeeze else y
 
 
-def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None) -> torch.Tensor:
+def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None,
+              spectrum: FFTSpectrum | None = None) -> torch.Tensor:
     """Gated causal conv for long filters: the FFT kernel where it covers the case, else the FIR kernel."""
     try:
-        return fft_conv(v, taps, group_size, q=q, k=k)
+        return fft_conv(v, taps, group_size, q=q, k=k, spectrum=spectrum)
     except NotImplementedError:
         return gated_conv(v, taps, group_size, q=q, k=k)
 

@@ -110,8 +110,12 @@ def main():
         for L, dt in ((131072, torch.bfloat16), (16384, torch.float32)):
             v = torch.randn((1, D, L), device=dev, dtype=dt, generator=g)
             taps = torch.randn((D, L), device=dev, generator=g) / 100
-            ms = timeit(lambda: ops.fft_conv(v, taps, 1, q=v, k=v), iters=3, warmup=1)
-            report("fft_conv", ms, 4 * D * L * v.element_size(), D=D, L=L, dtype=str(dt))
+            for path in ("register", "radix4"):
+                if path == "radix4":
+                    os.environ["HY_FFT_RADIX4"] = "1"
+                ms = timeit(lambda: ops.fft_conv(v, taps, 1, q=v, k=v), iters=3, warmup=1)
+                os.environ.pop("HY_FFT_RADIX4", None)
+                report("fft_conv_" + path, ms, 4 * D * L * v.element_size(), D=D, L=L, dtype=str(dt))
             del v, taps
 
 

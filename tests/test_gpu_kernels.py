@@ -330,6 +330,10 @@ def test_li_conv_segmented_equals_natural():
     ("f32", 1, 2, 20000, 20000, 1, False),     # N = 65536: N1 = 16 column transforms
     ("f32", 1, 2, 5, 3, 1, True),              # tiny: N padded to 16
     ("bf16", 1, 3, 16384, 16384, 1, True),
+    # register four-step path (fft_fast.cu): N = 8192 * N1 for N1 = 2 .. 32
+    ("f32", 2, 4, 9000, 100, 2, True),          # N = 16384, N1 = 2, groups, batch
+    ("bf16", 1, 2, 70000, 5000, 1, True),       # N = 131072, N1 = 16, lh < L
+    ("f32", 1, 2, 131072, 131072, 1, True),     # N = 262144, N1 = 32 (config C3 size)
 ])
 def test_fft_conv_vs_oracle(dtype, B, C, L, lh, gs, gated):
     # fp32 complex FFT conv (fft.py:128-145 semantics: zero-padded, truncated to L) vs the
@@ -382,3 +386,26 @@ def test_featurize_fwd_with_history(dtype):
     for cut in (2048, 1000, 256):
         u2, fq2 = ops.featurize(pd[..., cut:].contiguous(), dev(feat), rhist=pd[..., cut - 8:cut].contiguous())
         assert torch.equal(u2, u[..., cut:]) and torch.equal(fq2, fq[..., cut:]), cut
+
+
+@pytest.mark.parametrize("dtype,B,C,L,lh,gs", [
+    ("f32", 2, 4, 12000, 9000, 2),
+    ("bf16", 1, 3, 131072, 131072, 1),
+])
+def test_fft_conv_cached_spectrum(dtype, B, C, L, lh, gs):
+    """hy_fft_spectrum once + hy_fft_conv_spec_fwd (the filter transform as a parameter
+    transform) against the float64 oracle; sizes outside 2^14 <= N <= 2^18 report None."""
+    rng = np.random.default_rng(L + 7)
+    G = C // gs
+    taps = rng.standard_normal((G, lh)) / np.sqrt(lh)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: a.astype(np.float32).astype(np.float64))
+    v, q, k = (rnd(rng.standard_normal((B, C, L))) for _ in range(3))
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    spec = ops.fft_spectrum(dev(taps), L)
+    assert spec is not None
+    y = ops.fft_conv(dev(v, tdt), None, gs, q=dev(q, tdt), k=dev(k, tdt), spectrum=spec).double().cpu().numpy()
+    per_ch = np.repeat(taps, gs, axis=0)
+    for b in range(B):
+        want = oracle.fft_conv(v[b] * k[b], per_ch) * q[b]
+        assert oracle.rel_err(y[b], want) < TOL[dtype], b
+    assert ops.fft_spectrum(dev(taps[:, :100]), 4000) is None  # N = 8192: not cached
