@@ -34,20 +34,23 @@ def split3(a: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     return a0, a1, a2
 
 
-def matmul_split3(a_parts, b_parts, out: torch.Tensor | None = None) -> torch.Tensor:
-    """fp32 A @ B from split3 parts: A (M, K), B (K, N) or batched (Bt, K, N) with shared A."""
+def matmul_split3(a_parts, b_parts, out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """fp32 A @ B from split3 parts: A (M, K), B (K, N) or batched (Bt, K, N) with shared A.
+    accumulate: out += A @ B (out must be given)."""
     a0 = a_parts[0]
     b0 = b_parts[0]
+    if accumulate and out is None:
+        raise ValueError("accumulate needs out")
     if b0.dim() == 3:
         Bt, _, N = b0.shape
         if out is None:
             out = torch.empty((Bt, a0.shape[0], N), dtype=torch.float32, device=a0.device)
         for i in range(Bt):
-            matmul_split3(a_parts, tuple(p[i] for p in b_parts), out=out[i])
+            matmul_split3(a_parts, tuple(p[i] for p in b_parts), out=out[i], accumulate=accumulate)
         return out
     if out is None:
         out = torch.empty((a0.shape[0], b0.shape[1]), dtype=torch.float32, device=a0.device)
-    first = True
+    first = not accumulate
     for i, j in _PAIRS:
         if first:
             torch.mm(a_parts[i], b_parts[j], out_dtype=torch.float32, out=out)

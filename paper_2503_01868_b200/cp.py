@@ -647,12 +647,14 @@ class HyenaCP:
         comp.wait_stream(comm)
         return mixed
 
-    def forward(self, x_local: torch.Tensor, events=None) -> torch.Tensor:
-        """events: optional (start, end) CUDA events recorded around the mixer / local conv."""
+    def forward(self, x_local: torch.Tensor, events=None, accumulate_into: torch.Tensor | None = None) -> torch.Tensor:
+        """events: optional (start, end) CUDA events recorded around the mixer / local conv.
+        accumulate_into: caller-owned tensor the output is added into in the out-projection
+        GEMM epilogue (residual stacks; see HyenaOperator.forward)."""
         from . import _lib, ops
         op, grp = self.op, self.grp
         if grp.n_ranks == 1:  # one rank: the whole sequence is local, the fused operator applies
-            return op.forward(x_local, events=events)
+            return op.forward(x_local, events=events, accumulate_into=accumulate_into)
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
         B, D, m = x3.shape
         if self._fused() and m >= _lib.MIXER_HISTORY:
@@ -708,7 +710,10 @@ class HyenaCP:
                                            conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
                                            correct=lambda h, y: _correct(h, y, taps, op.gs))
             mixed = q * conv
-        y = op.out_project(mixed)
+        acc = None
+        if accumulate_into is not None:
+            acc = accumulate_into.unsqueeze(0) if x_local.dim() == 2 else accumulate_into
+        y = op.out_project(mixed, acc)
         return y[0] if x_local.dim() == 2 else y
 
     __call__ = forward
@@ -769,9 +774,11 @@ class LayoutCP:
 
     def forward(self, x_local: torch.Tensor) -> torch.Tensor:
         cur = x_local
-        for layer in self.layers:
-            out = layer.forward(cur)
-            cur = cur + out if self.residual else out
+        for i, layer in enumerate(self.layers):
+            if self.residual:  # residual add fused into the out-projection GEMM epilogue
+                cur = layer.forward(cur, accumulate_into=cur.clone() if i == 0 else cur)
+            else:
+                cur = layer.forward(cur)
         return cur
 
     __call__ = forward

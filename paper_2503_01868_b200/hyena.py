@@ -223,8 +223,11 @@ class HyenaOperator:
                                  spectrum=self._spec if self.dtype != torch.float64 else None)
         return ops.gated_conv(v, self.materialized_inner, self.gs, q=q, k=k)
 
-    def forward(self, x: torch.Tensor, events=None) -> torch.Tensor:
-        """events: optional (start, end) CUDA events recorded around the mixer kernel."""
+    def forward(self, x: torch.Tensor, events=None, accumulate_into: torch.Tensor | None = None) -> torch.Tensor:
+        """events: optional (start, end) CUDA events recorded around the mixer kernel.
+        accumulate_into: a caller-owned tensor of the output's shape (e.g. x itself in a residual
+        stack); the result is added into it in the out-projection GEMM's epilogue (beta = 1) and
+        it is returned — the residual add costs no separate pass."""
         squeeze = x.dim() == 2
         x3 = x.unsqueeze(0) if squeeze else x
         if x3.shape[1] != self.cfg.width:
@@ -240,7 +243,12 @@ class HyenaOperator:
         mixed = self.mixer(proj)
         if events is not None:
             events[1].record()
-        y = self.out_project(mixed)
+        acc = None
+        if accumulate_into is not None:
+            if tuple(accumulate_into.shape) != tuple(x.shape) or accumulate_into.dtype != self.dtype:
+                raise ValueError("accumulate_into must match the output's shape and dtype")
+            acc = accumulate_into.unsqueeze(0) if squeeze else accumulate_into
+        y = self.out_project(mixed, acc)
         return y[0] if squeeze else y
 
     def project(self, x3: torch.Tensor) -> torch.Tensor:
@@ -249,11 +257,18 @@ class HyenaOperator:
             return blas.matmul_split3(self.w_qkv_parts, blas.split3(x3))
         return torch.matmul(self.w_qkv_t, x3)
 
-    def out_project(self, mixed: torch.Tensor) -> torch.Tensor:
-        """y = W_out^T mixed (hyena.py:188)."""
+    def out_project(self, mixed: torch.Tensor, acc: torch.Tensor | None = None) -> torch.Tensor:
+        """y = W_out^T mixed (hyena.py:188); with acc: acc += W_out^T mixed in the GEMM epilogue
+        (the residual of hyena.py:405), returned."""
         if self.split3:
-            return blas.matmul_split3(self.w_out_parts, blas.split3(mixed))
-        return torch.matmul(self.w_out_t, mixed)
+            return blas.matmul_split3(self.w_out_parts, blas.split3(mixed), out=acc, accumulate=acc is not None)
+        if acc is None:
+            return torch.matmul(self.w_out_t, mixed)
+        if acc.shape[0] == 1:
+            acc[0].addmm_(self.w_out_t, mixed[0])
+        else:
+            acc.baddbmm_(self.w_out_t.expand(acc.shape[0], -1, -1), mixed)
+        return acc
 
     __call__ = forward
 
@@ -380,11 +395,16 @@ def build_layout(spec: LayoutSpec, residual: bool = False) -> OperatorStack:
 
 
 def layout_forward_device(x: torch.Tensor, stack: OperatorStack) -> torch.Tensor:
-    """Torch-native stack forward: activations stay on the device between layers."""
+    """Torch-native stack forward: activations stay on the device between layers. The residual
+    add (hyena.py:405) is fused into each layer's out-projection GEMM (beta = 1) on a buffer the
+    stack owns; the caller's x is never written."""
     cur = x
-    for cfg in stack.layers:
-        out = operator_for(cfg, x.dtype).forward(cur)
-        cur = cur + out if stack.residual else out
+    for i, cfg in enumerate(stack.layers):
+        op = operator_for(cfg, x.dtype)
+        if stack.residual:
+            cur = op.forward(cur, accumulate_into=cur.clone() if i == 0 else cur)
+        else:
+            cur = op.forward(cur)
     return cur
 
 

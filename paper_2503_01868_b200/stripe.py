@@ -55,8 +55,11 @@ class Stripe:
     def forward(self, x: torch.Tensor, events=None) -> torch.Tensor:
         cur = x
         for i, op in enumerate(self.ops):
-            out = op.forward(cur, events=None if events is None else events[i])
-            cur = cur + out if self.residual else out
+            ev = None if events is None else events[i]
+            if self.residual:  # residual add in the out-projection GEMM epilogue
+                cur = op.forward(cur, events=ev, accumulate_into=cur.clone() if i == 0 else cur)
+            else:
+                cur = op.forward(cur, events=ev)
         out = self.mha(cur)
         return cur + out if self.residual else out
 

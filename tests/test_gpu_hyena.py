@@ -169,3 +169,21 @@ def test_se_operator_fp32_full_width_parity():
                    "filters": [("explicit", f.taps) for f in g.filters]}
     want = oracle.hyena_forward(x, ocfg)
     assert oracle.rel_err(y, want) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_residual_fused_into_out_projection(dtype):
+    """accumulate_into: the residual add in the out-projection GEMM epilogue (beta = 1) equals
+    the separate add, for B = 1 (addmm) and B = 2 (batched), bf16 and split-bf16 fp32."""
+    for B in (1, 2):
+        cfg = hy.make_hyena_config("MR", 64, hy.make_rng(3), inner_len=128, block_size=128)
+        op = hy.HyenaOperator(cfg, dtype)
+        g = torch.Generator(device="cuda").manual_seed(B)
+        x = torch.randn((B, 64, 4096), device="cuda", generator=g).to(dtype)
+        want = (x.float() + op.forward(x).float())
+        acc = x.clone()
+        got = op.forward(x, accumulate_into=acc)
+        assert got.data_ptr() == acc.data_ptr()
+        tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+        err = float((got.float() - want).abs().max() / max(1.0, float(want.abs().max())))
+        assert err < tol, (B, err)
