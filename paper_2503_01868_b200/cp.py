@@ -57,14 +57,21 @@ class CPGroup:
         self.max_resident[rank] = max(self.max_resident.get(rank, 0), samples)
 
     def peer(self, kind: str, shape, dtype):
+        """The shared peer exchanger, or None when the ranks cannot map each other's memory
+        (then the callers use NCCL; every rank reaches the same answer)."""
         key = (kind, tuple(shape), dtype)
         if key not in self.peers:
             from . import p2p
-            if kind == "halo":
-                self.peers[key] = p2p.PeerHalo(self.group, shape, dtype)
-            else:  # the LI all-to-all: a scatter and a return exchanger
-                self.peers[key] = (p2p.PeerAllToAll(self.group, shape, dtype),
-                                   p2p.PeerAllToAll(self.group, shape, dtype))
+            try:
+                if kind == "halo":
+                    self.peers[key] = p2p.PeerHalo(self.group, shape, dtype)
+                else:  # the LI all-to-all: a scatter and a return exchanger
+                    self.peers[key] = (p2p.PeerAllToAll(self.group, shape, dtype),
+                                       p2p.PeerAllToAll(self.group, shape, dtype))
+            except p2p.PeerUnavailable as e:
+                import warnings
+                warnings.warn(f"peer-memory transfers unavailable, using NCCL: {e}")
+                self.peers[key] = None
         return self.peers[key]
 
     def __post_init__(self):

@@ -57,6 +57,10 @@ class _RawArray:
         return torch.as_tensor(self, device="cuda")
 
 
+class PeerUnavailable(RuntimeError):
+    """Raised on every rank when some rank cannot map its peers' buffers."""
+
+
 class _Symmetric:
     """`nslots` data slots of `slot` bytes plus `nflags` 32-bit flags per rank, cudaMalloc'd
     and mapped into every peer of `group` by CUDA IPC (lazy peer access over NVLink)."""
@@ -79,14 +83,23 @@ class _Symmetric:
         allh = [None] * self.n
         dist.all_gather_object(allh, mine, group=group)
         self.peer_data, self.peer_flags = [0] * self.n, [0] * self.n
-        for p in range(self.n):
-            if p == self.r:
-                self.peer_data[p], self.peer_flags[p] = self.data, self.flags
-                continue
-            hd, hf = _rt.cudaIpcMemHandle_t(), _rt.cudaIpcMemHandle_t()
-            hd.reserved, hf.reserved = allh[p][0], allh[p][1]
-            self.peer_data[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hd, _rt.cudaIpcMemLazyEnablePeerAccess)))
-            self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
+        err = None
+        try:
+            for p in range(self.n):
+                if p == self.r:
+                    self.peer_data[p], self.peer_flags[p] = self.data, self.flags
+                    continue
+                hd, hf = _rt.cudaIpcMemHandle_t(), _rt.cudaIpcMemHandle_t()
+                hd.reserved, hf.reserved = allh[p][0], allh[p][1]
+                self.peer_data[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hd, _rt.cudaIpcMemLazyEnablePeerAccess)))
+                self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
+        except RuntimeError as e:  # e.g. no IPC between these processes
+            err = e
+        # every rank learns whether every rank mapped its peers (no rank may wait alone)
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise PeerUnavailable(f"peer mapping failed on some rank ({err or 'another rank'})")
         self.use = [0] * nslots
         self.step = 0
 
