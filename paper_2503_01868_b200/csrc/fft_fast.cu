@@ -36,7 +36,7 @@ constexpr int M = 8192;  // row length
 constexpr int ROW_THREADS = 256;
 constexpr int COL_THREADS = 128;
 constexpr int PHYS = M + M / 16;  // padded shared row
-constexpr int ROW_SMEM = (PHYS + 128 + 64) * 8;
+constexpr int ROW_SMEM = (PHYS + 128 + 32) * 8;
 
 // cos / sin of 2 pi e / 32 (compile-time twiddles of the register DFTs)
 __host__ __device__ constexpr float w32c(int e) {
@@ -135,9 +135,18 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
   for (int i = 0; i < R; ++i) v[i] = t[i];
 }
 
-// W_N^e from the global two-level table: hi[m] = W_N^(64 m), lo[l] = W_N^l.
-__device__ __forceinline__ float2 tw_n(const float2* __restrict__ hi, const float2* __restrict__ lo, int e) {
-  return cmul(__ldg(hi + (e >> 6)), __ldg(lo + (e & 63)));
+// exp(-2 pi i l / n) for 0 <= l < 64 and n >= 8192 (angle < 0.05): Taylor terms to x^5 are
+// exact to fp32 rounding, so the fine factor of a twiddle costs FMAs, not a table read.
+__device__ __forceinline__ float2 w_fine(int l, float step) {
+  const float x = static_cast<float>(l) * step, x2 = x * x;
+  const float c = fmaf(x2, fmaf(x2, 1.f / 24.f, -0.5f), 1.f);
+  const float s = x * fmaf(x2, fmaf(x2, 1.f / 120.f, -1.f / 6.f), 1.f);
+  return make_float2(c, -s);
+}
+
+// W_N^e = hi[e >> 6] * fine(e & 63): hi[m] = W_N^(64 m) from the global table (double precision).
+__device__ __forceinline__ float2 tw_n(const float2* __restrict__ hi, int e, float step) {
+  return cmul(__ldg(hi + (e >> 6)), w_fine(e & 63, step));
 }
 
 __global__ void table_kernel(float2* hi, float2* lo, int N) {
@@ -153,40 +162,86 @@ __global__ void table_kernel(float2* hi, float2* lo, int N) {
 template <typename T>
 __device__ __forceinline__ float ldf(const T* p) { return Elem<T>::to_a(*p); }
 
-// Column pass: row r (blockIdx.y) of a block; FILTER: group g0 + r's taps (length lh), else
-// k * v of activation row row0 + r (length L). Output row k1 of r's N-point workspace row.
+// Column pass: a CTA covers COL_THREADS consecutive columns n2 of one row r (blockIdx.y);
+// FILTER: group g0 + r's taps (length lh), else k * v of activation row row0 + r (length L).
+// The N1 x COL_THREADS input tile is staged through shared memory — with 16-byte streaming
+// loads when rows are 16-byte aligned (L a multiple of the vector width) — then every thread
+// transforms its column in registers and stores row k1 of r's N-point workspace row.
 template <typename T, int N1, bool FILTER>
 __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, const float2* __restrict__ hi,
                                                        const float2* __restrict__ lo, const T* __restrict__ k,
                                                        const T* __restrict__ v, const float* __restrict__ taps,
                                                        int row0, int g0, int L, int lh, int N) {
-  const int n2 = blockIdx.x * COL_THREADS + threadIdx.x;
+  constexpr int VEC = Elem<T>::VEC, VPR = COL_THREADS / VEC;
+  __shared__ __align__(16) float tile[N1 * COL_THREADS];
+  const int n2_0 = blockIdx.x * COL_THREADS, tid = threadIdx.x, n2 = n2_0 + tid;
   const int r = blockIdx.y;
+  (void)lo;
+  if (!FILTER && L % VEC == 0) {
+    const size_t rowoff = static_cast<size_t>(row0 + r) * L;
+    for (int i = tid; i < N1 * VPR; i += COL_THREADS) {
+      const int n1 = i / VPR, jv = i % VPR;
+      const int t = n1 * M + n2_0 + jv * VEC;
+      float val[VEC];
+      if (t < L) {
+        unpack16<T>(ld_stream16(v + rowoff + t), val);
+        if (k) {
+          float kk[VEC];
+          unpack16<T>(ld_stream16(k + rowoff + t), kk);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) val[e] *= kk[e];
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) val[e] = 0.f;
+      }
+      float4* dst = reinterpret_cast<float4*>(tile + n1 * COL_THREADS + jv * VEC);
+#pragma unroll
+      for (int e = 0; e < VEC / 4; ++e) dst[e] = make_float4(val[4 * e], val[4 * e + 1], val[4 * e + 2], val[4 * e + 3]);
+    }
+  } else if (FILTER && lh % 4 == 0) {  // fp32 taps rows 16-byte aligned
+    const float* trow = taps + static_cast<size_t>(g0 + r) * lh;
+    for (int i = tid; i < N1 * (COL_THREADS / 4); i += COL_THREADS) {
+      const int n1 = i / (COL_THREADS / 4), jv = i % (COL_THREADS / 4);
+      const int t = n1 * M + n2_0 + jv * 4;
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < lh) f = __ldg(reinterpret_cast<const float4*>(trow + t));
+      *reinterpret_cast<float4*>(tile + n1 * COL_THREADS + jv * 4) = f;
+    }
+  } else {
+    for (int i = tid; i < N1 * COL_THREADS; i += COL_THREADS) {
+      const int t = (i / COL_THREADS) * M + n2_0 + i % COL_THREADS;
+      float val = 0.f;
+      if (FILTER) {
+        if (t < lh) val = taps[static_cast<size_t>(g0 + r) * lh + t];
+      } else if (t < L) {
+        const size_t off = static_cast<size_t>(row0 + r) * L + t;
+        val = ldf(v + off);
+        if (k) val *= ldf(k + off);
+      }
+      tile[i] = val;
+    }
+  }
+  __syncthreads();
   float2 x[N1];
 #pragma unroll
-  for (int n1 = 0; n1 < N1; ++n1) {
-    const int t = n1 * M + n2;
-    float val = 0.f;
-    if (FILTER) {
-      if (t < lh) val = taps[static_cast<size_t>(g0 + r) * lh + t];
-    } else if (t < L) {
-      const size_t off = static_cast<size_t>(row0 + r) * L + t;
-      val = ldf(v + off);
-      if (k) val *= ldf(k + off);
-    }
-    x[n1] = make_float2(val, 0.f);
-  }
+  for (int n1 = 0; n1 < N1; ++n1) x[n1] = make_float2(tile[n1 * COL_THREADS + tid], 0.f);
   dft<N1, false>(x);
+  const float step_n = 6.283185307179586f / static_cast<float>(N);
   float2* out = X + static_cast<size_t>(r) * N + n2;
 #pragma unroll
-  for (int k1 = 0; k1 < N1; ++k1) out[static_cast<size_t>(k1) * M] = cmul(x[k1], tw_n(hi, lo, (n2 * k1) & (N - 1)));
+  for (int k1 = 0; k1 < N1; ++k1)
+    out[static_cast<size_t>(k1) * M] = k1 ? cmul(x[k1], tw_n(hi, (n2 * k1) & (N - 1), step_n)) : x[k1];
 }
 
-// Inverse column pass: inverse DFT over k1, then y = q * Re(x) / N for t < L.
+// Inverse column pass: inverse DFT over k1, then y = q * Re(x) / N for t < L, the output tile
+// staged through shared memory for 16-byte stores (and gate loads) where rows are aligned.
 template <typename T, int N1>
 __global__ void __launch_bounds__(COL_THREADS) col_inv(const float2* __restrict__ X, const T* __restrict__ q,
                                                        T* __restrict__ y, int row0, int L, int N) {
-  const int n2 = blockIdx.x * COL_THREADS + threadIdx.x;
+  constexpr int VEC = Elem<T>::VEC, VPR = COL_THREADS / VEC;
+  __shared__ __align__(16) float tile[N1 * COL_THREADS];
+  const int n2_0 = blockIdx.x * COL_THREADS, tid = threadIdx.x, n2 = n2_0 + tid;
   const int r = blockIdx.y;
   const float2* in = X + static_cast<size_t>(r) * N + n2;
   float2 x[N1];
@@ -195,20 +250,47 @@ __global__ void __launch_bounds__(COL_THREADS) col_inv(const float2* __restrict_
   dft<N1, true>(x);
   const float scale = 1.f / static_cast<float>(N);
 #pragma unroll
-  for (int n1 = 0; n1 < N1; ++n1) {
-    const int t = n1 * M + n2;
-    if (t < L) {
-      const size_t off = static_cast<size_t>(row0 + r) * L + t;
-      float val = x[n1].x * scale;
-      if (q) val *= ldf(q + off);
-      y[off] = Elem<T>::from_a(val);
+  for (int n1 = 0; n1 < N1; ++n1) tile[n1 * COL_THREADS + tid] = x[n1].x * scale;
+  __syncthreads();
+  const size_t rowoff = static_cast<size_t>(row0 + r) * L;
+  if (L % VEC == 0) {
+    for (int i = tid; i < N1 * VPR; i += COL_THREADS) {
+      const int n1 = i / VPR, jv = i % VPR;
+      const int t = n1 * M + n2_0 + jv * VEC;
+      if (t >= L) continue;
+      float val[VEC];
+      const float4* src = reinterpret_cast<const float4*>(tile + n1 * COL_THREADS + jv * VEC);
+#pragma unroll
+      for (int e = 0; e < VEC / 4; ++e) {
+        const float4 f = src[e];
+        val[4 * e] = f.x;
+        val[4 * e + 1] = f.y;
+        val[4 * e + 2] = f.z;
+        val[4 * e + 3] = f.w;
+      }
+      if (q) {
+        float qq[VEC];
+        unpack16<T>(ld_stream16(q + rowoff + t), qq);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) val[e] *= qq[e];
+      }
+      st_stream16(y + rowoff + t, pack16<T>(val));
+    }
+  } else {
+    for (int i = tid; i < N1 * COL_THREADS; i += COL_THREADS) {
+      const int t = (i / COL_THREADS) * M + n2_0 + i % COL_THREADS;
+      if (t >= L) continue;
+      float val = tile[i];
+      if (q) val *= ldf(q + rowoff + t);
+      y[rowoff + t] = Elem<T>::from_a(val);
     }
   }
 }
 
-// shared-memory twiddle W_M^e (two-level: rhi[m] = W_M^(64 m), rlo[l] = W_M^l)
-__device__ __forceinline__ float2 tw_m(const float2* rhi, const float2* rlo, int e) {
-  return cmul(rhi[(e >> 6) & 127], rlo[e & 63]);
+// W_M^e: coarse factor rhi[m] = W_M^(64 m) from shared memory, fine factor by polynomial
+constexpr float STEP_M = 6.283185307179586f / M;
+__device__ __forceinline__ float2 tw_m(const float2* rhi, int e) {
+  return cmul(rhi[(e >> 6) & 127], w_fine(e & 63, STEP_M));
 }
 
 // Row pass over row k1 = blockIdx.x of block row r = blockIdx.y (X + r N + k1 M).
@@ -222,15 +304,22 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
   extern __shared__ float2 sm[];
   float2* xs = sm;
   float2* rhi = sm + PHYS;
-  float2* rlo = rhi + 128;
   const int k1 = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
-  if (tid < 192) {
-    const int e = tid < 128 ? 64 * tid : tid - 128;
+  float2* rk1 = rhi + 128;  // [32] W_N^(256 a k1)
+  if (tid < 128) {
     double s, c;
-    sincospi(-2.0 * static_cast<double>(e) / static_cast<double>(M), &s, &c);
-    (tid < 128 ? rhi[tid] : rlo[tid - 128]) = make_float2(static_cast<float>(c), static_cast<float>(s));
+    sincospi(-2.0 * static_cast<double>(64 * tid) / static_cast<double>(M), &s, &c);
+    rhi[tid] = make_float2(static_cast<float>(c), static_cast<float>(s));
+  } else if (tid < 160) {
+    const long long e = (256LL * (tid - 128) * k1) % N;
+    double s, c;
+    sincospi(-2.0 * static_cast<double>(e) / static_cast<double>(N), &s, &c);
+    rk1[tid - 128] = make_float2(static_cast<float>(c), static_cast<float>(s));
   }
   float2* row = X + static_cast<size_t>(r) * N + static_cast<size_t>(k1) * M;
+  const float step_n = 6.283185307179586f / static_cast<float>(N);
+  (void)lo;
+  const float2 w0 = FILTER ? make_float2(1.f, 0.f) : tw_n(hi, (tid * k1) & (N - 1), step_n);
   float2 v32[32];
   // A: DIF radix 32 over span M (group j = tid: x[j + 256 a]) straight from HBM
 #pragma unroll
@@ -238,10 +327,10 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
   __syncthreads();  // twiddle tables
   dft<32, false>(v32);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) xs[phys(tid + 256 * c)] = c ? cmul(v32[c], tw_m(rhi, rlo, tid * c)) : v32[c];
+  for (int c = 0; c < 32; ++c) xs[phys(tid + 256 * c)] = c ? cmul(v32[c], tw_m(rhi, tid * c)) : v32[c];
   __syncthreads();
   // B: DIF radix 16 over span 256 (group (blk, j): x[256 blk + j + 16 a]), twiddle W_256^(j c)
-#pragma unroll
+#pragma unroll 1
   for (int gg = 0; gg < 2; ++gg) {
     const int g = tid + gg * ROW_THREADS, j = g & 15, base = (g >> 4) * 256;
     float2 v[16];
@@ -249,7 +338,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
     for (int a = 0; a < 16; ++a) v[a] = xs[phys(base + j + 16 * a)];
     dft<16, false>(v);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) xs[phys(base + j + 16 * c)] = c ? cmul(v[c], tw_m(rhi, rlo, 32 * j * c)) : v[c];
+    for (int c = 0; c < 16; ++c) xs[phys(base + j + 16 * c)] = c ? cmul(v[c], tw_m(rhi, 32 * j * c)) : v[c];
   }
   __syncthreads();
   // C: DIF radix 16 over span 16 -> spectrum at logical index 16 g + c; then (conv) the
@@ -259,17 +348,16 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
     const int grp = (c0 + r) / gs - g0;
     hrow = Hf + static_cast<size_t>(grp) * N + static_cast<size_t>(k1) * M;
   }
-#pragma unroll
+#pragma unroll 1
   for (int gg = 0; gg < 2; ++gg) {
     const int g = tid + gg * ROW_THREADS;
     float2 v[16];
 #pragma unroll
     for (int a = 0; a < 16; ++a) v[a] = xs[phys(16 * g + a)];
     dft<16, false>(v);
-    if (FILTER) {
-      float4* dst = reinterpret_cast<float4*>(row + 16 * g);
+    if (FILTER) {  // back to shared memory; stored coalesced below
 #pragma unroll
-      for (int c = 0; c < 16; c += 2) dst[c / 2] = make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y);
+      for (int c = 0; c < 16; ++c) xs[phys(16 * g + c)] = v[c];
     } else {
       const float4* h4 = reinterpret_cast<const float4*>(hrow + 16 * g);
 #pragma unroll
@@ -283,17 +371,21 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
       for (int a = 0; a < 16; ++a) xs[phys(16 * g + a)] = v[a];
     }
   }
-  if (FILTER) return;
   __syncthreads();
+  if (FILTER) {  // the spectrum row in logical order, coalesced
+#pragma unroll 4
+    for (int i = tid; i < M; i += ROW_THREADS) row[i] = xs[phys(i)];
+    return;
+  }
   // D: DIT radix 16 over span 256: conj twiddle, inverse DFT
-#pragma unroll
+#pragma unroll 1
   for (int gg = 0; gg < 2; ++gg) {
     const int g = tid + gg * ROW_THREADS, j = g & 15, base = (g >> 4) * 256;
     float2 v[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const float2 x = xs[phys(base + j + 16 * c)];
-      v[c] = c ? cmulc(x, tw_m(rhi, rlo, 32 * j * c)) : x;
+      v[c] = c ? cmulc(x, tw_m(rhi, 32 * j * c)) : x;
     }
     dft<16, true>(v);
 #pragma unroll
@@ -304,13 +396,14 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const float2 x = xs[phys(tid + 256 * c)];
-    v32[c] = c ? cmulc(x, tw_m(rhi, rlo, tid * c)) : x;
+    v32[c] = c ? cmulc(x, tw_m(rhi, tid * c)) : x;
   }
   dft<32, true>(v32);
 #pragma unroll
   for (int a = 0; a < 32; ++a) {
     const int n2 = tid + 256 * a;
-    row[n2] = k1 ? cmulc(v32[a], tw_n(hi, lo, (n2 * k1) & (N - 1))) : v32[a];
+    // W_N^(n2 k1) = W_N^(tid k1) * W_N^(256 a k1): per-thread factor times a per-CTA table
+    row[n2] = k1 ? cmulc(v32[a], cmul(w0, rk1[a])) : v32[a];
   }
 }
 
