@@ -1,3 +1,4 @@
+#include <cstdlib>
 // CUDA-core causal FIR kernels (sm_100a):
 //   * causal_conv_kernel  — direct_causal_conv / gated two-stage semantics for any
 //     filter length (core.py:212-226, blockconv.py:182-220), fp32 / bf16 / fp64.
@@ -14,6 +15,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "internal.h"
 
 namespace hy {
 
@@ -266,6 +268,9 @@ int hy_gated_conv_fwd(const void* q, const void* k, const void* v, void* y, cons
                       int C, int L, int lh, int gs, int dtype, void* stream) {
   int s = check_common(v, y, taps, B, C, L, lh, gs, dtype);
   if (s != HY_OK) return s;
+  if (fir_stream_eligible(q, k, v, y, lh, L, dtype) && !getenv("HY_FIR_TILED") &&
+      static_cast<long long>(B) * C * ((L + 255) / 256) < 0x7fffffffLL)
+    return fir_stream_fwd(q, k, v, y, static_cast<const float*>(taps), B, C, L, lh, gs, dtype, stream);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (dtype) {
     case HY_F32: return launch_conv_gates<float>(q, k, v, y, taps, B, C, L, lh, gs, st);

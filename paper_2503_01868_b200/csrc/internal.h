@@ -12,4 +12,8 @@ int fft_fast_run(const void* q, const void* k, const void* v, void* y, const flo
 int fft_fast_spectrum(const float* taps, int G, int lh, int N, void* spec, void* tw, void* stream);
 int fft_fast_conv_spec(const void* q, const void* k, const void* v, void* y, const void* spec, int B, int C, int L,
                        int gs, int dtype, int N, int row_block, void* tw, void* x, void* stream);
+// kernel F as a TMA-fed chunk stream (mixer.cu) for lh <= 8 on 16-byte aligned rows
+bool fir_stream_eligible(const void* q, const void* k, const void* v, const void* y, int lh, int L, int dtype);
+int fir_stream_fwd(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L,
+                   int lh, int gs, int dtype, void* stream);
 }  // namespace hy

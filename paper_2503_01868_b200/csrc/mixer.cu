@@ -624,6 +624,169 @@ static int launch_se_dispatch(const void* proj, void* y, const float* ft, int lh
   return launch_se<T, 16, 16>(proj, y, ft, lhf, it, dec, lh, gs, B, C, L, st);
 }
 
+// fir_stream_kernel: y = [q *] (h conv ([k *] v)) for filters of <= 8 taps on 16-byte
+// aligned rows (kernel F: direct_causal_conv / the featurizer, core.py:212-226, and the short
+// gated two-stage conv). The se_stream_kernel scheme on one (or, gated, three) staged rows:
+// warps own contiguous ranges of 256-step chunks (row-major over rows), chunks arrive by 1-D
+// bulk copies into a per-warp ring, lane l holds steps [8l, 8l + 8) and takes its FIR history
+// from lane l - 1 by a rotation shuffle and, for lane 0, from the previous ring stage; packed
+// fp32 FMAs. Every byte is read once and written once.
+constexpr int kFsWarps = 8;
+constexpr int kFsStages = 4;
+
+template <typename T, int NJ, bool GK, bool GQ>
+__global__ void __launch_bounds__(kFsWarps * 32, 2)
+fir_stream_kernel(const T* __restrict__ q, const T* __restrict__ kk, const T* __restrict__ v, T* __restrict__ y,
+                  const float* __restrict__ taps, int lh, int gs, int C, int rows, int L) {
+  using namespace sm100;
+  constexpr int NR = 1 + (GK ? 1 : 0) + (GQ ? 1 : 0);  // staged rows: v [, k] [, q]
+  extern __shared__ __align__(128) unsigned char fs_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* ring = reinterpret_cast<T*>(fs_smem + warp * (kFsStages * NR * kSsChunk * static_cast<int>(sizeof(T))));
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(fs_smem + kFsWarps * kFsStages * NR * kSsChunk * static_cast<int>(sizeof(T))) +
+      warp * kFsStages;
+  const int nch = (L + kSsChunk - 1) / kSsChunk;
+  const long long total = static_cast<long long>(rows) * nch;
+  const long long gw = static_cast<long long>(blockIdx.x) * kFsWarps + warp;
+  const long long nw = static_cast<long long>(gridDim.x) * kFsWarps;
+  const int i0 = static_cast<int>(total * gw / nw), i1 = static_cast<int>(total * (gw + 1) / nw);
+  if (i0 >= i1) return;
+  if (lane == 0) {
+    for (int s = 0; s < kFsStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const bool warm = (i0 % nch) != 0;  // starts mid-row: first load the 16 steps before i0
+  const int n_issue = (i1 - i0) + (warm ? 1 : 0);
+  const int base = i0 - (warm ? 1 : 0);
+  int iss_row = base / nch, iss_k = base % nch, iss_st = 0, n_iss = 0;
+  auto issue = [&]() {
+    int t0 = iss_k * kSsChunk, cnt = min(kSsChunk, L - t0), off = 0;
+    if (warm && n_iss == 0) off = kSsChunk - 16, t0 += kSsChunk - 16, cnt = 16;
+    T* dst = ring + iss_st * NR * kSsChunk + off;
+    const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(T));
+    const size_t src = static_cast<size_t>(iss_row) * L + t0;
+    fence_proxy_async();  // the stage's earlier generic reads before the async refill
+    mbar_arrive_expect_tx(&bars[iss_st], NR * bytes);
+    bulk_g2s(dst, v + src, bytes, &bars[iss_st]);
+    if (GK) bulk_g2s(dst + kSsChunk, kk + src, bytes, &bars[iss_st]);
+    if (GQ) bulk_g2s(dst + (NR - 1) * kSsChunk, q + src, bytes, &bars[iss_st]);
+    if (++iss_k == nch) iss_k = 0, ++iss_row;
+    if (++iss_st == kFsStages) iss_st = 0;
+    ++n_iss;
+  };
+  if (lane == 0)
+    while (n_iss < kFsStages - 1 && n_iss < n_issue) issue();
+  float h[NJ];
+  int cur_row = -1;
+  int row = base / nch, k = base % nch;
+  int st = 0, prv_st = kFsStages - 1;
+  uint32_t parity = 0;
+  for (int n = 0; n < n_issue; ++n) {
+    if (row != cur_row) {
+      cur_row = row;
+      const int g = (row % C) / gs;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) h[j] = j < lh ? __ldg(taps + static_cast<size_t>(g) * lh + j) : 0.f;
+    }
+    mbar_wait(&bars[st], parity);
+    const T* cur = ring + st * NR * kSsChunk;
+    const T* prv = ring + prv_st * NR * kSsChunk;
+    float x[8], px[8], rq[8];
+    lds8<T>(x, cur + 8 * lane);
+    lds8<T>(px, prv + kSsChunk - 8);
+    if (GK) {
+      float xk[8], pk[8];
+      lds8<T>(xk, cur + kSsChunk + 8 * lane);
+      lds8<T>(pk, prv + 2 * kSsChunk - 8);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] *= xk[e], px[e] *= pk[e];
+    }
+    if (GQ) lds8<T>(rq, cur + (NR - 1) * kSsChunk + 8 * lane);
+    __syncwarp();
+    if (lane == 0 && n_iss < n_issue) issue();
+    const bool row_start = (k == 0);
+    const int t = k * kSsChunk + 8 * lane;
+    const int out_row = row;
+    prv_st = st;
+    if (++st == kFsStages) st = 0, parity ^= 1u;
+    if (++k == nch) k = 0, ++row;
+    if (row_start) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) px[e] = 0.f;
+    }
+    float hist[8], o[8];
+    hist_shfl<NJ - 1>(hist, x, px, lane);
+    fir_pairs<NJ>(o, x, hist, h);
+    if (GQ) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] *= rq[e];
+    }
+    if (!(warm && n == 0) && t < L) {
+      T* yp = y + static_cast<size_t>(out_row) * L + t;
+      if constexpr (sizeof(T) == 4) {
+        st_stream16(yp, pack16<T>(o));
+        st_stream16(yp + 4, pack16<T>(o + 4));
+      } else {
+        st_stream16(yp, pack16<T>(o));
+      }
+    }
+  }
+}
+
+template <typename T, int NJ, bool GK, bool GQ>
+static int launch_fir_stream_t(const void* q, const void* k, const void* v, void* y, const float* taps, int lh,
+                               int gs, int C, int rows, int L, cudaStream_t st) {
+  auto kern = fir_stream_kernel<T, NJ, GK, GQ>;
+  constexpr int NR = 1 + (GK ? 1 : 0) + (GQ ? 1 : 0);
+  constexpr int SMEM = kFsWarps * kFsStages * (NR * kSsChunk * static_cast<int>(sizeof(T)) + 8);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFsWarps * 32, SMEM);
+  const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * rows;
+  if (total > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many chunks");
+  long long grid = (total + kFsWarps - 1) / kFsWarps;
+  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (grid > cap) grid = cap;
+  kern<<<static_cast<int>(grid), kFsWarps * 32, SMEM, st>>>(static_cast<const T*>(q), static_cast<const T*>(k),
+                                                           static_cast<const T*>(v), static_cast<T*>(y), taps, lh, gs,
+                                                           C, rows, L);
+  return check_launch("fir_stream_kernel");
+}
+
+template <typename T, int NJ>
+static int launch_fir_stream_g(const void* q, const void* k, const void* v, void* y, const float* taps, int lh,
+                               int gs, int C, int rows, int L, cudaStream_t st) {
+  if (q && k) return launch_fir_stream_t<T, NJ, true, true>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+  if (k) return launch_fir_stream_t<T, NJ, true, false>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+  if (q) return launch_fir_stream_t<T, NJ, false, true>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+  return launch_fir_stream_t<T, NJ, false, false>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+}
+
+bool fir_stream_eligible(const void* q, const void* k, const void* v, const void* y, int lh, int L, int dtype) {
+  return (dtype == HY_F32 || dtype == HY_BF16) && lh <= 8 && L % 8 == 0 && aligned16(v) && aligned16(y) &&
+         (!q || aligned16(q)) && (!k || aligned16(k));
+}
+
+int fir_stream_fwd(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L,
+                   int lh, int gs, int dtype, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rows = B * C;
+  if (dtype == HY_F32)
+    return lh == 7 ? launch_fir_stream_g<float, 7>(q, k, v, y, taps, lh, gs, C, rows, L, st)
+                   : launch_fir_stream_g<float, 8>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+  return lh == 7 ? launch_fir_stream_g<__nv_bfloat16, 7>(q, k, v, y, taps, lh, gs, C, rows, L, st)
+                 : launch_fir_stream_g<__nv_bfloat16, 8>(q, k, v, y, taps, lh, gs, C, rows, L, st);
+}
+
 }  // namespace hy
 
 using namespace hy;

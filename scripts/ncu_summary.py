@@ -54,11 +54,13 @@ def summarize_rep(rep: str, dst: str, workload: str | None = None) -> None:
     m = raw_metrics(rep)
     lines = [f"ncu --set full capture: {os.path.basename(rep)}", f"kernel: {m.pop('kernel')}", ""]
     lines += [f"{k:85s} {v}" for k, v in m.items()]
-    rd = float(m["dram__bytes_read.sum"].split()[0].replace(",", ""))
-    wr = float(m["dram__bytes_write.sum"].split()[0].replace(",", ""))
-    unit = m["dram__bytes_read.sum"].split()[1]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-    traffic = (rd + wr) * scale
+    scales = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def nbytes(key):  # each metric carries its own unit
+        val, unit = m[key].split()[:2]
+        return float(val.replace(",", "")) * scales[unit]
+
+    traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
     lines += ["", f"traffic (dram read + write) per launch: {traffic:.0f} bytes"]
     open(dst, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))

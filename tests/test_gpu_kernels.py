@@ -409,3 +409,41 @@ def test_fft_conv_cached_spectrum(dtype, B, C, L, lh, gs):
         want = oracle.fft_conv(v[b] * k[b], per_ch) * q[b]
         assert oracle.rel_err(y[b], want) < TOL[dtype], b
     assert ops.fft_spectrum(dev(taps[:, :100]), 4000) is None  # N = 8192: not cached
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("B,C,L,lh,gs,gates", [
+    (1, 3, 8, 7, 1, ""),            # one partial chunk
+    (2, 5, 264, 7, 1, ""),          # a full chunk + a partial one
+    (3, 64, 4096, 7, 2, ""),        # many warps start mid-row (warm-up chunk)
+    (1, 300, 2048, 5, 3, "kq"),     # gated, groups
+    (2, 7, 1000, 8, 1, "k"),        # ungated output gate only on k
+    (1, 9, 520, 3, 1, "q"),
+])
+def test_fir_stream_vs_oracle(dtype, B, C, L, lh, gs, gates):
+    """Kernel F as a TMA-fed chunk stream (lh <= 8, L % 8 == 0): y = [q *] conv([k *] v)
+    against the float64 oracle, and equal to the tiled kernel (HY_FIR_TILED) within rounding."""
+    import os
+    rng = np.random.default_rng(L * 7 + lh)
+    G = C // gs
+    taps = rng.standard_normal((G, lh)) / np.sqrt(lh)
+    rnd = bf16_round if dtype == "bf16" else (lambda a: a.astype(np.float32).astype(np.float64))
+    v = rnd(rng.standard_normal((B, C, L)))
+    k = rnd(rng.standard_normal((B, C, L))) if "k" in gates else None
+    q = rnd(rng.standard_normal((B, C, L))) if "q" in gates else None
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    args = dict(q=None if q is None else dev(q, tdt), k=None if k is None else dev(k, tdt))
+    y = ops.gated_conv(dev(v, tdt), dev(taps), gs, **args)
+    per_ch = np.repeat(taps, gs, axis=0)
+    yn = y.double().cpu().numpy()
+    for b in range(B):
+        u = v[b] * (k[b] if k is not None else 1.0)
+        want = oracle.direct_causal_conv(u, explicit_bank_from_taps(per_ch, 1)) * (q[b] if q is not None else 1.0)
+        assert oracle.rel_err(yn[b], want) < TOL[dtype], b
+    os.environ["HY_FIR_TILED"] = "1"
+    try:
+        y2 = ops.gated_conv(dev(v, tdt), dev(taps), gs, **args)
+    finally:
+        os.environ.pop("HY_FIR_TILED")
+    assert float((y.double() - y2.double()).abs().max()) <= (2e-2 if dtype == "bf16" else 1e-5) * max(
+        1.0, float(y2.double().abs().max()))
