@@ -242,6 +242,8 @@ def fft_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k
 def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, k=None,
               spectrum: FFTSpectrum | None = None) -> torch.Tensor:
     """Gated causal conv for long filters: the FFT kernel where it covers the case, else the FIR kernel."""
+    if spectrum is None and taps.shape[-1] > v.shape[-1]:
+        taps = taps[..., : v.shape[-1]].contiguous()  # lags >= L never reach the L outputs
     try:
         return fft_conv(v, taps, group_size, q=q, k=k, spectrum=spectrum)
     except NotImplementedError:
