@@ -5,7 +5,26 @@ C-ABI of include/hyena_b200.h; there is no CPU fallback.
 """
 
 from . import cp, fft
-from .cp import CPGroup, LayoutCP, ShardedSeq, a2a_conv, a2a_conv_pipelined, gather, layout_forward_cp, p2p_conv, p2p_conv_overlapped, shard
+from . import cp as cpsim  # the reference's module name; schemes take this rank's shard + a CPGroup
+from .cp import (
+    CPGroup,
+    LayoutCP,
+    ShardedSeq,
+    a2a_conv,
+    a2a_conv_backward,
+    a2a_conv_pipelined,
+    a2a_conv_saved,
+    gather,
+    layout_forward_cp,
+    p2p_conv,
+    p2p_conv_overlapped,
+    p2p_fft_causal_wrapper,
+    p2p_fft_conv,
+    p2p_fft_forward,
+    p2p_fft_inverse,
+    shard,
+)
+from .fft import bit_reversal, circular_conv_oracle, dft_oracle, dif_split, dit_merge, idft_oracle
 from .backward import (
     DeviceGrads,
     HyenaGrads,
