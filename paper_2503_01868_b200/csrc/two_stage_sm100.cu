@@ -113,7 +113,7 @@ struct Layout {
   static constexpr int OFF_HP = OFF_FQ + NBUF * NCH * LB * 2;  // padded taps, bf16 [512]
   // implicit (LI) mode: P[m][n] = R_n lam_n^(m+1) (tf32 A operand, 128 x 8), per-chunk mode
   // inputs E[chunk][n], carried states S_prev[chunk][n] (tf32 B operand, [NBUF] x 32 x 8)
-  static constexpr int OFF_P = OFF_HP + 1024;
+  static constexpr int OFF_P = OFF_HP + 2048;  // hpad[2]: the explicit modes prebuild the next group
   static constexpr int OFF_E = OFF_P + 128 * NPOLE * 4;
   static constexpr int OFF_S = OFF_E + NCH * NPOLE * 4;
   // implicit mode: Lam[n][t] = lam_n^(127 - t), the bf16 A operand of the mode-input MMA
@@ -125,7 +125,7 @@ struct Layout {
   static constexpr int OFF_P2 = OFF_UP, OFF_L2 = OFF_UP + 8192;
   static_assert(OFF_L2 % 1024 == 0 && OFF_L2 + 4096 <= OFF_FQ, "implicit factor buffers");
   static constexpr int OFF_BAR = OFF_L + 2048;
-  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 4;
+  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 6;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
   // IMPL factor buffers b = 0 / 1: tfree[b] (MMA warp: last T0 . U / Lam . U of buffer b
   // retired), tfreep[b] (scan warp: last P . S_prev of buffer b retired), tready[b]
   uint64_t* tfreep = eempty + 2;         // [2]
+  // explicit modes: T0 is double-buffered (tready[b] / tfree[b] per T0 buffer), T1 is single
+  uint64_t* t1ready = tfreep + 2;        // [1] T builder -> MMA: T1 of the current group
+  uint64_t* t1free = t1ready + 1;        // [1] MMA commit: last T1 . U_prev of a group retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -299,6 +302,8 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       mbar_init(&eempty[i], 1);
       mbar_init(&tfreep[i], 1);
     }
+    mbar_init(t1ready, 1);
+    mbar_init(t1free, 1);
     fence_mbar_init();
   }
   if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
@@ -502,20 +507,22 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         mbar_wait(&ufull[u], ph);
         mbar_wait(&tempty[u], ph ^ 1);
         if (lane == 0) trace(p, j, 4);
-        if (first) mbar_wait(&tready[0], gi & 1);
+        const int fb = gi & 1;  // T0 buffer of this group (built one group ahead)
+        if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
         const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
         const uint32_t upa = smem_u32(smem + LY::OFF_UP + u * NCH * LB * 2);
+        const uint32_t ta = fb ? tmem_base + TM_T0B : t0a;
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            mma_bf16_ts(d, t0a + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+            mma_bf16_ts(d, ta + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           }
-          if (last) mma_commit(&tfree[0]);
+          if (last) mma_commit(&tfree[fb]);
           if (first) {
-            mbar_wait(&tready[1], gi & 1);
+            mbar_wait(t1ready, gi & 1);
             tc_fence_after();
           }
 #pragma unroll
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
             mma_bf16_ts(d, t1a + ks * 8, desc_sw128(upa + bo), idesc_main, 1u);
           }
-          if (last) mma_commit(&tfree[1]);
+          if (last) mma_commit(t1free);
           mma_commit(&uempty[u]);
           mma_commit(&tfull[u]);
         }
@@ -732,8 +739,8 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-    auto build = [&](int fct, uint32_t tcol, uint64_t* rdy) {
-      const unsigned short* hp = reinterpret_cast<const unsigned short*>(hpad) + 128 + fct * 128 + mrow;
+    auto build = [&](int fct, uint32_t tcol, uint64_t* rdy, const bf16* hbuf) {
+      const unsigned short* hp = reinterpret_cast<const unsigned short*>(hbuf) + 128 + fct * 128 + mrow;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t w[32];
@@ -780,17 +787,39 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
       fence_proxy_async();
       named_bar_sync(BAR_TB, TB_THREADS);
-      build(0, b ? TM_T0B : TM_T0, &tready[b]);
+      build(0, b ? TM_T0B : TM_T0, &tready[b], hpad);
     };
     int gi = 0, g_prev = -1;
     Tile t;
     t.init(tb, p);
     const int g_end = ntiles > 0 ? ((te - 1) / (p.tiles_per_seq * p.B)) / p.gs : -1;  // last group
+    // explicit modes: hpad[b] <- the prefetched group's taps (decay applied), b = group & 1
+    auto fill_hpad = [&](bf16* hb) {
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int tt = bt + r * TB_THREADS - 128;
+        const float h = (tt >= 0 && tt < p.lh) ? pf_h[r] * exp2f(-pf_dec * static_cast<float>(tt)) : 0.f;
+        hb[bt + r * TB_THREADS] = __float2bfloat16_rn(h);
+      }
+      named_bar_sync(BAR_TB, TB_THREADS);
+    };
     if (ntiles > 0) {
-      prefetch(t.c / p.gs);
+      const int g0 = t.c / p.gs;
+      prefetch(g0);
       if (IMPL) {
         build_impl(0);
-        if (t.c / p.gs < g_end) prefetch(t.c / p.gs + 1);
+        if (g0 < g_end) prefetch(g0 + 1);
+      } else {
+        // group 0: T0 (buffer 0) and T1; then group 1's T0 into buffer 1 ahead of time
+        fill_hpad(hpad);
+        build(0, TM_T0, &tready[0], hpad);
+        build(1, TM_T1, t1ready, hpad);
+        if (g0 < g_end) {
+          prefetch(g0 + 1);
+          fill_hpad(hpad + 512);
+          build(0, TM_T0B, &tready[1], hpad + 512);
+          if (g0 + 1 < g_end) prefetch(g0 + 2);
+        }
       }
     }
     for (int j = 0; j < ntiles; ++j, t.next(p)) {
@@ -807,18 +836,21 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         ++gi;
         continue;
       }
-#pragma unroll
-      for (int r = 0; r < PER; ++r) {
-        const int tt = bt + r * TB_THREADS - 128;
-        const float h = (tt >= 0 && tt < p.lh) ? pf_h[r] * exp2f(-pf_dec * static_cast<float>(tt)) : 0.f;
-        hpad[bt + r * TB_THREADS] = __float2bfloat16_rn(h);
+      // group gi starts (gi >= 1; group 0 was built in the prologue): its T0 is already in
+      // buffer gi & 1; T1 (single buffer) waits for the previous group's last T1 . U_prev,
+      // then group gi + 1's T0 is built into the other buffer (its previous user, group
+      // gi - 1, retired long ago) from the taps prefetched during the previous group
+      if (gi > 0) {
+        mbar_wait(t1free, (gi - 1) & 1);
+        build(1, TM_T1, t1ready, hpad + 512 * (gi & 1));
+        if (g < g_end) {
+          const int nb = (gi + 1) & 1;
+          fill_hpad(hpad + 512 * nb);
+          mbar_wait(&tfree[nb], ((gi - 1) >> 1) & 1);
+          build(0, nb ? TM_T0B : TM_T0, &tready[nb], hpad + 512 * nb);
+          if (g + 1 < g_end) prefetch(g + 2);
+        }
       }
-      named_bar_sync(BAR_TB, TB_THREADS);
-      if (gi > 0) mbar_wait(&tfree[0], (gi - 1) & 1);
-      build(0, TM_T0, &tready[0]);
-      if (gi > 0) mbar_wait(&tfree[1], (gi - 1) & 1);
-      build(1, TM_T1, &tready[1]);
-      if (g < g_end) prefetch(g + 1);  // next group's taps load during this group
       ++gi;
     }
   }
