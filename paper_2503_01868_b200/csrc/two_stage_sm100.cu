@@ -771,12 +771,20 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       unsigned char* lrow = smem + LY::OFF_L2 + b * 2048 + (bt >> 6) * 1024 + (bt & 7) * 2;
 #pragma unroll
       for (int n = 0; n < NPOLE; ++n) {
-        const float lt = powf(pf_pole[n], static_cast<float>(bt));
+        // lam^t for integer t = exp2(t log2|lam|) with the sign of lam^t (|lam| <= 1); the
+        // relative error (~t ulp of the exponent) is far below the bf16 / tf32 operands'
+        const float lam = pf_pole[n], la = log2f(fabsf(lam));
+        auto ipow = [&](int e) {
+          if (e == 0) return 1.f;
+          if (lam == 0.f) return 0.f;
+          const float m = exp2f(static_cast<float>(e) * la);
+          return (lam < 0.f && (e & 1)) ? -m : m;
+        };
+        const float lt = ipow(bt);
         hv = fmaf(pf_res[n], lt, hv);
-        pm[n] = pf_res[n] * lt * pf_pole[n];
+        pm[n] = pf_res[n] * lt * lam;
         const int jj = (bt >> 3) & 7;
-        *reinterpret_cast<bf16*>(lrow + n * 128 + ((jj ^ n) << 4)) =
-            __float2bfloat16_rn(powf(pf_pole[n], static_cast<float>(127 - bt)));
+        *reinterpret_cast<bf16*>(lrow + n * 128 + ((jj ^ n) << 4)) = __float2bfloat16_rn(ipow(127 - bt));
       }
       hpad[bt] = __float2bfloat16_rn(0.f);
       hpad[128 + bt] = __float2bfloat16_rn(hv);
