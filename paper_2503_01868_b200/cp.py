@@ -609,6 +609,13 @@ class HyenaCP:
             for q in reqs:
                 q.wait()
         mixed = torch.empty((B, D, m), dtype=x3.dtype, device=x3.device)
+        for r_ in range(n):
+            grp.filter_elements[r_] = self.cfg.inner.n_groups // n * self.cfg.inner.filter_len
+        if peer is not None and os.environ.get("HY_CP_LI_SCHED", "serial") == "serial":
+            self._li_serial(x3, segs, hist, peer, mixed, events)
+            grp.count_rounds("a2a_conv_pipelined", 2 * self.n_pipe * B)
+            hpeer.release(hk)
+            return mixed
         pending = []
         for s, (rows, w, wp, ft, res, poles) in enumerate(segs):
             proj_s = blas.matmul_split3(wp, blas.split3(x3)) if op.split3 else torch.matmul(w, x3)
@@ -646,13 +653,72 @@ class HyenaCP:
                 u_s.record_stream(comm)
                 fq_s.record_stream(comm)
             pending.append(u_s)
-        for r_ in range(n):
-            grp.filter_elements[r_] = self.cfg.inner.n_groups // n * self.cfg.inner.filter_len
         grp.count_rounds("a2a_conv_pipelined", 2 * self.n_pipe * B)
         if hpeer is not None:  # every segment's featurizer stream has read the history
             hpeer.release(hk)
         comp.wait_stream(comm)
         return mixed
+
+    def _li_serial(self, x3, segs, hist, peer, mixed, events=None):
+        """The LI layer as a software pipeline on ONE compute stream, the all-to-all rounds on
+        the copy engines: iteration s runs segment s's projection GEMM and featurizer stream and
+        starts its scatter copies, then segment s-1's slab conv (its scatter landed during
+        GEMM s) and the start of its return copies, then segment s-2's gating (its return
+        landed during GEMM s). No kernel shares the SMs with the GEMMs, and no stream waits on
+        copies issued after it."""
+        from . import ops
+        op, grp = self.op, self.grp
+        n, r = grp.n_ranks, grp.rank
+        B, D, m = x3.shape
+        seg = D // self.n_pipe
+        slab = seg // n
+        live = {}  # s -> (fq_s, scatter slots, return slots)
+
+        def start(s):
+            rows, w, wp, ft, _, _ = segs[s]
+            proj_s = blas.matmul_split3(wp, blas.split3(x3)) if op.split3 else torch.matmul(w, x3)
+            rh = hist.index_select(1, rows).contiguous() if r > 0 else None
+            u_s, fq_s = ops.featurize(proj_s, ft, rhist=rh)
+            ks = []
+            for b in range(B):
+                for src in range(n):  # the reference's accounting: scatter + return rounds
+                    for dst in range(n):
+                        if dst != src:
+                            grp._send("a2a_conv_pipelined", src, dst, 2 * slab * m)
+                k = peer[0].next_slot()
+                peer[0].send(u_s[b].view(n, slab, m), k)
+                ks.append(k)
+            live[s] = (fq_s, ks, [])
+
+        def conv(s):
+            _, _, _, _, res, poles = segs[s]
+            fq_s, ks, kb = live[s]
+            for b in range(B):
+                recv = peer[0].wait(ks[b])
+                if events is not None and s == 0 and b == 0:
+                    events[0].record()
+                y_slab = ops.li_conv_segmented(recv, res, poles, op.gs)
+                if events is not None and s == 0 and b == 0:
+                    events[1].record()
+                peer[0].release(ks[b])
+                k = peer[1].next_slot()
+                peer[1].send(y_slab, k)
+                kb.append(k)
+
+        def gate(s):
+            fq_s, _, kb = live.pop(s)
+            for b in range(B):
+                back = peer[1].wait(kb[b])
+                torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
+                peer[1].release(kb[b])
+
+        for it in range(self.n_pipe + 2):
+            if it < self.n_pipe:
+                start(it)
+            if 1 <= it <= self.n_pipe:
+                conv(it - 1)
+            if it >= 2:
+                gate(it - 2)
 
     def forward(self, x_local: torch.Tensor, events=None, accumulate_into: torch.Tensor | None = None) -> torch.Tensor:
         """events: optional (start, end) CUDA events recorded around the mixer / local conv.

@@ -134,9 +134,10 @@ class PeerAllToAll(_Symmetric):
         """Slot k of this rank's receive buffer as (n, *chunk_shape): [src] = what src sent."""
         return _RawArray(self.data + k * self.slot, (self.n,) + self.chunk_shape, self.dtype).tensor()
 
-    def exchange(self, send: torch.Tensor, k: int) -> torch.Tensor:
-        """send: (n, *chunk_shape) contiguous on this rank, [dst] goes to rank dst. Enqueued on
-        the current stream; returns slot k of the receive buffer (valid on that stream)."""
+    def send(self, send: torch.Tensor, k: int) -> None:
+        """Start the transfer of send (n, *chunk_shape), [dst] to rank dst, into slot k of every
+        rank: copy-engine copies on per-destination side streams after the current stream's
+        work so far; the current stream does not wait for them (see wait)."""
         if tuple(send.shape) != (self.n,) + self.chunk_shape or send.dtype != self.dtype or not send.is_contiguous():
             raise ValueError("send must be a contiguous (n_ranks, *chunk_shape) tensor of the exchange dtype")
         cur = torch.cuda.current_stream()
@@ -145,7 +146,8 @@ class PeerAllToAll(_Symmetric):
         src_base = send.data_ptr()
         ev = torch.cuda.Event()
         ev.record(cur)
-        done = []
+        if not hasattr(self, "_local_done"):
+            self._local_done = [None] * self.nslots
         for d in range(self.n):
             st = self.streams[d]
             st.wait_event(ev)
@@ -156,17 +158,28 @@ class PeerAllToAll(_Symmetric):
             _ck(_rt.cudaMemcpyAsync(dst, src_base + d * self.chunk, self.chunk, _D2D, h))
             if d != self.r:
                 _ck(_cu.cuStreamWriteValue32(h, self._arrive(self.peer_flags[d], k, self.r), u, _WDEF))
-            e = torch.cuda.Event()
-            e.record(st)
-            done.append(e)
-        send.record_stream(cur)
-        for e in done:
-            cur.wait_event(e)
+            else:
+                e = torch.cuda.Event()
+                e.record(st)
+                self._local_done[k] = e
+            send.record_stream(st)  # the allocator keeps send alive until the copy ran
+
+    def wait(self, k: int) -> torch.Tensor:
+        """The current stream waits until every rank's chunk of slot k's current use has
+        landed; returns slot k of the receive buffer as (n, *chunk_shape)."""
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self._local_done[k])
         h = cur.cuda_stream
         for s in range(self.n):
             if s != self.r:
-                _ck(_cu.cuStreamWaitValue32(h, self._arrive(self.flags, k, s), u, _GEQ))
+                _ck(_cu.cuStreamWaitValue32(h, self._arrive(self.flags, k, s), self.use[k], _GEQ))
         return self.recv_tensor(k)
+
+    def exchange(self, send: torch.Tensor, k: int) -> torch.Tensor:
+        """send + wait: enqueued on the current stream; returns slot k of the receive buffer
+        (valid on that stream)."""
+        self.send(send, k)
+        return self.wait(k)
 
     def release(self, k: int) -> None:
         """Enqueue on the current stream (after the last reader of slot k): tell every sender
