@@ -257,9 +257,11 @@ class Runner:
             mod = cp.HyenaCP(build_config(wl), dt)
             self.m = L // ws
             self.fwd = lambda x, ev=None: mod.forward(x, events=None if ev is None else ev[0])
-            # the slab long conv (ungated li_conv): D/ws channels x L tokens, in + out; one rank
-            # runs the fused single-GPU operator (li_mixer: 3 projected rows in, 1 out)
-            self.kernels = [("LI slab conv", "LI", 2 * self.esize * (D // ws) * B * L)] if ws > 1 else \
+            # the slab long conv (ungated li_conv), one launch = one channel segment's slab of one
+            # sequence: D/(ws*n_pipe) channels x L tokens, in + out; one rank runs the fused
+            # single-GPU operator (li_mixer: 3 projected rows in, 1 out)
+            npipe = mod.n_pipe if mod._li_pipelined(self.m) else 1
+            self.kernels = [("LI slab conv", "LI", 2 * self.esize * (D // (ws * npipe)) * L)] if ws > 1 else \
                 [("LI mixer (one rank: fused operator)", "LI", 4 * self.esize * D * B * L)]
             self.parallelism = f"cp{ws} (sequence sharded, all-to-all to channel slabs for the long conv)"
             self.l_global = L
