@@ -73,7 +73,9 @@ HY_API const char* hy_last_error(void);
 
 /* Causal FIR, any filter length:
  *   y[b,c,t] = sum_{j < lh, j <= t} taps[c/gs, j] * x[b,c,t-j]
- * CUDA cores, 128-bit coalesced loads, fp32 accumulation (fp64 for HY_F64). */
+ * CUDA cores, fp32 accumulation (fp64 for HY_F64). lh <= 8 on 16-byte aligned rows
+ * (L % 8 == 0, fp32 / bf16): a TMA-fed chunk stream with warp-shuffle history (every byte
+ * read once); otherwise tiled windows with 128-bit coalesced loads. */
 HY_API int hy_causal_conv_fwd(const void* x, void* y, const void* taps,
                        int B, int C, int L, int lh, int group_size, int dtype, void* stream);
 
