@@ -27,7 +27,7 @@ constexpr int kFbGrad = 256;   // staged g / c / du steps per chunk
 constexpr unsigned kFbFull = 0xffffffffu;
 
 template <typename T>
-constexpr int fb_warps() { return sizeof(T) == 2 ? 8 : 4; }
+constexpr int fb_warps() { return 4; }  // 164 registers: 4-warp CTAs fit 3 per SM (8-warp CTAs only 1)
 template <typename T>
 constexpr int fb_stage_elems() { return 3 * kFbRaw + 3 * kFbGrad; }
 template <typename T>
