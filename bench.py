@@ -169,10 +169,14 @@ def dist_env():
     return ws, rank, local
 
 
+GROUP_SIZE = 1  # the reference default; --group-size 16 is the paper's grouped setting
+
+
 def build_config(wl: dict, variant=None, L=None):
     import paper_2503_01868_b200 as hy
     return hy.make_hyena_config(variant or wl["variant"], wl["D"], hy.make_rng(0), seq_len=L or wl["L"],
-                                group_size=1, inner_len=wl.get("inner_len"), block_size=wl.get("block_size", 16))
+                                group_size=GROUP_SIZE, inner_len=wl.get("inner_len"),
+                                block_size=wl.get("block_size", 16))
 
 
 def _max_over_ranks(ms: float, ws: int) -> float:
@@ -377,7 +381,7 @@ def run_ours(args, wl):
         "dtype": wl["dtype"],
         "data": "synthetic N(0,1) inputs, random-init weights (make_hyena_config seed 0)",
         "config": {"workload": wl["desc"], "global_batch": run.B, "seq_len": run.l_global, "width": run.D,
-                   "group_size": 1, "parallelism": run.parallelism,
+                   "group_size": GROUP_SIZE, "parallelism": run.parallelism,
                    "l2": f"per-step projections ({l2_bytes / 1e6:.0f} MB per rank) larger than L2 (126 MB); "
                          f"no flush" if l2_bytes > 126e6 else "inputs smaller than L2; no flush"},
         "e2e": {"value": run.tokens_step / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s",
@@ -406,7 +410,7 @@ def run_ours(args, wl):
 
 def _oracle_cfg(variant, D, L, inner_len, block_size, backend="blocked"):
     import oracle
-    return oracle.make_hyena_config(variant, D, oracle.make_rng(0), seq_len=L, group_size=1,
+    return oracle.make_hyena_config(variant, D, oracle.make_rng(0), seq_len=L, group_size=GROUP_SIZE,
                                     inner_len=inner_len, block_size=block_size, backend=backend)
 
 
@@ -543,7 +547,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="mr", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--group-size", type=int, default=1, help="filter group size d_g (1 = reference default)")
     args = ap.parse_args()
+    global GROUP_SIZE
+    GROUP_SIZE = args.group_size
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
