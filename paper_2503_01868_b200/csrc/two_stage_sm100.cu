@@ -740,14 +740,23 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     const int mrow = quarter * 32 + lane;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
     auto build = [&](int fct, uint32_t tcol, uint64_t* rdy, const bf16* hbuf) {
-      const unsigned short* hp = reinterpret_cast<const unsigned short*>(hbuf) + 128 + fct * 128 + mrow;
+      // pair c = (hpad[p], hpad[p - 1]) with p = p0 - 2c, from 32-bit words of hpad: for odd
+      // p both halves sit in word p >> 1 (swapped); for even p they straddle words p >> 1 and
+      // p >> 1 - 1. One byte permute with a per-lane selector covers both, and consecutive
+      // columns share a word, so a thread loads 65 words instead of 128 halves.
+      const int p0 = 128 + fct * 128 + mrow;
+      const uint32_t* hw = reinterpret_cast<const uint32_t*>(hbuf);
+      const uint32_t sel = (p0 & 1) ? 0x1032u : 0x7610u;
+      uint32_t wa = hw[p0 >> 1];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t w[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int cc = half * 32 + c;
-          w[c] = static_cast<uint32_t>(hp[-2 * cc]) | (static_cast<uint32_t>(hp[-2 * cc - 1]) << 16);
+          const uint32_t wb = hw[(p0 >> 1) - cc - 1];
+          w[c] = __byte_perm(wa, wb, sel);
+          wa = wb;
         }
         tmem_st_32x32b_x32(trow + tcol + half * 32, w);
       }
