@@ -7,14 +7,15 @@ bits), so
 
     A @ B = sum_{i + j <= 2} Ai @ Bj  + O(2^-24 |A| |B|)
 
-takes six bf16 tensor-core GEMMs with fp32 accumulation (the dropped terms are below fp32
+takes six bf16 tensor-core products with fp32 accumulation (the dropped terms are below fp32
 rounding). The weight splits are made once per operator; the activation split is one
-elementwise pass. Products are accumulated smallest first into one fp32 output (cuBLAS
-beta = 1). Measured on B200 at the C1 projection (M = 12288, K = N = 4096): the error is set by
-the fp32 accumulation inside a long-K tensor-core GEMM (5.0e-6 relative to max with one
-K = 4096 pass), so the leading term A0 @ B0 is accumulated in K chunks of 1024 with fp32 adds
-between them: 1.2e-6, against 3.0e-6 for cuBLAS's CUDA-core fp32 GEMM, at 3.2x its speed
-(1.99 ms vs 6.27 ms).
+elementwise pass. The five small products run as ONE GEMM with the splits concatenated along
+K (Split3.cat, K' = 5K); the leading term A0 @ B0 follows, accumulated into the same fp32
+output (cuBLAS beta = 1). The error is set by the fp32 accumulation inside a long-K
+tensor-core GEMM, so the leading term is accumulated in K chunks with fp32 adds between them.
+Measured on B200 at the C1 projection (M = 12288, K = N = 4096, `scripts/split3_err.py`):
+one K = 4096 pass 5.8e-6 relative to max, chunks of 2048 2.8e-6 (used: 1.73 ms), of 1024
+1.3e-6 (1.85 ms); cuBLAS's CUDA-core fp32 GEMM: 3.0e-6 at 6.27 ms.
 """
 
 from __future__ import annotations
@@ -22,7 +23,26 @@ from __future__ import annotations
 import torch
 
 _PAIRS = ((1, 1), (0, 2), (2, 0), (0, 1), (1, 0))  # smallest terms first; A0 @ B0 last, K-chunked
-_KC = 1024
+_KC = 2048
+
+
+class Split3(tuple):
+    """split3 parts of a weight plus `cat` = [A1 | A0 | A2 | A0 | A1] (M, 5K): the five small
+    products of _PAIRS as ONE bf16 GEMM against [B1; B2; B0; B1; B0] (K' = 5K). Their
+    magnitudes are <= 2^-8 of the result, so the long-K fp32 accumulation error of that GEMM is
+    negligible, and one GEMM replaces five output read-modify-write passes."""
+
+    cat: torch.Tensor
+
+
+def split3_weight(a: torch.Tensor) -> Split3:
+    parts = Split3(split3(a))
+    parts.cat = torch.cat([parts[i] for i, _ in _PAIRS], dim=1).contiguous()
+    return parts
+
+
+def _b_cat(b_parts) -> torch.Tensor:
+    return torch.cat([b_parts[j] for _, j in _PAIRS], dim=-2)
 
 
 def split3(a: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
@@ -50,13 +70,21 @@ def matmul_split3(a_parts, b_parts, out: torch.Tensor | None = None, accumulate:
         return out
     if out is None:
         out = torch.empty((a0.shape[0], b0.shape[1]), dtype=torch.float32, device=a0.device)
-    first = not accumulate
-    for i, j in _PAIRS:
-        if first:
-            torch.mm(a_parts[i], b_parts[j], out_dtype=torch.float32, out=out)
-            first = False
+    cat = getattr(a_parts, "cat", None)
+    if cat is not None:  # the five small products in one GEMM
+        bc = _b_cat(b_parts)
+        if accumulate:
+            torch.addmm(out, cat, bc, out_dtype=torch.float32, out=out)
         else:
-            torch.addmm(out, a_parts[i], b_parts[j], out_dtype=torch.float32, out=out)
+            torch.mm(cat, bc, out_dtype=torch.float32, out=out)
+    else:
+        first = not accumulate
+        for i, j in _PAIRS:
+            if first:
+                torch.mm(a_parts[i], b_parts[j], out_dtype=torch.float32, out=out)
+                first = False
+            else:
+                torch.addmm(out, a_parts[i], b_parts[j], out_dtype=torch.float32, out=out)
     K = a0.shape[1]
     for k0 in range(0, K, _KC):
         torch.addmm(out, a0[:, k0:k0 + _KC], b0[k0:k0 + _KC], out_dtype=torch.float32, out=out)

@@ -564,7 +564,10 @@ class HyenaCP:
         for s in range(self.n_pipe):
             rows = torch.cat([torch.arange(i * D + s * seg, i * D + (s + 1) * seg) for i in range(3)]).to(op.dev)
             w = op.w_qkv_t.index_select(0, rows).contiguous()
-            wp = tuple(p.index_select(0, rows).contiguous() for p in op.w_qkv_parts) if op.split3 else None
+            wp = None
+            if op.split3:
+                wp = blas.Split3(tuple(p.index_select(0, rows).contiguous() for p in op.w_qkv_parts))
+                wp.cat = op.w_qkv_parts.cat.index_select(0, rows).contiguous()
             ft = op.feat_taps[:, s * seg:(s + 1) * seg].contiguous()
             g0 = (s * seg + self.grp.rank * (seg // n)) // op.gs
             ng = (seg // n) // op.gs

@@ -156,8 +156,8 @@ class HyenaOperator:
         # HY_FP32_GEMM=simt keeps cuBLAS's CUDA-core fp32 GEMM
         self.split3 = dtype == torch.float32 and os.environ.get("HY_FP32_GEMM", "split3") == "split3"
         if self.split3:
-            self.w_qkv_parts = blas.split3(self.w_qkv_t)
-            self.w_out_parts = blas.split3(self.w_out_t.contiguous())
+            self.w_qkv_parts = blas.split3_weight(self.w_qkv_t)
+            self.w_out_parts = blas.split3_weight(self.w_out_t.contiguous())
         tdt = ops.tap_dtype(dtype)
         self.lhf = max(cfg.q_feat.filter_len, cfg.k_feat.filter_len, cfg.v_feat.filter_len)
         feat = np.zeros((3, D, self.lhf))
