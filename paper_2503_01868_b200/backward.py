@@ -21,7 +21,7 @@ from typing import Iterator
 import numpy as np
 import torch
 
-from . import ops
+from . import blas, ops
 from .core import ExplicitFilter, GroupSpec, ImplicitFilter, RegularizedFilter, SeqTensor, device
 
 # ---------------------------------------------------------------- reference API
@@ -177,13 +177,20 @@ class DeviceGrads:
     inner: dict
 
 
-def _batched_outer(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+def _batched_outer(a: torch.Tensor, b: torch.Tensor, split3: bool = False) -> torch.Tensor:
     """sum_b a[b] @ b[b]^T for (B, M, L) x (B, N, L): cuBLAS GEMMs accumulating in an fp32 output
     (fp64 for fp64 inputs) across the batch (beta = 1), no separate conversion / add passes."""
     if a.dtype == torch.float64:
         out = torch.matmul(a[0], b[0].transpose(0, 1))
         for i in range(1, a.shape[0]):
             out.addmm_(a[i], b[i].transpose(0, 1))
+        return out
+    if a.dtype == torch.float32 and split3:
+        # fp32 on the bf16 tensor cores (blas.py: exact three-way splits, fp32 accumulation)
+        out = None
+        for i in range(a.shape[0]):
+            out = blas.matmul_split3(blas.split3(a[i]), blas.split3(b[i].transpose(0, 1)), out=out,
+                                     accumulate=i > 0)
         return out
     kw = {} if a.dtype == torch.float32 else {"out_dtype": torch.float32}
     out = torch.mm(a[0], b[0].transpose(0, 1), **kw)
@@ -231,7 +238,16 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             return ops.long_conv(a, op.materialized_inner, op.gs)
         return ops.gated_conv(a, op.materialized_inner, op.gs)
 
-    dmixed = torch.matmul(op.w_out_t.transpose(0, 1), dy3)
+    def wt_mm(name, w_t, rhs):  # W^T-side products: W (= w_t^T) @ rhs, fp32 via split-bf16
+        if not op.split3:
+            return torch.matmul(w_t.transpose(0, 1), rhs)
+        parts = getattr(op, name, None)
+        if parts is None:
+            parts = blas.split3_weight(w_t.transpose(0, 1).contiguous())
+            setattr(op, name, parts)
+        return blas.matmul_split3(parts, blas.split3(rhs))
+
+    dmixed = wt_mm("_w_out_bwd_parts", op.w_out_t, dy3)
     fused = op.dtype != torch.float64 and op.lhf <= 8 and L % 8 == 0
     rev = fused and (modal or ts_ok)  # du runs as the causal tcgen05 conv of the reversed dc
     dc_rev = None
@@ -252,7 +268,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         c = inner_conv(u)
         mixed = q * c
         dc = dmixed * q
-    g_out = _batched_outer(dy3, mixed)
+    g_out = _batched_outer(dy3, mixed, op.split3)
     inner_g = {}
     du_rev = None  # du stored time-reversed (consumed mirrored by the featurizer backward)
     if scan:
@@ -319,7 +335,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         torch.mul(du, v, out=dfeats[:, D:2 * D])                 # dk
         torch.mul(du, k, out=dfeats[:, 2 * D:])                  # dv
         dproj, dfeat = ops.causal_conv_bwd(dfeats, proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
-    g_qkv = _batched_outer(dproj, x3)
-    dx = torch.matmul(op.w_qkv_t.transpose(0, 1), dproj)
+    g_qkv = _batched_outer(dproj, x3, op.split3)
+    dx = wt_mm("_w_qkv_bwd_parts", op.w_qkv_t, dproj)
     grads = DeviceGrads(w_qkv_t=g_qkv, w_out_t=g_out, feat_taps=dfeat.reshape(3, D, op.lhf), inner=inner_g)
     return (dx[0] if squeeze else dx), grads
