@@ -56,18 +56,18 @@ class CPGroup:
     def note_resident(self, rank: int, samples: int) -> None:
         self.max_resident[rank] = max(self.max_resident.get(rank, 0), samples)
 
-    def peer(self, kind: str, shape, dtype):
+    def peer(self, kind: str, shape, dtype, nslots: int = 2):
         """The shared peer exchanger, or None when the ranks cannot map each other's memory
         (then the callers use NCCL; every rank reaches the same answer)."""
-        key = (kind, tuple(shape), dtype)
+        key = (kind, tuple(shape), dtype, nslots)
         if key not in self.peers:
             from . import p2p
             try:
                 if kind == "halo":
                     self.peers[key] = p2p.PeerHalo(self.group, shape, dtype)
                 else:  # the LI all-to-all: a scatter and a return exchanger
-                    self.peers[key] = (p2p.PeerAllToAll(self.group, shape, dtype),
-                                       p2p.PeerAllToAll(self.group, shape, dtype))
+                    self.peers[key] = (p2p.PeerAllToAll(self.group, shape, dtype, nslots),
+                                       p2p.PeerAllToAll(self.group, shape, dtype, nslots))
             except p2p.PeerUnavailable as e:
                 import warnings
                 warnings.warn(f"peer-memory transfers unavailable, using NCCL: {e}")
@@ -598,7 +598,9 @@ class HyenaCP:
         comm = self._comm
         peer = None
         if os.environ.get("HY_CP_P2P", "1") != "0":
-            peer = grp.peer("a2a", (slab, m), x3.dtype)
+            # two segments in flight (scatter of s while s-1 is convolved): 2 B slots, so no
+            # slot is rewritten while a use of it is still being read
+            peer = grp.peer("a2a", (slab, m), x3.dtype, 2 * B)
         tail = op.project(x3[..., m - 8:].contiguous())  # (B, 3D, 8)
         hpeer = self._halo_peer(tail) if peer is not None else None
         if hpeer is not None:
@@ -689,31 +691,29 @@ class HyenaCP:
                         if dst != src:
                             grp._send("a2a_conv_pipelined", src, dst, 2 * slab * m)
                 k = peer[0].next_slot()
-                peer[0].send(u_s[b].view(n, slab, m), k)
-                ks.append(k)
+                ks.append((k, peer[0].send(u_s[b].view(n, slab, m), k)))
             live[s] = (fq_s, ks, [])
 
         def conv(s):
             _, _, _, _, res, poles = segs[s]
             fq_s, ks, kb = live[s]
             for b in range(B):
-                recv = peer[0].wait(ks[b])
+                recv = peer[0].wait(*ks[b])  # this use of the slot (later sends may share it)
                 if events is not None and s == 0 and b == 0:
                     events[0].record()
                 y_slab = ops.li_conv_segmented(recv, res, poles, op.gs)
                 if events is not None and s == 0 and b == 0:
                     events[1].record()
-                peer[0].release(ks[b])
+                peer[0].release(*ks[b])
                 k = peer[1].next_slot()
-                peer[1].send(y_slab, k)
-                kb.append(k)
+                kb.append((k, peer[1].send(y_slab, k)))
 
         def gate(s):
             fq_s, _, kb = live.pop(s)
             for b in range(B):
-                back = peer[1].wait(kb[b])
+                back = peer[1].wait(*kb[b])
                 torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
-                peer[1].release(kb[b])
+                peer[1].release(*kb[b])
 
         for it in range(self.n_pipe + 2):
             if it < self.n_pipe:

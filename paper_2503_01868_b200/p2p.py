@@ -134,10 +134,11 @@ class PeerAllToAll(_Symmetric):
         """Slot k of this rank's receive buffer as (n, *chunk_shape): [src] = what src sent."""
         return _RawArray(self.data + k * self.slot, (self.n,) + self.chunk_shape, self.dtype).tensor()
 
-    def send(self, send: torch.Tensor, k: int) -> None:
+    def send(self, send: torch.Tensor, k: int) -> int:
         """Start the transfer of send (n, *chunk_shape), [dst] to rank dst, into slot k of every
         rank: copy-engine copies on per-destination side streams after the current stream's
-        work so far; the current stream does not wait for them (see wait)."""
+        work so far; the current stream does not wait for them (see wait). Returns the slot's
+        use number, which wait / release take when several uses are in flight."""
         if tuple(send.shape) != (self.n,) + self.chunk_shape or send.dtype != self.dtype or not send.is_contiguous():
             raise ValueError("send must be a contiguous (n_ranks, *chunk_shape) tensor of the exchange dtype")
         cur = torch.cuda.current_stream()
@@ -147,7 +148,7 @@ class PeerAllToAll(_Symmetric):
         ev = torch.cuda.Event()
         ev.record(cur)
         if not hasattr(self, "_local_done"):
-            self._local_done = [None] * self.nslots
+            self._local_done = {}
         for d in range(self.n):
             st = self.streams[d]
             st.wait_event(ev)
@@ -161,18 +162,20 @@ class PeerAllToAll(_Symmetric):
             else:
                 e = torch.cuda.Event()
                 e.record(st)
-                self._local_done[k] = e
+                self._local_done[(k, u)] = e
             send.record_stream(st)  # the allocator keeps send alive until the copy ran
+        return u
 
-    def wait(self, k: int) -> torch.Tensor:
-        """The current stream waits until every rank's chunk of slot k's current use has
-        landed; returns slot k of the receive buffer as (n, *chunk_shape)."""
+    def wait(self, k: int, u: int | None = None) -> torch.Tensor:
+        """The current stream waits until every rank's chunk of use u (default: the latest) of
+        slot k has landed; returns slot k of the receive buffer as (n, *chunk_shape)."""
+        u = self.use[k] if u is None else u
         cur = torch.cuda.current_stream()
-        cur.wait_event(self._local_done[k])
+        cur.wait_event(self._local_done.pop((k, u)))
         h = cur.cuda_stream
         for s in range(self.n):
             if s != self.r:
-                _ck(_cu.cuStreamWaitValue32(h, self._arrive(self.flags, k, s), self.use[k], _GEQ))
+                _ck(_cu.cuStreamWaitValue32(h, self._arrive(self.flags, k, s), u, _GEQ))
         return self.recv_tensor(k)
 
     def exchange(self, send: torch.Tensor, k: int) -> torch.Tensor:
@@ -181,13 +184,14 @@ class PeerAllToAll(_Symmetric):
         self.send(send, k)
         return self.wait(k)
 
-    def release(self, k: int) -> None:
+    def release(self, k: int, u: int | None = None) -> None:
         """Enqueue on the current stream (after the last reader of slot k): tell every sender
-        that this rank is done with slot k's current use."""
+        that this rank is done with use u (default: the latest) of slot k."""
+        u = self.use[k] if u is None else u
         h = torch.cuda.current_stream().cuda_stream
         for s in range(self.n):
             if s != self.r:
-                _ck(_cu.cuStreamWriteValue32(h, self._free(self.peer_flags[s], k, self.r), self.use[k], _WDEF))
+                _ck(_cu.cuStreamWriteValue32(h, self._free(self.peer_flags[s], k, self.r), u, _WDEF))
 
 
 class PeerHalo(_Symmetric):

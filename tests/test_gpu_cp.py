@@ -40,7 +40,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _cp_worker(rank, world, port, variant, q, p2p="1"):
+def _cp_worker(rank, world, port, variant, q, p2p="1", batch=1):
     import torch.distributed as dist
     os.environ["HY_CP_P2P"] = p2p
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -52,7 +52,7 @@ def _cp_worker(rank, world, port, variant, q, p2p="1"):
         kw = {"inner_len": 128, "block_size": 128} if variant == "MR" else {}
         cfg = hy.make_hyena_config(variant, D, hy.make_rng(0), seq_len=L, **kw)
         gen = torch.Generator(device="cuda").manual_seed(7)
-        x = torch.randn((1, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
+        x = torch.randn((batch, D, L), device="cuda", dtype=torch.bfloat16, generator=gen)
         m = L // world
         cpop = hy.cp.HyenaCP(cfg, torch.bfloat16)
         for _ in range(3):  # repeated steps exercise the slot flow control of the peer transfers
@@ -120,6 +120,25 @@ def _a2a_bwd_worker(rank, world, port, q):
             q.put(res)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_hyena_cp_li_batched():
+    """LI CP layer with B = 2: the software pipeline's peer slots cycle through both batch
+    elements of every segment (flow control across segments)."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, "LI", q, "1", 2)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert err < 2e-2, err
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
