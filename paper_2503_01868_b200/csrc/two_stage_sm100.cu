@@ -458,9 +458,8 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
         if (first) ++gi;
         g_prev = g;
-        mbar_wait(&ufull[u], ph);
+        mbar_wait(&ufull[u], ph);  // U written and accumulator u drained (converter)
         if (lane == 0) trace(p, j, 16);
-        mbar_wait(&tempty[u], ph ^ 1);
         if (lane == 0) trace(p, j, 17);
         if (lane == 0) trace(p, j, 4);
         const int fb = gi & 1;  // this group's factor buffer
@@ -504,8 +503,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
         if (first) ++gi;
         g_prev = g;
-        mbar_wait(&ufull[u], ph);
-        mbar_wait(&tempty[u], ph ^ 1);
+        mbar_wait(&ufull[u], ph);  // U written and accumulator u drained (converter)
         if (lane == 0) trace(p, j, 4);
         const int fb = gi & 1;  // T0 buffer of this group (built one group ahead)
         if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
@@ -598,7 +596,12 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       }
       fence_proxy_async();
       named_bar_sync(BAR_CONV, CONV_THREADS);
-      if (ctid == 0) mbar_arrive(&ufull[u]);
+      // ufull also certifies that the accumulator buffer u is free (the epilogue drained
+      // tile it - NBUF): the MMA warp, the pipeline's bottleneck, then waits on one barrier
+      if (ctid == 0) {
+        mbar_wait(&tempty[u], uph ^ 1);
+        mbar_arrive(&ufull[u]);
+      }
       // 3) featurized q -> SMEM for the epilogue (times t0 + 8m .. +7)
       if (GQ) {
         mbar_wait(&qempty[u], uph ^ 1);
