@@ -464,7 +464,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         if (lane == 0) trace(p, j, 4);
         const int fb = gi & 1;  // this group's factor buffer
         if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
-        mbar_wait(&eempty[j & 1], ((j >> 1) & 1) ^ 1);
         if (lane == 0) trace(p, j, 18);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
@@ -600,6 +599,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       // tile it - NBUF): the MMA warp, the pipeline's bottleneck, then waits on one barrier
       if (ctid == 0) {
         mbar_wait(&tempty[u], uph ^ 1);
+        if (IMPL) mbar_wait(&eempty[it & 1], ((it >> 1) & 1) ^ 1);  // E buffer drained by the scan
         mbar_arrive(&ufull[u]);
       }
       // 3) featurized q -> SMEM for the epilogue (times t0 + 8m .. +7)
