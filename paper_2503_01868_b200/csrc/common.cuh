@@ -7,6 +7,9 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 
 #include "../../include/hyena_b200.h"
@@ -67,6 +70,28 @@ __device__ __forceinline__ int4 pack16(const typename Elem<T>::A* in) {
 #pragma unroll
   for (int i = 0; i < Elem<T>::VEC; ++i) e[i] = Elem<T>::from_a(in[i]);
   return raw;
+}
+
+// Resident-CTA grid cap (SMs x CTAs per SM) of `kern` at (threads, smem) on the current device,
+// queried once per key: the attribute + occupancy queries cost host microseconds per launch.
+inline long long resident_cap(const void* kern, int threads, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, long long> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int sms = 148, per_sm = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = cap;
+  return cap;
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

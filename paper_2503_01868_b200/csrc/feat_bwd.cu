@@ -286,14 +286,10 @@ static int launch_fb(const void* proj, const void* g, const void* c, const void*
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM);
+  const long long cap = resident_cap(reinterpret_cast<const void*>(kern), THREADS, SMEM);
   const long long total = static_cast<long long>((L + kFbStep - 1) / kFbStep) * C * B;
   if (total > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many chunks");
   long long grid = (total + fb_warps<T>() - 1) / fb_warps<T>();
-  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   const int n = 3 * C * lhf;
   cudaError_t e = cudaMemsetAsync(ws, 0, static_cast<size_t>(n) * sizeof(double), st);

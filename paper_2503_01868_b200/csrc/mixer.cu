@@ -566,17 +566,13 @@ static int launch_se(const void* proj, void* y, const float* ft, int lhf, const 
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSeThreads, smem);
+  const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kSeThreads, smem);
   constexpr int N2 = NF > NI ? NF : NI;
   constexpr int H = (NF > 8 ? 2 : 1) + (N2 > 8 ? 2 : 1);
   const long long items = static_cast<long long>((L + 8 * (32 - H) - 1) / (8 * (32 - H))) * C * B;
   if (items > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many work items");
   const long long warps_per_cta = kSeThreads / 32;
   long long grid = (items + warps_per_cta - 1) / warps_per_cta;
-  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   kern<<<static_cast<int>(grid), kSeThreads, smem, st>>>(static_cast<const T*>(proj), static_cast<T*>(y), ft, lhf,
                                                         it, dec, lh, gs, B, C, L);
@@ -595,14 +591,10 @@ static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf,
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSsWarps * 32, SMEM);
+  const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kSsWarps * 32, SMEM);
   const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * C * B;
   if (total > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many chunks");
   long long grid = (total + kSsWarps - 1) / kSsWarps;
-  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   kern<<<static_cast<int>(grid), kSsWarps * 32, SMEM, st>>>(static_cast<const T*>(proj), static_cast<T*>(y), ft, lhf,
                                                              it, dec, lh, gs, B, C, L, static_cast<const T*>(gmix),
@@ -747,14 +739,10 @@ static int launch_fir_stream_t(const void* q, const void* k, const void* v, void
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFsWarps * 32, SMEM);
+  const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kFsWarps * 32, SMEM);
   const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * rows;
   if (total > 0x7fffffffLL) return fail(HY_ERR_UNSUPPORTED, "too many chunks");
   long long grid = (total + kFsWarps - 1) / kFsWarps;
-  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   kern<<<static_cast<int>(grid), kFsWarps * 32, SMEM, st>>>(static_cast<const T*>(q), static_cast<const T*>(k),
                                                            static_cast<const T*>(v), static_cast<T*>(y), taps, lh, gs,

@@ -31,6 +31,9 @@ def timeit(fn, iters=20, warmup=5):
         fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # hold the stream ~10 ms so the host enqueues every iteration before the first one starts:
+    # the events then bracket device time, not the per-call host overhead (~tens of us)
+    torch.cuda._sleep(20_000_000)
     s.record()
     for _ in range(iters):
         fn()
