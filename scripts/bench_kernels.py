@@ -86,6 +86,10 @@ def main():
             taps = torch.randn((D, 7), device=dev, generator=g) / 3
             ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, se_only=True))
             report(name, ms, 4 * D * B * L * proj.element_size(), B=B, D=D, L=L)
+            if dt == torch.bfloat16:  # the path the operator takes for bf16 SE: the tcgen05 mixer
+                pk = ops.feat_pack(feat)  # packed featurizer factors, built once per weight set
+                ms = timeit(lambda: ops.hyena_mixer(proj, feat, taps, 1, packed=pk))
+                report("se_mixer_bf16_tcgen05", ms, 4 * D * B * L * proj.element_size(), B=B, D=D, L=L)
             x = proj.reshape(B * 3, D, L)
             ms = timeit(lambda: ops.causal_conv(x, feat.reshape(3 * D, 7), 1))
             report(name.replace("se_mixer", "featurizer"), ms, 2 * x.numel() * x.element_size(), rows=3 * D, L=L)
