@@ -74,31 +74,80 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region
-    (written to a file by nvidia-smi itself, read back after the region)."""
+    """SM clock and clock-event (throttle) reasons sampled every 10 ms during the timed region
+    by a host thread over NVML (the library nvidia-smi reads); falls back to nvidia-smi's own
+    50 ms logging when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    INTERVAL_S = 0.010
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.thread = None
+        self.samples = []
+        self.stop_flag = threading.Event()
+
+    def _nvml_loop(self, nv, h):
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, smax, [n for n, b in bits.items() if r & b]))
+            except Exception:  # noqa: BLE001 - sampling is best effort
+                pass
+            time.sleep(self.INTERVAL_S)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            # NVML enumerates physical GPUs; map through CUDA_VISIBLE_DEVICES when it is set
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[self.gpu].isdigit() else self.gpu
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            time.sleep(0.05)
+            return
+        except Exception:  # noqa: BLE001
+            self.thread = None
+        self._start_smi()
+
+    def stop(self):
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            sm = [s[0] for s in self.samples]
+            reasons = sorted({r for s in self.samples for r in s[2]})
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": max(s[1] for s in self.samples) if sm else None,
+                    "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
+                    "interval_ms": self.INTERVAL_S * 1e3, "source": "NVML"}
+        return self._stop_smi()
+
+    def _start_smi(self):
         import tempfile
         fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
         time.sleep(0.3)
 
-    def stop(self):
+    def _stop_smi(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -128,7 +177,7 @@ class ClockSampler:
                 if val.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "interval_ms": 50, "source": "nvidia-smi"}
 
 
 def operator_roofline(op_tf: float, peaks: dict, dtype: str, flops: int) -> dict:
@@ -174,9 +223,10 @@ GROUP_SIZE = 1  # the reference default; --group-size 16 is the paper's grouped 
 
 def build_config(wl: dict, variant=None, L=None):
     import paper_2503_01868_b200 as hy
-    return hy.make_hyena_config(variant or wl["variant"], wl["D"], hy.make_rng(0), seq_len=L or wl["L"],
+    v = variant or wl["variant"]
+    return hy.make_hyena_config(v, wl["D"], hy.make_rng(0), seq_len=L or wl["L"],
                                 group_size=GROUP_SIZE, inner_len=wl.get("inner_len"),
-                                block_size=wl.get("block_size", 16))
+                                block_size=wl.get("block_size", 16), backend="fft" if v == "LI" else "blocked")
 
 
 def _max_over_ranks(ms: float, ws: int) -> float:
@@ -318,6 +368,13 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
     clocks = sampler.stop()
+    # parity sample: batch element 0 of this rank's input and of one more step's output
+    # (compared with the oracle in the cpu_baseline leg, outside every timed region)
+    parity_io = None
+    if wl["kind"] == "op" and ws == 1:
+        y = run.step()
+        parity_io = (run.x[0].double().cpu().numpy(), y[0].double().cpu().numpy())
+        del y
     ms_step = _max_over_ranks(t0.elapsed_time(t1), ws) / args.steps
     kern_ms = [statistics.mean(evs[i][j][0].elapsed_time(evs[i][j][1]) for i in range(args.steps))
                for j in range(nk)]
@@ -402,7 +459,7 @@ def run_ours(args, wl):
     }
     if dist.is_initialized():
         dist.destroy_process_group()
-    return result, rank
+    return result, rank, parity_io
 
 
 # ---------------------------------------------------------------- CPU legs (oracle: test/baseline only)
@@ -446,34 +503,85 @@ def cpu_seconds_train(variant, D, L, inner_len, block_size, sample_len=512):
                        f"to the reference)"), time.perf_counter() - w0
 
 
-def cpu_seconds_per_element(variant, D, L, inner_len=None, block_size=16, sample_len=2048, f32=False):
-    """(seconds for the oracle's forward of one (D, L) batch element, description, wall seconds
-    actually spent).
+SAMPLE_LEN = {"mr": 8192, "se": 4096, "li": 4096, "stripe": 4096}  # token window of the CPU legs
 
-    SE / MR: every stage is linear in L, so a (D, sample_len) window is timed and scaled.
-    LI: the token-local part (projections, featurizers, gates) is timed on a sample_len
-    window; the long conv (filter materialisation + radix-2 FFT conv, fft.py:128-145) is
-    timed on a few channels at the full L and scaled to D channels."""
+
+def host_info() -> dict:
+    """CPU model, cores and the BLAS thread pool the CPU legs ran with."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": p.get("internal_api"), "threads": p.get("num_threads"), "version": p.get("version")}
+                for p in threadpool_info() if p.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset (OpenBLAS default: all cores)"),
+            "blas_pools": blas}
+
+
+def _bf16_params(ocfg: dict) -> dict:
+    """The oracle config with the parameters the bf16 device path stores in bf16 rounded to bf16
+    (projection weights, featurizer taps); inner taps stay fp64 (the kernels round the decayed
+    taps themselves, part of the measured error)."""
+    import torch
+    r = lambda a: torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).double().numpy()  # noqa: E731
+    out = dict(ocfg)
+    for n in ("w_q", "w_k", "w_v", "w_out"):
+        out[n] = r(ocfg[n])
+    for n in ("q_feat", "k_feat", "v_feat"):
+        b = ocfg[n]
+        out[n] = dict(b, filters=[("explicit", r(f[1])) for f in b["filters"]])
+    return out
+
+
+def cpu_seconds_per_element(variant, D, L, inner_len=None, block_size=16, sample_len=2048, f32=False,
+                            x0=None, y0=None, bf16=False):
+    """(seconds for the oracle's forward of one (D, L) batch element, description, wall seconds
+    actually spent, parity rel_err or None).
+
+    The timed call is oracle.hyena_forward on the first `sample_len` tokens of one batch
+    element. Every layer is causal, so its output is exactly the first `sample_len` columns of
+    the full-length forward: with the device's batch-0 input x0 and output y0 the same call is
+    the parity check (rel_err = ||a-b||_inf / max(||b||_inf, 1), testing.py:57-62).
+    SE / MR: every stage is linear in L, so the window is scaled to L.
+    LI: the window forward (projections, featurizers, gates, FFT long conv at the window's
+    length) is scaled to L, plus the filter materialisation and FFT long conv at the full L
+    on a few channels, scaled to D channels (the long conv is O(L log L) per channel)."""
     import oracle
     rng = oracle.make_rng(1, stream=0)
     n = min(L, sample_len)
     w0 = time.perf_counter()
-    if variant in ("SE", "MR"):
-        cfg = _oracle_cfg(variant, D, L, inner_len, block_size)
+    if x0 is not None:
+        x = np.ascontiguousarray(x0[:, :n], dtype=np.float32 if f32 else np.float64)
+    else:
         x = rng.standard_normal((D, n)).astype(np.float32 if f32 else np.float64)
-        t = _time(lambda: oracle.hyena_forward(x, cfg), 1)
-        return t * L / n, f"oracle.hyena_forward over a ({D}, {n}) token window, scaled x{L / n:g}", \
-            time.perf_counter() - w0
-    cfg = _oracle_cfg("LI", D, n, None, block_size, backend="fft")
-    x = rng.standard_normal((D, n))
-    t_local = _time(lambda: oracle.hyena_forward(x, cfg), 1)
+    backend = "fft" if variant == "LI" else "blocked"
+    cfg = _oracle_cfg(variant, D, n, inner_len, block_size, backend=backend)
+    if bf16:
+        cfg = _bf16_params(cfg)
+    out = {}
+    t = _time(lambda: out.setdefault("y", oracle.hyena_forward(x, cfg)), 1)
+    parity = oracle.rel_err(np.asarray(y0[:, :n], dtype=np.float64), out["y"]) if y0 is not None else None
+    if variant in ("SE", "MR"):
+        return t * L / n, f"oracle.hyena_forward over the first {n} tokens of one ({D}, {L}) batch element, " \
+                          f"scaled x{L / n:g}", time.perf_counter() - w0, parity
     ch = max(1, min(16, 16 * 131072 // L))
     full = _oracle_cfg("LI", ch, L, None, block_size, backend="fft")
     u = rng.standard_normal((ch, L))
     t_conv = _time(lambda: oracle.fft_conv(u, oracle.bank_taps_per_channel(full["inner"])), 1)
-    return (t_local * L / n + t_conv * D / ch,
-            f"oracle LI forward on a ({D}, {n}) window (scaled x{L / n:g}) + filter materialisation and "
-            f"FFT long conv on {ch} channels at L={L} (scaled x{D / ch:g})", time.perf_counter() - w0)
+    return (t * L / n + t_conv * D / ch,
+            f"oracle LI forward on the first {n} tokens (scaled x{L / n:g}) + filter materialisation and "
+            f"FFT long conv on {ch} channels at L={L} (scaled x{D / ch:g})", time.perf_counter() - w0, parity)
 
 
 def _stripe_or_single(wl):
@@ -482,44 +590,47 @@ def _stripe_or_single(wl):
     return ((wl["variant"], wl.get("inner_len")),)
 
 
-def cpu_sample(wl, sample_len=2048):
-    """Summed over the workload's Hyena layers: (tokens/s, description, wall seconds)."""
+def cpu_sample(wl, name, x0=None, y0=None):
+    """Summed over the workload's Hyena layers: (tokens/s, description, wall seconds, parity)."""
     D, L = wl["D"], wl["L"]
     if wl["kind"] == "train":
         sec, desc, wall = cpu_seconds_train(wl["variant"], D, L, wl.get("inner_len"), wl.get("block_size", 16))
-        return L / sec, desc, wall
+        return L / sec, desc, wall, None
     parts = [cpu_seconds_per_element(v, D, L, ln, 128 if wl["kind"] == "stripe" else wl.get("block_size", 16),
-                                     sample_len=sample_len, f32=wl["dtype"] == "f32")
+                                     sample_len=SAMPLE_LEN.get(name, 4096), f32=wl["dtype"] == "f32",
+                                     x0=x0 if wl["kind"] == "op" else None,
+                                     y0=y0 if wl["kind"] == "op" else None, bf16=wl["dtype"] == "bf16")
              for v, ln in _stripe_or_single(wl)]
     sec = sum(p[0] for p in parts)
     desc = "; ".join(p[1] for p in parts)
     if wl["kind"] == "stripe":
         desc = "stripe Hyena layers only (the reference has no MHA): " + desc
-    return L / sec, desc, sum(p[2] for p in parts)
+    return L / sec, desc, sum(p[2] for p in parts), parts[0][3] if wl["kind"] == "op" else None
 
 
-def run_cpu_baseline(wl):
-    """Oracle (numpy, float64 like the reference) on a bounded sample of the workload."""
-    value, desc, _ = cpu_sample(wl, sample_len=8192 if wl["kind"] == "op" and wl["variant"] == "MR" else 4096)
-    if wl["kind"] == "train":
-        return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                "sample": f"{desc}; OpenBLAS on all {os.cpu_count()} host cores"}
-    return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{desc}; numpy float64 restatement of hyena.py:157-190, OpenBLAS on all "
-                      f"{os.cpu_count()} host cores"}
+def run_cpu_baseline(wl, name, x0=None, y0=None):
+    """Oracle (numpy, float64 like the reference) on a bounded sample of the workload, fed the
+    device's batch-0 input; its output is the parity check of the device output."""
+    value, desc, wall, parity = cpu_sample(wl, name, x0, y0)
+    info = host_info()
+    base = {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{desc}; numpy float64 restatement of hyena.py:157-190 (oracle/ref.py), OpenBLAS GEMMs "
+                      f"multithreaded, np.convolve / FFT single-threaded" if wl["kind"] != "train" else desc,
+            "wall_s": wall, "host": info}
+    return base, parity
 
 
 def run_reference(args, wl):
     """Reference arm: the reference algorithm's CPU implementation (the numpy oracle port,
-    float64 as the reference computes) on the host, rank 0 only. Each step is one bounded
-    sample of the workload (see cpu_seconds_per_element); value = tokens/s of the workload
-    extrapolated from the sample."""
+    float64 as the reference computes) on the host, rank 0 only. Each step is the same bounded
+    sample as the cpu_baseline leg (same token window, same extrapolation); value = tokens/s
+    of the workload extrapolated from the sample."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return None, rank
     vals, walls = [], []
     for i in range(args.warmup + args.steps):
-        v, desc, wall = cpu_sample(wl)
+        v, desc, wall, _ = cpu_sample(wl, args.workload)
         if i >= args.warmup:
             vals.append(v)
             walls.append(wall)
@@ -534,7 +645,7 @@ def run_reference(args, wl):
         "data": "synthetic N(0,1) inputs, random-init weights (make_hyena_config seed 0)",
         "config": {"workload": wl["desc"], "global_batch": wl["B"], "seq_len": wl["L"], "width": wl["D"]},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }, rank
 
@@ -556,9 +667,16 @@ def main():
     if args.impl == "reference":
         res, rank = run_reference(args, wl)
     else:
-        res, rank = run_ours(args, wl)
+        res, rank, pio = run_ours(args, wl)
         if rank == 0 and res["n_gpus"] == 1 and not args.no_cpu_baseline:
-            res["cpu_baseline"] = run_cpu_baseline(wl)
+            x0, y0 = pio if pio is not None else (None, None)
+            res["cpu_baseline"], err = run_cpu_baseline(wl, args.workload, x0, y0)
+            tol = 1e-5 if wl["dtype"] == "f32" else 1e-2  # north-star bars (fp32 / bf16 vs the fp64 oracle)
+            res["parity"] = {"rel_err": err, "tol": tol, "ok": None if err is None else bool(err <= tol),
+                             "vs": "oracle.hyena_forward (numpy f64) on the device's batch-0 input, first "
+                                   f"{SAMPLE_LEN.get(args.workload, 4096)} tokens (causal prefix), parameters the "
+                                   "device stores in bf16 rounded to bf16" if err is not None else
+                                   "no oracle for this workload's composition (parity in tests/)"}
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)
 

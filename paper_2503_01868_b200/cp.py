@@ -74,6 +74,14 @@ class CPGroup:
                 self.peers[key] = None
         return self.peers[key]
 
+    def close(self) -> None:
+        """Release the group's peer exchangers (collective: every rank calls it)."""
+        for key in sorted(self.peers, key=repr):
+            ex = self.peers.pop(key)
+            for e in (ex if isinstance(ex, tuple) else (ex,)):
+                if e is not None:
+                    e.close()
+
     def __post_init__(self):
         n = self.n_ranks
         if n < 1 or (n & (n - 1)) != 0:
@@ -101,6 +109,71 @@ class CPGroup:
 
     def total_messages(self, scheme: str | None = None) -> int:
         return self.scheme_messages.get(scheme, 0) if scheme else sum(self.scheme_messages.values())
+
+
+# ---------------------------------------------------------------- transport
+# NCCL moves CUDA tensors itself. A gloo group (CPU-only collectives) that is handed CUDA
+# tensors -- e.g. two ranks sharing one GPU, where NCCL refuses to run -- stages them
+# through host memory; bf16 travels as its int16 bit pattern (no arithmetic on the way).
+
+
+def _staged(grp: CPGroup, t: torch.Tensor) -> bool:
+    return t.is_cuda and dist.get_backend(grp.group) != "nccl"
+
+
+def _wire(t: torch.Tensor) -> torch.Tensor:
+    return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+
+
+class _HostReq:
+    """A gloo request on a host copy; wait() copies a received host buffer back."""
+
+    def __init__(self, req, host, dst=None):
+        self.req, self.host, self.dst = req, host, dst
+
+    def wait(self):
+        self.req.wait()
+        if self.dst is not None:
+            self.dst.copy_(self.host.view(self.dst.dtype) if self.dst.dtype == torch.bfloat16 else self.host)
+        return True
+
+
+def _batch_p2p(grp: CPGroup, ops_) -> list:
+    """ops_: [("send" | "recv", tensor, peer)] -> requests with wait()."""
+    if not ops_:
+        return []
+    if not any(_staged(grp, t) for _, t, _ in ops_):
+        return dist.batch_isend_irecv([dist.P2POp(dist.isend if k == "send" else dist.irecv, t, p, grp.group)
+                                       for k, t, p in ops_])
+    torch.cuda.synchronize()
+    reqs = []
+    for k, t, p in ops_:
+        if k == "send":
+            host = _wire(t.detach().contiguous()).cpu()
+            reqs.append(_HostReq(dist.isend(host, p, group=grp.group), host))
+        else:
+            host = torch.empty(t.shape, dtype=_wire(t).dtype)
+            reqs.append(_HostReq(dist.irecv(host, p, group=grp.group), host, t))
+    return reqs
+
+
+def _all_to_all(grp: CPGroup, out: torch.Tensor, inp: torch.Tensor) -> None:
+    if not _staged(grp, inp):
+        dist.all_to_all_single(out, inp, group=grp.group)
+        return
+    host = torch.empty(out.shape, dtype=_wire(out).dtype)
+    dist.all_to_all_single(host, _wire(inp.contiguous()).cpu(), group=grp.group)
+    out.copy_(host.view(out.dtype) if out.dtype == torch.bfloat16 else host)
+
+
+def _all_gather(grp: CPGroup, parts: list, t: torch.Tensor) -> None:
+    if not _staged(grp, t):
+        dist.all_gather(parts, t, group=grp.group)
+        return
+    hosts = [torch.empty(p.shape, dtype=_wire(p).dtype) for p in parts]
+    dist.all_gather(hosts, _wire(t.contiguous()).cpu(), group=grp.group)
+    for p, h in zip(parts, hosts):
+        p.copy_(h.view(p.dtype) if p.dtype == torch.bfloat16 else h)
 
 
 # ---------------------------------------------------------------- sharding (cpsim.py:244-319)
@@ -228,11 +301,10 @@ def _exchange_halo(local: torch.Tensor, halo: int, grp: CPGroup, scheme: str):
     left = torch.zeros(local.shape[:-1] + (halo,), dtype=local.dtype, device=local.device)
     ops_ = []
     if r < n - 1:
-        ops_.append(dist.P2POp(dist.isend, local[..., local.shape[-1] - halo:].contiguous(), r + 1, grp.group))
+        ops_.append(("send", local[..., local.shape[-1] - halo:].contiguous(), r + 1))
     if r > 0:
-        ops_.append(dist.P2POp(dist.irecv, left, r - 1, grp.group))
-    reqs = dist.batch_isend_irecv(ops_) if ops_ else []
-    return left, reqs
+        ops_.append(("recv", left, r - 1))
+    return left, _batch_p2p(grp, ops_)
 
 
 def p2p_conv(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, layout: str = "sequential",
@@ -309,7 +381,7 @@ def _a2a(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int, layo
                 if dst != src:
                     grp._send(scheme, src, dst, slab * m)
         recv = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
-        dist.all_to_all_single(recv, local[lo:lo + seg].contiguous(), group=grp.group)
+        _all_to_all(grp, recv, local[lo:lo + seg].contiguous())
         if segmented:
             # recv[src, c] is time segment src of slab row c: the conv reads and writes this
             # rank-major layout directly, and its output is already the return send buffer
@@ -325,10 +397,10 @@ def _a2a(local: torch.Tensor, groups: GroupSpec, grp: CPGroup, n_pipe: int, layo
                 if dst != src:
                     grp._send(scheme, src, dst, slab * m)
         if n_pipe == 1:
-            dist.all_to_all_single(out.view(n, slab, m), back, group=grp.group)
+            _all_to_all(grp, out.view(n, slab, m), back)
         else:
             ret = torch.empty((n, slab, m), dtype=local.dtype, device=local.device)
-            dist.all_to_all_single(ret, back, group=grp.group)
+            _all_to_all(grp, ret, back)
             out[lo:lo + seg] = ret.reshape(seg, m)
     grp.count_rounds(scheme, 2 * n_pipe)
     return out
@@ -396,8 +468,7 @@ def _partner_exchange(x: torch.Tensor, partner: int, grp: CPGroup) -> torch.Tens
     """Swap a complex tensor with one partner rank (both send, both receive)."""
     xr = torch.view_as_real(x).contiguous()
     out = torch.empty_like(xr)
-    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, xr, partner, grp.group),
-                                   dist.P2POp(dist.irecv, out, partner, grp.group)])
+    reqs = _batch_p2p(grp, [("send", xr, partner), ("recv", out, partner)])
     for q in reqs:
         q.wait()
     return torch.view_as_complex(out)
@@ -513,7 +584,7 @@ def p2p_fft_causal_wrapper(x: SeqTensor, h_taps, grp: CPGroup | None = None, dev
     lh = torch.from_numpy(np.ascontiguousarray(hp[:, r * m:(r + 1) * m])).to(dev)
     y_local = p2p_fft_conv(lx, lh, grp)
     parts = [torch.empty_like(y_local) for _ in range(n)]
-    dist.all_gather(parts, y_local, group=grp.group)
+    _all_gather(grp, parts, y_local)
     y = torch.cat(parts, dim=-1)[:, : x.length].cpu().numpy()
     return SeqTensor(y, dtype=x.dtype)
 
@@ -543,8 +614,10 @@ class HyenaCP:
         """The group's PeerHalo for this tail shape (CUDA devices only)."""
         return self.grp.peer("halo", tail.shape, tail.dtype) if tail.is_cuda else None
 
-    def _fused(self) -> bool:
-        return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI"
+    def _fused(self, m: int) -> bool:
+        """The tcgen05 mixer with a projection history (the only mixer that takes one): bf16,
+        lh <= 129, rows of m % 8 == 0 (hy_hyena_mixer_fwd's routing rule)."""
+        return self.op.dtype == torch.bfloat16 and self.op.lh <= 129 and self.cfg.variant != "LI" and m % 8 == 0
 
     def _li_pipelined(self, m: int) -> bool:
         op, n = self.op, self.grp.n_ranks
@@ -640,7 +713,7 @@ class HyenaCP:
                         recv = peer[0].exchange(u_s[b].view(n, slab, m), k)
                     else:
                         recv = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
-                        dist.all_to_all_single(recv, u_s[b], group=grp.group)
+                        _all_to_all(grp, recv, u_s[b])
                     if events is not None and s == 0 and b == 0:
                         events[0].record(comm)
                     y_slab = ops.li_conv_segmented(recv, res, poles, op.gs)
@@ -651,7 +724,7 @@ class HyenaCP:
                         back = peer[1].exchange(y_slab, k)
                     else:
                         back = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
-                        dist.all_to_all_single(back, y_slab, group=grp.group)
+                        _all_to_all(grp, back, y_slab)
                     torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
                     if peer is not None:
                         peer[1].release(k)
@@ -733,7 +806,7 @@ class HyenaCP:
             return op.forward(x_local, events=events, accumulate_into=accumulate_into)
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
         B, D, m = x3.shape
-        if self._fused() and m >= _lib.MIXER_HISTORY:
+        if self._fused(m) and m >= _lib.MIXER_HISTORY:
             # the successor needs only the projections of the last 144 steps: compute those
             # first and start the send, so the transfer overlaps the full projection GEMM
             tail = op.project(x3[..., m - _lib.MIXER_HISTORY:].contiguous())

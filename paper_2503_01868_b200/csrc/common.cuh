@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <map>
+#include <set>
 #include <mutex>
 #include <tuple>
 #include <string>
@@ -92,6 +93,26 @@ inline long long resident_cap(const void* kern, int threads, int smem) {
   std::lock_guard<std::mutex> g(mu);
   cache[key] = cap;
   return cap;
+}
+
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device. The
+// attribute belongs to each device's context, so the once-only cache is keyed by device.
+inline cudaError_t ensure_smem_attr(const void* kern, int smem) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, dev, smem);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(key)) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    done.insert(key);
+  }
+  return e;
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -280,11 +280,9 @@ static int launch_fb(const void* proj, const void* g, const void* c, const void*
   auto kern = feat_bwd_kernel<T, NF>;
   constexpr int SMEM = fb_smem<T>();
   constexpr int THREADS = fb_warps<T>() * 32;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), SMEM);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   const long long cap = resident_cap(reinterpret_cast<const void*>(kern), THREADS, SMEM);
   const long long total = static_cast<long long>((L + kFbStep - 1) / kFbStep) * C * B;

@@ -291,15 +291,11 @@ int run_cols(const void* q, const void* k, const void* v, void* y, const float* 
              int gs, const Plan& pl, float2* tw, float2* Hf, float2* X, cudaStream_t st) {
   const size_t col_smem = (COL_POINTS + MAX_N1 / 2) * sizeof(float2);
   const size_t row_smem = (MAX_N2 + MAX_N2 / 2) * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(col_fwd_kernel<T, true, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem);
-    cudaFuncSetAttribute(col_fwd_kernel<T, false, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem);
-    cudaFuncSetAttribute(col_inv_kernel<T, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem);
-    cudaFuncSetAttribute(row_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem);
-    cudaFuncSetAttribute(row_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem);
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(col_fwd_kernel<T, true, COLS>), (int)col_smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(col_fwd_kernel<T, false, COLS>), (int)col_smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(col_inv_kernel<T, COLS>), (int)col_smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<true>), (int)row_smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<false>), (int)row_smem);
   const int ncol = pl.N2 / COLS;
   for (int c0 = 0; c0 < C; c0 += ROW_BLOCK) {
     const int rows = C - c0 < ROW_BLOCK ? C - c0 : ROW_BLOCK;

@@ -410,12 +410,8 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
 template <typename T, int N1>
 int run_n1(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L, int lh,
            int gs, int N, int row_block, float2* hi, float2* lo, float2* Hf, float2* X, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(row_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM);
-    cudaFuncSetAttribute(row_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM);
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<true>), ROW_SMEM);
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<false>), ROW_SMEM);
   const dim3 cgrid_x(M / COL_THREADS);
   for (int c0 = 0; c0 < C; c0 += row_block) {
     const int rows = C - c0 < row_block ? C - c0 : row_block;
@@ -439,11 +435,7 @@ int run_n1(const void* q, const void* k, const void* v, void* y, const float* ta
 // Spectra of all G groups (cached by the caller) and the conv that reads them.
 template <int N1>
 int spectrum_n1(const float* taps, int G, int lh, int N, float2* hi, float2* lo, float2* spec, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(row_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM);
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<true>), ROW_SMEM);
   for (int g0 = 0; g0 < G; g0 += 32768) {  // grid.y limit
     const int ng = G - g0 < 32768 ? G - g0 : 32768;
     col_fwd<float, N1, true><<<dim3(M / COL_THREADS, ng), COL_THREADS, 0, st>>>(
@@ -457,11 +449,7 @@ int spectrum_n1(const float* taps, int G, int lh, int N, float2* hi, float2* lo,
 template <typename T, int N1>
 int conv_spec_n1(const void* q, const void* k, const void* v, void* y, const float2* spec, int B, int C, int L,
                  int gs, int N, int row_block, float2* hi, float2* lo, float2* X, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(row_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ROW_SMEM);
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<false>), ROW_SMEM);
   for (int c0 = 0; c0 < C; c0 += row_block) {
     const int rows = C - c0 < row_block ? C - c0 : row_block;
     const int g0 = c0 / gs;

@@ -559,12 +559,9 @@ static int launch_se(const void* proj, void* y, const float* ft, int lhf, const 
   auto kern = vec ? se_mixer_kernel<T, NF, NI, true> : se_mixer_kernel<T, NF, NI, false>;
   constexpr int RING = (kSeThreads / 32) * 2 * 3 * 256 * static_cast<int>(sizeof(T));
   const int smem = vec ? RING : 0;
-  static bool attr_set = false;
-  if (!attr_set && RING > 0) {
-    cudaError_t e = cudaFuncSetAttribute(se_mixer_kernel<T, NF, NI, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, RING);
+  if (RING > 0) {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(se_mixer_kernel<T, NF, NI, true>), RING);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kSeThreads, smem);
   constexpr int N2 = NF > NI ? NF : NI;
@@ -585,11 +582,9 @@ static int launch_se_stream(const void* proj, void* y, const float* ft, int lhf,
                             void* dc_out = nullptr, void* dc_rev = nullptr, const void* rhist = nullptr) {
   auto kern = se_stream_kernel<T, NF, NI, PREP>;
   constexpr int SMEM = kSsWarps * kSsStages * ((PREP ? 4 : 3) * kSsChunk * static_cast<int>(sizeof(T)) + 8);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), SMEM);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kSsWarps * 32, SMEM);
   const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * C * B;
@@ -733,11 +728,9 @@ static int launch_fir_stream_t(const void* q, const void* k, const void* v, void
   auto kern = fir_stream_kernel<T, NJ, GK, GQ>;
   constexpr int NR = 1 + (GK ? 1 : 0) + (GQ ? 1 : 0);
   constexpr int SMEM = kFsWarps * kFsStages * (NR * kSsChunk * static_cast<int>(sizeof(T)) + 8);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), SMEM);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   const long long cap = resident_cap(reinterpret_cast<const void*>(kern), kFsWarps * 32, SMEM);
   const long long total = static_cast<long long>((L + kSsChunk - 1) / kSsChunk) * rows;

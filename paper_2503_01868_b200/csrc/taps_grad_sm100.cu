@@ -285,11 +285,9 @@ extern "C" int hy_two_stage_taps_grad(const void* dc, const void* u, float* dtap
     return fail(HY_ERR_UNSUPPORTED, "tcgen05 taps gradient needs L %% 8 == 0 and 16-byte aligned rows");
   if (ws_bytes < hy_two_stage_taps_grad_workspace_size(C, lh)) return fail(HY_ERR_INVALID, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tg::taps_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tg::SMEM);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(tg::taps_grad_kernel), tg::SMEM);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -885,11 +885,9 @@ template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL = false>
 static int launch_ks(const Params& p, cudaStream_t st) {
   auto kern = two_stage_kernel<FEAT, GK, GQ, KS, IMPL>;
   constexpr int smem = Layout<KS>::SMEM_BYTES;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -136,6 +136,15 @@ def _implicit_taps_device(inner: GroupSpec, dev, dtype) -> torch.Tensor:
     return out.to(dtype)
 
 
+def fused_mixer_eligible(dtype: torch.dtype, lh: int, L: int) -> bool:
+    """The routing rule of hy_hyena_mixer_fwd (csrc/mixer.cu): the tcgen05 mixer for bf16 with
+    lh <= 129 on rows of L % 8 == 0, else the CUDA-core SE stream mixer for lh <= 16 (fp32 /
+    bf16, any L). Anything else composes the unfused kernels."""
+    if dtype == torch.bfloat16 and lh <= 129 and L % 8 == 0:
+        return True
+    return dtype in (torch.float32, torch.bfloat16) and lh <= 16
+
+
 class HyenaOperator:
     """Device-resident parameters of one HyenaConfig and the torch-native forward.
 
@@ -205,10 +214,10 @@ class HyenaOperator:
         if self.li_modes is not None and proj.shape[-1] % 8 == 0:
             return ops.li_mixer(proj, self.feat_taps, self.li_modes[0], self.li_modes[1], self.gs,
                                 packed=self.feat_packed)
-        fused_ok = (self.dtype == torch.bfloat16 and self.lh <= 129) or \
-                   (self.dtype in (torch.float32, torch.bfloat16) and self.lh <= 16)
-        if fused_ok:
-            return ops.hyena_mixer(proj, self.feat_taps, self.inner_taps, self.gs, decay=self.decay,
+        if fused_mixer_eligible(self.dtype, self.lh, proj.shape[-1]):
+            # LI keeps no explicit taps (modal form); a short LI filter is materialised once
+            taps = self.inner_taps if self.inner_taps is not None else self.materialized_inner
+            return ops.hyena_mixer(proj, self.feat_taps, taps, self.gs, decay=self.decay,
                                    packed=self.feat_packed)
         # unfused: featurizers over all 3D rows in one launch, then the gated inner conv
         B, _, L = proj.shape

@@ -83,6 +83,7 @@ class _Symmetric:
         allh = [None] * self.n
         dist.all_gather_object(allh, mine, group=group)
         self.peer_data, self.peer_flags = [0] * self.n, [0] * self.n
+        self.closed = False
         err = None
         try:
             for p in range(self.n):
@@ -95,13 +96,44 @@ class _Symmetric:
                 self.peer_flags[p] = int(_ck(_rt.cudaIpcOpenMemHandle(hf, _rt.cudaIpcMemLazyEnablePeerAccess)))
         except RuntimeError as e:  # e.g. no IPC between these processes
             err = e
-        # every rank learns whether every rank mapped its peers (no rank may wait alone)
-        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+        # every rank learns whether every rank mapped its peers (no rank may wait alone); the
+        # flag travels on the device for NCCL groups, on the host for gloo groups
+        on = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=on)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         if int(ok.item()) == 0:
+            self._unmap()  # handles opened before the failure, then the local buffers
+            self._free_local()
+            self.closed = True
             raise PeerUnavailable(f"peer mapping failed on some rank ({err or 'another rank'})")
         self.use = [0] * nslots
         self.step = 0
+
+    def _unmap(self):
+        for p in range(self.n):
+            for lst in (self.peer_data, self.peer_flags):
+                if p != self.r and lst[p]:
+                    _rt.cudaIpcCloseMemHandle(lst[p])
+                    lst[p] = 0
+
+    def _free_local(self):
+        for name in ("data", "flags"):
+            if getattr(self, name, 0):
+                _rt.cudaFree(getattr(self, name))
+                setattr(self, name, 0)
+
+    def close(self) -> None:
+        """Collective over the group (every rank calls it, in the same order as the other
+        exchangers' close): drain this rank's transfers, unmap the peers' buffers, and free
+        this rank's own buffers once no peer maps them any more."""
+        if self.closed:
+            return
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # every rank's copies into its peers have landed
+        self._unmap()
+        dist.barrier(group=self.group)  # no peer maps this rank's buffers any more
+        self._free_local()
+        self.closed = True
 
     def next_slot(self) -> int:
         """Slots are taken round robin; every rank calls this in the same order."""

@@ -1,8 +1,14 @@
 """GPU checks of the context-parallel path.
 
-* single GPU: the fused mixer with a projection history equals the second half of a
-  full-sequence run (the property the CP operator relies on);
-* >= 2 GPUs (skipped otherwise): HyenaCP over NCCL equals the single-GPU operator.
+* the fused mixer with a projection history equals the second half of a full-sequence run
+  (the property the CP operator relies on);
+* the multi-rank schemes (HyenaCP for MR / SE / LI over the peer-memory and the collective
+  transports, LayoutCP, the all-to-all backward, the distributed FFT) against the
+  single-GPU operator or the oracle. With >= 2 GPUs every rank owns a GPU and the group is
+  NCCL; on a one-GPU box two ranks share cuda:0 over a gloo group: the peer-memory path is
+  then CUDA IPC between the two processes on the same device (the same copy-engine copies
+  and stream flag waits), and the collective path stages through host memory (cp.py
+  transport) -- so every scheme runs on the device on any box.
 """
 
 from __future__ import annotations
@@ -40,13 +46,58 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _cp_worker(rank, world, port, variant, q, p2p="1", batch=1):
+def _world() -> int:
+    n = torch.cuda.device_count()
+    return min(n, 4) if n >= 2 else 2
+
+
+def _init(rank, world, port):
+    """One GPU per rank over NCCL when the box has them; else every rank on cuda:0 over gloo."""
     import torch.distributed as dist
-    os.environ["HY_CP_P2P"] = p2p
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    if torch.cuda.device_count() >= world:
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _gather(t: torch.Tensor) -> list:
+    """all_gather of a device tensor on either backend (host tensors for gloo)."""
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    if dist.get_backend() == "nccl":
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return parts
+    h = t.float().cpu()
+    parts = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(parts, h)
+    return [p.to(t.device, t.dtype) for p in parts]
+
+
+def _run(target, *args):
+    import torch.multiprocessing as mp
+    world = _world()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    return res
+
+
+def _cp_worker(rank, world, port, variant, p2p, batch, q):
+    import torch.distributed as dist
+    os.environ["HY_CP_P2P"] = p2p
+    _init(rank, world, port)
     try:
         D, L = 64, 8192 * world
         kw = {"inner_len": 128, "block_size": 128} if variant == "MR" else {}
@@ -57,44 +108,38 @@ def _cp_worker(rank, world, port, variant, q, p2p="1", batch=1):
         cpop = hy.cp.HyenaCP(cfg, torch.bfloat16)
         for _ in range(3):  # repeated steps exercise the slot flow control of the peer transfers
             y_local = cpop.forward(x[..., rank * m:(rank + 1) * m].contiguous())
+        parts = _gather(y_local)
         if rank == 0:
-            y_ref = hy.HyenaOperator(cfg, torch.bfloat16).forward(x)
-        parts = [torch.empty_like(y_local) for _ in range(world)]
-        dist.all_gather(parts, y_local)
-        if rank == 0:
+            y_ref = hy.HyenaOperator(cfg, torch.bfloat16).forward(x).float()
             y = torch.cat(parts, dim=-1).float()
-            err = float((y - y_ref.float()).abs().max() / max(1.0, float(y_ref.float().abs().max())))
-            q.put(err)
+            err = float((y - y_ref).abs().max() / max(1.0, float(y_ref.abs().max())))
+            q.put((err, dist.get_backend(), sum(v is not None for v in cpop.grp.peers.values())))
+        cpop.grp.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("p2p", ["1", "0"], ids=["peer", "nccl"])
+@pytest.mark.parametrize("p2p", ["1", "0"], ids=["peer", "collective"])
 @pytest.mark.parametrize("variant", ["MR", "SE", "LI"])
 def test_hyena_cp_matches_single_gpu(variant, p2p):
-    """HyenaCP's halo / all-to-all over copy-engine peer transfers (default) and over NCCL."""
-    import torch.multiprocessing as mp
-    world = min(torch.cuda.device_count(), 4)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, variant, q, p2p)) for r in range(world)]
-    for p in procs:
-        p.start()
-    err = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    assert err < 2e-2, err
+    """HyenaCP's halo / all-to-all over copy-engine peer transfers (default) and over the
+    group's collectives (NCCL; gloo host staging when two ranks share one GPU)."""
+    err, backend, npeers = _run(_cp_worker, variant, p2p, 1)
+    assert err < 2e-2, (err, backend)
+    if p2p == "1":
+        assert npeers > 0  # the peer-memory transport was mapped, not silently skipped
+
+
+def test_hyena_cp_li_batched():
+    """LI CP layer with B = 2: the software pipeline's peer slots cycle through both batch
+    elements of every segment (flow control across segments)."""
+    err, backend, _ = _run(_cp_worker, "LI", "1", 2)
+    assert err < 2e-2, (err, backend)
 
 
 def _a2a_bwd_worker(rank, world, port, q):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    _init(rank, world, port)
     try:
         from oracle import backward as ob
         D, L, lh = 16, 4096, 9
@@ -110,8 +155,8 @@ def _a2a_bwd_worker(rank, world, port, q):
             dys = hy.cp.shard(hy.SeqTensor(dy), world, layout)
             _, saved = hy.cp.a2a_conv_saved(torch.from_numpy(xs.shards[rank].copy()).cuda(), groups, grp, layout)
             dx = hy.cp.a2a_conv_backward(saved, torch.from_numpy(dys.shards[rank].copy()).cuda(), grp)
-            parts = [torch.empty_like(dx) for _ in range(world)]
-            dist.all_gather(parts, dx)
+            assert dx.is_cuda
+            parts = _gather(dx)
             if rank == 0:
                 got = hy.cp.gather(hy.cp.ShardedSeq([p.cpu().numpy() for p in parts], layout)).data
                 want = ob.causal_conv_input_grad(dy, np.repeat(taps, 2, axis=0))
@@ -122,51 +167,17 @@ def _a2a_bwd_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_hyena_cp_li_batched():
-    """LI CP layer with B = 2: the software pipeline's peer slots cycle through both batch
-    elements of every segment (flow control across segments)."""
-    import torch.multiprocessing as mp
-    world = min(torch.cuda.device_count(), 4)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_cp_worker, args=(r, world, port, "LI", q, "1", 2)) for r in range(world)]
-    for p in procs:
-        p.start()
-    err = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    assert err < 2e-2, err
-
-
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_a2a_backward_nccl_matches_oracle():
-    """a2a_conv_backward (cpsim.py:440-446) over NCCL, fp64 slab adjoint on the device, both
-    layouts, against the oracle's unsharded input adjoint (core.py:245-252)."""
-    import torch.multiprocessing as mp
-    world = min(torch.cuda.device_count(), 4)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_a2a_bwd_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+def test_a2a_backward_matches_oracle():
+    """a2a_conv_backward (cpsim.py:440-446), fp64 slab adjoint on the device, both layouts,
+    against the oracle's unsharded input adjoint (core.py:245-252)."""
+    res = _run(_a2a_bwd_worker)
     for layout, err in res.items():
         assert err < 1e-12, (layout, err)
 
 
 def _layout_worker(rank, world, port, q):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    _init(rank, world, port)
     try:
         D, L = 64, 8192 * world
         rng = hy.make_rng(4)
@@ -181,8 +192,7 @@ def _layout_worker(rank, world, port, q):
         lcp = hy.LayoutCP(stack, torch.bfloat16)
         for _ in range(2):
             y_local = lcp.forward(x[..., rank * m:(rank + 1) * m].contiguous())
-        parts = [torch.empty_like(y_local) for _ in range(world)]
-        dist.all_gather(parts, y_local)
+        parts = _gather(y_local)
         if rank == 0:
             y_ref = hy.layout_forward_device(x, stack).float()
             y = torch.cat(parts, dim=-1).float()
@@ -191,38 +201,23 @@ def _layout_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 def test_layout_cp_matches_single_gpu():
     """SE-MR-LI-MR residual stack sharded once across ranks (LayoutCP) equals the single-GPU
     layout forward; the layers share the group's peer buffers."""
-    import torch.multiprocessing as mp
-    world = min(torch.cuda.device_count(), 4)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_layout_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    err = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    err = _run(_layout_worker)
     assert err < 2e-2, err
 
 
 def _dfft_worker(rank, world, port, q):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    _init(rank, world, port)
     try:
         import oracle
         rng = np.random.default_rng(21)
         C, L, lh = 4, 3000, 700
         x = rng.standard_normal((C, L))
         taps = rng.standard_normal((C, lh)) / np.sqrt(lh)
-        y = hy.cp.p2p_fft_causal_wrapper(hy.SeqTensor(x), taps, hy.cp.CPGroup())
+        y = hy.cp.p2p_fft_causal_wrapper(hy.SeqTensor(x), taps, hy.cp.CPGroup(), device="cuda")
         if rank == 0:
             want = oracle.direct_causal_conv(x, {"channels": C, "group_size": 1,
                                                  "filters": [("explicit", t) for t in taps]})
@@ -231,20 +226,8 @@ def _dfft_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_p2p_fft_causal_nccl_matches_oracle():
-    """Distributed FFT conv (cpsim.py:634-659) over NCCL on the devices, float64 (cuFFT local
-    transforms), against the oracle's direct causal conv."""
-    import torch.multiprocessing as mp
-    world = min(torch.cuda.device_count(), 4)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_dfft_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    err = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+def test_p2p_fft_causal_matches_oracle():
+    """Distributed FFT conv (cpsim.py:634-659) on the devices, float64, against the oracle's
+    direct causal conv."""
+    err = _run(_dfft_worker)
     assert err < 1e-10, err

@@ -187,3 +187,42 @@ def test_residual_fused_into_out_projection(dtype):
         tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
         err = float((got.float() - want).abs().max() / max(1.0, float(want.abs().max())))
         assert err < tol, (B, err)
+
+
+@pytest.mark.parametrize("variant,dtype,L", [("LI", "f32", 16), ("LI", "bf16", 100), ("LI", "bf16", 16),
+                                             ("MR", "bf16", 100), ("SE", "bf16", 100)])
+def test_mixer_routing_edge_lengths(variant, dtype, L):
+    """Lengths and dtypes at the edges of the fused-mixer routing (hyena.fused_mixer_eligible):
+    short fp32 LI filters through the SE stream mixer, bf16 rows with L % 8 != 0 through the
+    unfused kernels, against the oracle (fp32 1e-5, bf16 1e-2)."""
+    D = 16
+    kw = {"inner_len": 128, "block_size": 128} if variant == "MR" else {}
+    cfg = hy.make_hyena_config(variant, D, hy.make_rng(3), seq_len=L, backend="fft" if variant == "LI" else "blocked",
+                               **kw)
+    if dtype == "bf16":
+        rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+        feats = {n: hy.GroupSpec(D, 1, tuple(hy.ExplicitFilter(bf16_round(f.taps)) for f in getattr(cfg, n).filters))
+                 for n in ("q_feat", "k_feat", "v_feat")}
+        cfg = hy.HyenaConfig(**{**cfg.__dict__, **rnd, **feats})
+    x = hy.make_rng(4).standard_normal((D, L))
+    x = bf16_round(x) if dtype == "bf16" else x.astype(np.float32)
+    if dtype == "bf16":
+        y = hy.HyenaOperator(cfg, torch.bfloat16).forward(torch.from_numpy(x).to("cuda", torch.bfloat16))
+        y = y.double().cpu().numpy()
+    else:
+        y = hy.hyena_forward(hy.SeqTensor(x, "f32"), cfg).data
+    ocfg = {"variant": variant, "width": D, "block_size": cfg.block_size, "backend": cfg.backend,
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        g = getattr(cfg, n)
+        fl = []
+        for f in g.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fl.append(("explicit", f.taps))
+            elif isinstance(f, hy.RegularizedFilter):
+                fl.append(("regularized", f.taps_hat, f.decay_rate, f.base))
+            else:
+                fl.append(("implicit", f.residues, f.poles, f.length))
+        ocfg[n] = {"channels": g.channels, "group_size": g.group_size, "filters": fl}
+    want = oracle.hyena_forward(x, ocfg)
+    assert oracle.rel_err(y, want) < (1e-5 if dtype == "f32" else 1e-2)

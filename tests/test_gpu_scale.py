@@ -1,0 +1,195 @@
+"""GPU parity at the scale that is benchmarked.
+
+The tcgen05 kernels are persistent: grid = min(work units, 148 SMs) and each CTA walks a
+contiguous range of tiles, rebuilding the Toeplitz factors (T0 double-buffered, T1 single)
+at every filter-group change and cycling the NBUF = 3 accumulator ring and the 4-stage
+input ring. Small parity cases give each CTA one or two tiles, so these cases are sized to
+give every CTA many tiles and many filter groups, as the C2 / C3 benchmarks do:
+
+* explicit / MR (two_stage_kernel, both the two_stage API and the fused FEAT mixer):
+  B=1, C=4096, L=4096 (one tile per group per CTA step: a factor rebuild on every tile,
+  ~28 groups per CTA) and B=4, C=1024, L=8192 (the C2 tile walk: 8 tiles per channel);
+  gs = 1 and gs = 16;
+* implicit / LI (IMPL instantiation): L = 131072 (config C3's length, 32 tiles of carried
+  modal state per sequence) with poles at +-1, +-0.9999 and 0, more sequences than SMs;
+* the bf16 MR operator at the full width D = 4096 (config C2 with B = 1) against
+  oracle.hyena_forward end to end.
+
+The conv is channel-separable, so the kernel-level checks compare ~32 channels sampled
+across all CTAs against the fp64 oracle (north-star bf16 bar 1e-2, written below).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2503_01868_b200 as hy
+from paper_2503_01868_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2  # north star: bf16 path rel-err <= 1e-2 against the fp64 oracle
+SMS = 148
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def _bf16_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to("cuda", torch.bfloat16)
+
+
+def _sample_channels(C: int, n: int = 32) -> list:
+    """Channels spread over every CTA's range (first / last channel of several CTAs)."""
+    per = C / SMS
+    picks = {0, C - 1, C // 2}
+    for cta in np.linspace(0, SMS - 1, n // 2).astype(int):
+        lo = int(cta * per)
+        hi = min(C - 1, int((cta + 1) * per))
+        picks.update((lo, hi))
+    return sorted(picks)[:n + 3]
+
+
+def _conv(x, h):
+    return np.convolve(x, h)[: x.shape[-1]]
+
+
+@pytest.mark.parametrize("B,C,L,gs", [(1, 4096, 4096, 1), (4, 1024, 8192, 1), (4, 1024, 8192, 16)])
+def test_two_stage_api_many_groups_per_cta(B, C, L, gs):
+    """two_stage (non-FEAT instantiation, gated, decay in-kernel) across many groups per CTA."""
+    g = torch.Generator(device="cuda").manual_seed(B * C + gs)
+    G = C // gs
+    v, q, k = (torch.randn((B, C, L), device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    taps_hat = (torch.randn((G, 128), device="cuda", generator=g) / 11.3).to(torch.bfloat16).float()
+    rates = torch.linspace(0.01, 2.0, G, device="cuda")
+    y = ops.two_stage(v, taps_hat, gs, q=q, k=k, decay=rates).double().cpu().numpy()
+    vh, qh, kh = (t.double().cpu().numpy() for t in (v, q, k))
+    th, rh = taps_hat.double().cpu().numpy(), rates.double().cpu().numpy()
+    worst = 0.0
+    for c in _sample_channels(C):
+        h = oracle.materialize(("regularized", th[c // gs], rh[c // gs], 2.0))
+        for b in range(B):
+            want = qh[b, c] * _conv(kh[b, c] * vh[b, c], h)
+            worst = max(worst, oracle.rel_err(y[b, c], want))
+    assert worst < BF16_TOL, worst
+
+
+@pytest.mark.parametrize("B,C,L,gs", [(1, 4096, 4096, 1), (4, 1024, 8192, 1), (4, 1024, 8192, 16)])
+def test_mr_mixer_many_groups_per_cta(B, C, L, gs):
+    """The fused FEAT mixer (featurizers on tcgen05 + gates + T0/T1 conv with decay) that the
+    C2 bench runs, walking many filter groups per CTA."""
+    g = torch.Generator(device="cuda").manual_seed(7 * C + gs)
+    G = C // gs
+    proj = torch.randn((B, 3 * C, L), device="cuda", generator=g).to(torch.bfloat16)
+    feat = (torch.randn((3, C, 7), device="cuda", generator=g) / 2.65).to(torch.bfloat16).float()
+    taps_hat = (torch.randn((G, 128), device="cuda", generator=g) / 11.3).to(torch.bfloat16).float()
+    rates = torch.linspace(0.01, 2.0, G, device="cuda")
+    y = ops.hyena_mixer(proj, feat, taps_hat, gs, decay=rates).double().cpu().numpy()
+    ph = proj.double().cpu().numpy()
+    fh, th, rh = feat.double().cpu().numpy(), taps_hat.double().cpu().numpy(), rates.double().cpu().numpy()
+    worst = 0.0
+    for c in _sample_channels(C):
+        h = oracle.materialize(("regularized", th[c // gs], rh[c // gs], 2.0))
+        for b in range(B):
+            fq, fk, fv = (_conv(ph[b, i * C + c], fh[i, c]) for i in range(3))
+            want = fq * _conv(fk * fv, h)
+            worst = max(worst, oracle.rel_err(y[b, c], want))
+    assert worst < BF16_TOL, worst
+
+
+def _li_params(G, seed):
+    rng = np.random.default_rng(seed)
+    poles = rng.uniform(-0.95, 0.95, (G, 8))
+    residues = rng.standard_normal((G, 8)) / 8
+    poles[0, :5] = [1.0, -1.0, 0.9999, -0.9999, 0.0]  # undamped and near-undamped tails, a zero pole
+    poles[G // 2, :4] = [0.9999, 0.9999, -1.0, 0.0]
+    poles[-1, :2] = [1.0, 0.0]
+    return residues, poles
+
+
+def _li_taps(residues, poles, L):
+    return oracle.materialize(("implicit", residues, poles, L))
+
+
+@pytest.mark.parametrize("gated", [True, False])
+def test_li_conv_c3_length(gated):
+    """Implicit-filter conv at L = 131072 (C3): 32 tiles of carried modal state per sequence,
+    320 sequences (> 148 SMs, so CTAs restart the recurrence), tail poles at +-1 / +-0.9999."""
+    C, L = 320, 131072
+    residues, poles = _li_params(C, 31 + gated)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    v, q, k = (torch.randn((1, C, L), device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    y = ops.li_conv(v, torch.from_numpy(residues).cuda(), torch.from_numpy(poles).cuda(), 1,
+                    q=q if gated else None, k=k if gated else None).double().cpu().numpy()
+    sel = [0, 1, 147, 148, C // 2, C - 2, C - 1]
+    vh, qh, kh = (t[0, sel].double().cpu().numpy() for t in (v, q, k))
+    u = vh * kh if gated else vh
+    taps = np.stack([_li_taps(residues[c], poles[c], L) for c in sel])
+    want = oracle.fft_conv(u, taps) * (qh if gated else 1.0)
+    for i, c in enumerate(sel):
+        err = oracle.rel_err(y[0, c], want[i])
+        assert err < BF16_TOL, (c, err)
+
+
+def test_li_mixer_c3_length():
+    """The fused LI mixer (FEAT + IMPL) at L = 131072 with the tail poles."""
+    C, L = 160, 131072
+    residues, poles = _li_params(C, 41)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    proj = torch.randn((1, 3 * C, L), device="cuda", generator=g).to(torch.bfloat16)
+    feat = (torch.randn((3, C, 7), device="cuda", generator=g) / 2.65).to(torch.bfloat16).float()
+    y = ops.li_mixer(proj, feat, torch.from_numpy(residues).cuda(), torch.from_numpy(poles).cuda(), 1)
+    y = y.double().cpu().numpy()
+    sel = [0, 1, 80, 147, C - 1]
+    ph, fh = proj.double().cpu().numpy(), feat.double().cpu().numpy()
+    for c in sel:
+        fq, fk, fv = (_conv(ph[0, i * C + c], fh[i, c]) for i in range(3))
+        want = fq * oracle.fft_conv(fk * fv, _li_taps(residues[c], poles[c], L))
+        err = oracle.rel_err(y[0, c], want)
+        assert err < BF16_TOL, (c, err)
+
+
+def _rounded_cfg(cfg):
+    rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+
+    def rbank(gspec):
+        fs = []
+        for f in gspec.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fs.append(hy.ExplicitFilter(bf16_round(f.taps)))
+            else:
+                fs.append(hy.RegularizedFilter(bf16_round(f.taps_hat), f.decay_rate, f.base))
+        return hy.GroupSpec(gspec.channels, gspec.group_size, tuple(fs))
+
+    return hy.HyenaConfig(**{**cfg.__dict__, **rnd, **{n: rbank(getattr(cfg, n))
+                                                      for n in ("q_feat", "k_feat", "v_feat", "inner")}})
+
+
+def _oracle_cfg(cfg):
+    ocfg = {"variant": cfg.variant, "width": cfg.width, "block_size": cfg.block_size, "backend": cfg.backend,
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        gspec = getattr(cfg, n)
+        ocfg[n] = {"channels": gspec.channels, "group_size": gspec.group_size,
+                   "filters": [("explicit", f.taps) if isinstance(f, hy.ExplicitFilter)
+                               else ("regularized", f.taps_hat, f.decay_rate, f.base) for f in gspec.filters]}
+    return ocfg
+
+
+@pytest.mark.parametrize("gs", [1, 16])
+def test_mr_operator_full_width(gs):
+    """Config C2's operator at its full width D = 4096 (one batch element, L = 8192): cuBLAS
+    projections + the fused tcgen05 mixer walking ~28 filter groups per CTA, against
+    oracle.hyena_forward on the same bf16-representable parameters and input."""
+    D, L = 4096, 8192
+    cfg = _rounded_cfg(hy.make_hyena_config("MR", D, hy.make_rng(0), group_size=gs, inner_len=128,
+                                            block_size=128))
+    x = bf16_round(hy.make_rng(1, stream=0).standard_normal((D, L)))
+    y = hy.HyenaOperator(cfg, torch.bfloat16).forward(_bf16_dev(x)).double().cpu().numpy()
+    want = oracle.hyena_forward(x, _oracle_cfg(cfg))
+    err = oracle.rel_err(y, want)
+    assert err < BF16_TOL, err
