@@ -38,6 +38,10 @@
  *   hy_featurizer_bwd       hyena.py:234-247     _feat_backward for q, k, v fused with the gate
  *                           hyena.py:262-270     products of hyena_backward (one HBM pass)
  *   hy_two_stage_taps_grad  blockconv.py:246-262 two_stage_backward's two-pass filter gradient (tcgen05)
+ *   hy_li_scan_fwd          fft.py:128-145       fft_conv on an ImplicitFilter bank (core.py:147-151), gated as
+ *                           hyena.py:183-186     hyena_forward's LI inner conv, by exact per-mode scans
+ *   hy_li_scan_mixer_fwd    hyena.py:162-186     the LI mixer (featurizers + gates + modal scan), fused
+ *   hy_split3_cat           hyena.py:124,188     the fp32 projections' operand split (split-bf16 GEMM)
  *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
  *                           core.py:255-268      the tap correlation it consumes
  */
@@ -232,6 +236,26 @@ HY_API size_t hy_li_param_grad_workspace_size(int B, int C);
 HY_API int hy_li_param_grad(const void* dc, const void* u, const float* residues, const float* poles, int npoles,
                             int group_size, int B, int C, int L, int dtype, float* d_res, float* d_pole,
                             void* ws, size_t ws_bytes, void* stream);
+
+/* Hyena-LI long conv as an exact modal state scan on CUDA cores (the reference-precision path):
+ *   y = q * (h conv (k * v)),  h_t = sum_n R_n lam_n^t  (core.py:147-151, fft.py:128-145)
+ * computed as y[t] = q[t] sum_n R_n s_n[t], s_n[t] = lam_n s_n[t-1] + k[t] v[t]. Any dtype
+ * (fp32 / bf16 with fp32 states, fp64 with fp64 states; fp64 tile carries), 1..64 poles per
+ * group, any L; q / k nullable. residues, poles: fp64 (n_groups, npoles). */
+HY_API int hy_li_scan_fwd(const void* q, const void* k, const void* v, void* y, const double* residues,
+                          const double* poles, int npoles, int group_size, int B, int C, int L, int dtype,
+                          void* stream);
+/* The same modal scan fused with the featurizers (lhf <= 8) and gates: the LI mixer from the
+ * projections proj (B, 3C, L) = [q; k; v] rows, y = Fq(pq) * (h conv (Fk(pk) * Fv(pv)))
+ * (hyena.py:162-186), one pass. feat_taps fp32 (3, C, lhf); residues, poles fp64. */
+HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const double* residues,
+                                const double* poles, int npoles, int group_size, int B, int C, int L, int dtype,
+                                void* stream);
+/* fp32 activation -> the K-concatenated bf16 operand of the split-bf16 fp32 GEMM (blas.py; the
+ * fp32 projections of hyena.py:124,188 on tensor cores): x (batch, K, N) fp32, out
+ * (batch, 5K, N) bf16 = [X1; X2; X0; X1; X0] with X0 = bf16(x), X1 = bf16(x - X0),
+ * X2 = bf16(x - X0 - X1) (x == X0 + X1 + X2 exactly). One pass, 4 bytes in / 10 out. */
+HY_API int hy_split3_cat(const float* x, void* out, long long batch, long long K, long long N, void* stream);
 
 /* Debug / tuning: CTA-0 per-tile timeline (clock64) of the last two-stage launch made
  * with HY_TS_TRACE=1 in the environment; n <= 4096 values, 8 events per tile. */

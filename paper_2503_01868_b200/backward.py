@@ -234,6 +234,8 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             return ops.li_conv(a, res, poles, op.gs)
         if ts_ok:
             return ops.two_stage(a, op.inner_taps, op.gs, decay=op.decay)
+        if op.cfg.variant == "LI" and op.li_scan_modes is not None:
+            return ops.li_scan(a, op.li_scan_modes[0], op.li_scan_modes[1], op.gs)  # exact modal scans
         if op.lh > 129 or op.cfg.variant == "LI":
             return ops.long_conv(a, op.materialized_inner, op.gs)
         return ops.gated_conv(a, op.materialized_inner, op.gs)
@@ -245,7 +247,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         if parts is None:
             parts = blas.split3_weight(w_t.transpose(0, 1).contiguous())
             setattr(op, name, parts)
-        return blas.matmul_split3(parts, blas.split3(rhs))
+        return blas.matmul_split3(parts, blas.split3_act(rhs))
 
     dmixed = wt_mm("_w_out_bwd_parts", op.w_out_t, dy3)
     fused = op.dtype != torch.float64 and op.lhf <= 8 and L % 8 == 0
@@ -277,7 +279,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             du_rev = inner_conv(dc_rev)
         else:
             rdc = torch.flip(dc, dims=[-1]).contiguous()
-            rdu = ops.li_conv(rdc, res, poles, op.gs) if modal else ops.long_conv(rdc, op.materialized_inner, op.gs)
+            rdu = ops.li_conv(rdc, res, poles, op.gs) if modal else inner_conv(rdc)
             du = torch.flip(rdu, dims=[-1])
         mark("inner_taps", 0)
         inner_g["residues"], inner_g["poles"] = ops.li_param_grad(dc, u, res, poles, op.gs)

@@ -9,7 +9,7 @@ bits), so
 
 takes six bf16 tensor-core products with fp32 accumulation (the dropped terms are below fp32
 rounding). The weight splits are made once per operator; the activation split is one
-elementwise pass. The five small products run as ONE GEMM with the splits concatenated along
+kernel (hy_split3_cat, csrc/split3.cu) writing the K-concatenated operand. The five small products run as ONE GEMM with the splits concatenated along
 K (Split3.cat, K' = 5K); the leading term A0 @ B0 follows, accumulated into the same fp32
 output (cuBLAS beta = 1). The error is set by the fp32 accumulation inside a long-K
 tensor-core GEMM, so the leading term is accumulated in K chunks with fp32 adds between them.
@@ -42,7 +42,42 @@ def split3_weight(a: torch.Tensor) -> Split3:
 
 
 def _b_cat(b_parts) -> torch.Tensor:
+    if isinstance(b_parts, Split3Act):
+        return b_parts.cat
     return torch.cat([b_parts[j] for _, j in _PAIRS], dim=-2)
+
+
+class Split3Act:
+    """An activation's split in the K-concatenated operand layout, made by one kernel
+    (hy_split3_cat): cat = [X1; X2; X0; X1; X0] ((Bt,) 5K, N) bf16, the B operand of the five
+    small products (the order of _PAIRS); its last K rows are X0, the leading product's."""
+
+    def __init__(self, cat: torch.Tensor, K: int):
+        self.cat = cat
+        self.K = K
+
+    def __getitem__(self, j: int) -> torch.Tensor:
+        if j != 0:
+            raise IndexError("Split3Act exposes only the leading part X0 (index 0) and .cat")
+        return self.cat[..., 4 * self.K:, :]
+
+    def batch(self, i: int) -> "Split3Act":
+        return Split3Act(self.cat[i], self.K)
+
+
+def split3_act(x: torch.Tensor) -> Split3Act:
+    """fp32 (K, N) or (Bt, K, N) CUDA activation -> Split3Act in one HBM pass (hy_split3_cat)."""
+    from . import _lib
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise ValueError("split3_act takes a float32 CUDA tensor")
+    x = x.contiguous()
+    x3 = x.unsqueeze(0) if x.dim() == 2 else x
+    Bt, K, N = x3.shape
+    cat = torch.empty((Bt, 5 * K, N), dtype=torch.bfloat16, device=x.device)
+    lib = _lib.load()
+    _lib.check(lib.hy_split3_cat(x3.data_ptr(), cat.data_ptr(), Bt, K, N,
+                                 torch.cuda.current_stream().cuda_stream), "split3_cat")
+    return Split3Act(cat[0] if x.dim() == 2 else cat, K)
 
 
 def split3(a: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
@@ -66,7 +101,8 @@ def matmul_split3(a_parts, b_parts, out: torch.Tensor | None = None, accumulate:
         if out is None:
             out = torch.empty((Bt, a0.shape[0], N), dtype=torch.float32, device=a0.device)
         for i in range(Bt):
-            matmul_split3(a_parts, tuple(p[i] for p in b_parts), out=out[i], accumulate=accumulate)
+            bi = b_parts.batch(i) if isinstance(b_parts, Split3Act) else tuple(p[i] for p in b_parts)
+            matmul_split3(a_parts, bi, out=out[i], accumulate=accumulate)
         return out
     if out is None:
         out = torch.empty((a0.shape[0], b0.shape[1]), dtype=torch.float32, device=a0.device)
@@ -78,6 +114,8 @@ def matmul_split3(a_parts, b_parts, out: torch.Tensor | None = None, accumulate:
         else:
             torch.mm(cat, bc, out_dtype=torch.float32, out=out)
     else:
+        if isinstance(b_parts, Split3Act):
+            raise ValueError("a Split3Act operand needs a weight split made by split3_weight")
         first = not accumulate
         for i, j in _PAIRS:
             if first:

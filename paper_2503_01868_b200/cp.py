@@ -114,7 +114,7 @@ class CPGroup:
 # ---------------------------------------------------------------- transport
 # NCCL moves CUDA tensors itself. A gloo group (CPU-only collectives) that is handed CUDA
 # tensors -- e.g. two ranks sharing one GPU, where NCCL refuses to run -- stages them
-# through host memory; bf16 travels as its int16 bit pattern (no arithmetic on the way).
+# through host memory; bf16 (no gloo type) travels as its bytes (no arithmetic on the way).
 
 
 def _staged(grp: CPGroup, t: torch.Tensor) -> bool:
@@ -122,7 +122,16 @@ def _staged(grp: CPGroup, t: torch.Tensor) -> bool:
 
 
 def _wire(t: torch.Tensor) -> torch.Tensor:
-    return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+    return t.view(torch.uint8) if t.dtype == torch.bfloat16 else t
+
+
+def _host_like(t: torch.Tensor) -> torch.Tensor:
+    """An empty host buffer of t's wire shape and type."""
+    return torch.empty(_wire(t).shape, dtype=_wire(t).dtype)
+
+
+def _unwire(host: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+    return host.view(like.dtype) if like.dtype == torch.bfloat16 else host
 
 
 class _HostReq:
@@ -134,7 +143,7 @@ class _HostReq:
     def wait(self):
         self.req.wait()
         if self.dst is not None:
-            self.dst.copy_(self.host.view(self.dst.dtype) if self.dst.dtype == torch.bfloat16 else self.host)
+            self.dst.copy_(_unwire(self.host, self.dst))
         return True
 
 
@@ -152,7 +161,7 @@ def _batch_p2p(grp: CPGroup, ops_) -> list:
             host = _wire(t.detach().contiguous()).cpu()
             reqs.append(_HostReq(dist.isend(host, p, group=grp.group), host))
         else:
-            host = torch.empty(t.shape, dtype=_wire(t).dtype)
+            host = _host_like(t)
             reqs.append(_HostReq(dist.irecv(host, p, group=grp.group), host, t))
     return reqs
 
@@ -161,19 +170,19 @@ def _all_to_all(grp: CPGroup, out: torch.Tensor, inp: torch.Tensor) -> None:
     if not _staged(grp, inp):
         dist.all_to_all_single(out, inp, group=grp.group)
         return
-    host = torch.empty(out.shape, dtype=_wire(out).dtype)
+    host = _host_like(out.contiguous())
     dist.all_to_all_single(host, _wire(inp.contiguous()).cpu(), group=grp.group)
-    out.copy_(host.view(out.dtype) if out.dtype == torch.bfloat16 else host)
+    out.copy_(_unwire(host, out))
 
 
 def _all_gather(grp: CPGroup, parts: list, t: torch.Tensor) -> None:
     if not _staged(grp, t):
         dist.all_gather(parts, t, group=grp.group)
         return
-    hosts = [torch.empty(p.shape, dtype=_wire(p).dtype) for p in parts]
+    hosts = [_host_like(p) for p in parts]
     dist.all_gather(hosts, _wire(t.contiguous()).cpu(), group=grp.group)
     for p, h in zip(parts, hosts):
-        p.copy_(h.view(p.dtype) if p.dtype == torch.bfloat16 else h)
+        p.copy_(_unwire(h, p))
 
 
 # ---------------------------------------------------------------- sharding (cpsim.py:244-319)
@@ -696,7 +705,7 @@ class HyenaCP:
             return mixed
         pending = []
         for s, (rows, w, wp, ft, res, poles) in enumerate(segs):
-            proj_s = blas.matmul_split3(wp, blas.split3(x3)) if op.split3 else torch.matmul(w, x3)
+            proj_s = blas.matmul_split3(wp, blas.split3_act(x3)) if op.split3 else torch.matmul(w, x3)
             rh = hist.index_select(1, rows).contiguous() if r > 0 else None
             u_s, fq_s = ops.featurize(proj_s, ft, rhist=rh)
             ev = torch.cuda.Event()
@@ -754,7 +763,7 @@ class HyenaCP:
 
         def start(s):
             rows, w, wp, ft, _, _ = segs[s]
-            proj_s = blas.matmul_split3(wp, blas.split3(x3)) if op.split3 else torch.matmul(w, x3)
+            proj_s = blas.matmul_split3(wp, blas.split3_act(x3)) if op.split3 else torch.matmul(w, x3)
             rh = hist.index_select(1, rows).contiguous() if r > 0 else None
             u_s, fq_s = ops.featurize(proj_s, ft, rhist=rh)
             ks = []
@@ -850,6 +859,8 @@ class HyenaCP:
                 m = u.shape[-1]
                 if op.li_modes is not None and m % 4096 == 0:
                     slab_conv = _li_slab_conv(op, events)
+                elif op.li_scan_modes is not None:
+                    slab_conv = _li_scan_slab_conv(op)
                 else:
                     slab_conv = None  # materialised taps, direct conv on the natural-order slab
                 conv = torch.stack([a2a_conv(u[b].contiguous(), self.cfg.inner, grp, conv_slab=slab_conv)
@@ -885,6 +896,19 @@ def _li_slab_conv(op, events=None):
             events[1].record()
         return y
     conv.segmented = True
+    return conv
+
+
+def _li_scan_slab_conv(op):
+    """Implicit long conv of a natural-order channel slab by the modal scan (hy_li_scan_fwd:
+    fp32 / fp64 slabs, > 8 poles, shards that are not multiples of the tcgen05 tile)."""
+    from . import ops
+    res, poles = op.li_scan_modes
+
+    def conv(natural, slab_groups):
+        g0 = _group_index(op.cfg.inner, slab_groups)
+        ng = slab_groups.n_groups
+        return ops.li_scan(natural.contiguous(), res[g0:g0 + ng], poles[g0:g0 + ng], slab_groups.group_size)
     return conv
 
 

@@ -1,0 +1,325 @@
+// Hyena-LI long convolution as an exact modal state scan on CUDA cores (any dtype, any pole count).
+//
+// The implicit filter h_t = sum_n R_n lam_n^t (core.py:147-151) makes the causal conv
+// (fft.py:128-145 in the reference, O(L log L) per channel) a sum of first-order recurrences:
+//
+//     y[t] = sum_n R_n s_n[t],   s_n[t] = lam_n s_n[t-1] + u[t],   u = k * v,   out = q * y
+//
+// exact in exact arithmetic (no FFT, no length-L filter). This kernel is the reference-precision
+// path (fp32; also fp64, and bf16 with more than 8 poles), where the tcgen05 kernel's bf16
+// operands / tf32 state MMA would miss the fp32 bar. HBM-bound: q, k, v in, y out, once.
+//
+// Work decomposition: one CTA (8 warps) walks whole rows (b, c); a row is cut into tiles of
+// 256 lanes x S consecutive steps. Per tile and block of 8 modes:
+//   1. each lane runs the recurrence over its S steps from zero -> its segment's end state b_l;
+//   2. warp inclusive scan over lanes (Kogge-Stone, multiplier lam^(S d) at offset d);
+//   3. warp totals through shared memory; each warp's incoming state is
+//      lam^(32 S w) C + sum_{w' < w} lam^(32 S (w - 1 - w')) T_w'   (fp64), C = the state
+//      carried into the tile (fp64, updated once per tile);
+//   4. each lane's incoming state lam^(S l) in_w + I_{l-1}; the recurrence is re-run from it and
+//      R_n s_n[t] accumulated into y.
+// Powers of lam are evaluated in fp64 once per row (pow with integer exponents: exact sign,
+// 0^0 = 1 as numpy); states are fp32 for fp32 / bf16 rows, fp64 for fp64 rows.
+#include "common.cuh"
+
+namespace hy {
+namespace lis {
+
+constexpr int WARPS = 8, THREADS = WARPS * 32;
+constexpr int MB = 8;     // modes per register block
+constexpr int MAXP = 64;  // poles per group
+
+template <typename T> struct Cfg;
+template <> struct Cfg<float> {
+  using A = float;
+  static constexpr int S = 16;
+};
+template <> struct Cfg<__nv_bfloat16> {
+  using A = float;
+  static constexpr int S = 16;
+};
+template <> struct Cfg<double> {
+  using A = double;
+  static constexpr int S = 8;
+};
+
+template <typename T, int S, bool VEC>
+__device__ __forceinline__ void load_seg(const T* __restrict__ p, int nv, typename Cfg<T>::A* out) {
+  if (VEC && nv == S) {
+    constexpr int PER = 16 / static_cast<int>(sizeof(T));
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) {
+      const int4 raw = __ldcs(reinterpret_cast<const int4*>(p) + i);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) out[i * PER + j] = Elem<T>::to_a(e[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < S; ++j) out[j] = j < nv ? Elem<T>::to_a(p[j]) : typename Cfg<T>::A(0);
+  }
+}
+
+// steps [t - 8, t + S) of a row of length L into out[0 .. S + 8) (zeros outside [0, L))
+template <typename T, int S, bool VEC>
+__device__ __forceinline__ void load_halo_seg(const T* __restrict__ row, int t, int L, typename Cfg<T>::A* out) {
+  using A = typename Cfg<T>::A;
+  constexpr int PER = 16 / static_cast<int>(sizeof(T));
+  if (VEC && t >= 8 && t + S <= L) {
+#pragma unroll
+    for (int i = 0; i < (S + 8) / PER; ++i) {
+      const int4 raw = __ldg(reinterpret_cast<const int4*>(row + t - 8) + i);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) out[i * PER + j] = Elem<T>::to_a(e[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < S + 8; ++j) {
+      const int tt = t - 8 + j;
+      out[j] = (tt >= 0 && tt < L) ? Elem<T>::to_a(row[tt]) : A(0);
+    }
+  }
+}
+
+// featurizer FIR (hyena.py:122-126, lhf <= 8 taps zero padded to 8) over S outputs
+template <typename A, int S>
+__device__ __forceinline__ void fir8(const A* raw, const A* h, A* out) {
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    A acc = A(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = fma(h[j], raw[8 + t - j], acc);
+    out[t] = acc;
+  }
+}
+
+template <typename T, int S, bool VEC>
+__device__ __forceinline__ void store_seg(T* __restrict__ p, int nv, const typename Cfg<T>::A* in) {
+  if (VEC && nv == S) {
+    constexpr int PER = 16 / static_cast<int>(sizeof(T));
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) {
+      int4 raw;
+      T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) e[j] = Elem<T>::from_a(in[i * PER + j]);
+      __stcs(reinterpret_cast<int4*>(p) + i, raw);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j < nv) p[j] = Elem<T>::from_a(in[j]);
+  }
+}
+
+// FEAT: q, k, v are the raw projections (B, 3C, L) = [q; k; v] rows (`q` points at them), the
+// featurizers (feat_taps (3, C, lhf) fp32, lhf <= 8) run in registers on each lane's segment
+// with its 8-step history read from the row (L1 / L2 hits), so the fused mixer reads every
+// projected row once and writes y once.
+template <typename T, bool VEC, bool FEAT>
+__global__ void __launch_bounds__(THREADS, 2)
+li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ y,
+               const double* __restrict__ res, const double* __restrict__ poles, int np, int gs, int C, int L,
+               long long rows, const float* __restrict__ feat, int lhf) {
+  using A = typename Cfg<T>::A;
+  constexpr int S = Cfg<T>::S;
+  constexpr int TILE = THREADS * S;
+  __shared__ A s_lam[MAXP], s_r[MAXP];
+  __shared__ A s_pk[MAXP][5];           // lam^(S 2^k): the scan multipliers
+  __shared__ A s_pl[MAXP][32];          // lam^(S l): a lane's offset in its warp
+  __shared__ double s_pw[MAXP][WARPS + 1];  // lam^(32 S w): a warp's offset in the tile
+  __shared__ double s_carry[MAXP];      // state entering the tile
+  __shared__ A s_tot[2][WARPS][MB];     // warp totals (double-buffered by block iteration)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = (np + MB - 1) / MB;
+  int it = 0;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int c = static_cast<int>(row % C);
+    const int g = c / gs;
+    A fh[3][8];  // FEAT: this channel's [q, k, v] featurizer taps
+    const T* rq = nullptr;
+    const T* rk = nullptr;
+    const T* rv = nullptr;
+    if constexpr (FEAT) {
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          fh[x][j] = j < lhf ? static_cast<A>(feat[(static_cast<size_t>(x) * C + c) * lhf + j]) : A(0);
+      const long long b = row / C;
+      rq = q + (static_cast<size_t>(b) * 3 * C + c) * L;
+      rk = rq + static_cast<size_t>(C) * L;
+      rv = rk + static_cast<size_t>(C) * L;
+    }
+    __syncthreads();  // the previous row's readers of the tables are done
+    for (int i = threadIdx.x; i < nb * MB * 32; i += THREADS) {
+      const int p = i >> 5, l = i & 31;
+      const double lam = p < np ? poles[static_cast<size_t>(g) * np + p] : 0.0;
+      s_pl[p][l] = static_cast<A>(pow(lam, static_cast<double>(S * l)));
+      if (l < 5) s_pk[p][l] = static_cast<A>(pow(lam, static_cast<double>(S << l)));
+      if (l <= WARPS) s_pw[p][l] = pow(lam, static_cast<double>(32 * S * l));
+      if (l == 0) {
+        s_lam[p] = static_cast<A>(lam);
+        s_r[p] = p < np ? static_cast<A>(res[static_cast<size_t>(g) * np + p]) : A(0);
+        s_carry[p] = 0.0;
+      }
+    }
+    __syncthreads();
+    const size_t base = static_cast<size_t>(row) * L;
+    for (int t0 = 0; t0 < L; t0 += TILE) {
+      const int ts = t0 + threadIdx.x * S;
+      const int nv = max(0, min(S, L - ts));
+      A u[S], yv[S];
+      if constexpr (FEAT) {
+        A raw[S + 8], fk[S];
+        load_halo_seg<T, S, VEC>(rv, ts, L, raw);
+        fir8<A, S>(raw, fh[2], u);
+        load_halo_seg<T, S, VEC>(rk, ts, L, raw);
+        fir8<A, S>(raw, fh[1], fk);
+#pragma unroll
+        for (int j = 0; j < S; ++j) u[j] *= fk[j];
+      } else {
+        load_seg<T, S, VEC>(v + base + ts, nv, u);
+        if (k != nullptr) {
+          A kk[S];
+          load_seg<T, S, VEC>(k + base + ts, nv, kk);
+#pragma unroll
+          for (int j = 0; j < S; ++j) u[j] *= kk[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < S; ++j) yv[j] = A(0);
+      for (int b = 0; b < nb; ++b, ++it) {
+        const int buf = it & 1;
+        A lam[MB], st[MB];
+#pragma unroll
+        for (int n = 0; n < MB; ++n) lam[n] = s_lam[b * MB + n];
+        // 1. segment end state from zero
+#pragma unroll
+        for (int n = 0; n < MB; ++n) {
+          A s = A(0);
+#pragma unroll
+          for (int j = 0; j < S; ++j) s = fma(lam[n], s, u[j]);
+          st[n] = s;
+        }
+        // 2. inclusive scan over the warp's lanes
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) {
+          const int d = 1 << kk;
+#pragma unroll
+          for (int n = 0; n < MB; ++n) {
+            const A o = __shfl_up_sync(0xffffffffu, st[n], d);
+            if (lane >= d) st[n] = fma(s_pk[b * MB + n][kk], o, st[n]);
+          }
+        }
+        if (lane == 31) {
+#pragma unroll
+          for (int n = 0; n < MB; ++n) s_tot[buf][warp][n] = st[n];
+        }
+        __syncthreads();
+        // 3. this warp's incoming state (lane n < MB computes mode n, fp64)
+        A inw_l = A(0);
+        if (lane < MB) {
+          const int p = b * MB + lane;
+          double acc = s_carry[p] * s_pw[p][warp];
+          for (int w = 0; w < warp; ++w) acc += s_pw[p][warp - 1 - w] * static_cast<double>(s_tot[buf][w][lane]);
+          inw_l = static_cast<A>(acc);
+        }
+        // 4. each lane's incoming state, then the recurrence again with the output sum
+#pragma unroll
+        for (int n = 0; n < MB; ++n) {
+          const A inw = __shfl_sync(0xffffffffu, inw_l, n);
+          A ex = __shfl_up_sync(0xffffffffu, st[n], 1);
+          if (lane == 0) ex = A(0);
+          st[n] = fma(s_pl[b * MB + n][lane], inw, ex);
+        }
+        __syncthreads();  // every warp has read s_carry / s_tot[buf]
+        if (warp == 0 && lane < MB) {
+          const int p = b * MB + lane;
+          double acc = s_carry[p] * s_pw[p][WARPS];
+          for (int w = 0; w < WARPS; ++w) acc += s_pw[p][WARPS - 1 - w] * static_cast<double>(s_tot[buf][w][lane]);
+          s_carry[p] = acc;
+        }
+#pragma unroll
+        for (int n = 0; n < MB; ++n) {
+          const A r = s_r[b * MB + n];
+          A s = st[n];
+#pragma unroll
+          for (int j = 0; j < S; ++j) {
+            s = fma(lam[n], s, u[j]);
+            yv[j] = fma(r, s, yv[j]);
+          }
+        }
+      }
+      if constexpr (FEAT) {
+        A raw[S + 8], fq[S];
+        load_halo_seg<T, S, VEC>(rq, ts, L, raw);
+        fir8<A, S>(raw, fh[0], fq);
+#pragma unroll
+        for (int j = 0; j < S; ++j) yv[j] *= fq[j];
+      } else if (q != nullptr) {
+        A qq[S];
+        load_seg<T, S, VEC>(q + base + ts, nv, qq);
+#pragma unroll
+        for (int j = 0; j < S; ++j) yv[j] *= qq[j];
+      }
+      store_seg<T, S, VEC>(y + base + ts, nv, yv);
+    }
+  }
+}
+
+template <typename T, bool FEAT = false>
+int launch(const void* q, const void* k, const void* v, void* y, const double* res, const double* poles, int np,
+           int gs, int B, int C, int L, cudaStream_t st, const float* feat = nullptr, int lhf = 0) {
+  const bool vec = (static_cast<size_t>(L) * sizeof(T)) % 16 == 0 && aligned16(y) && (!v || aligned16(v)) &&
+                   (!q || aligned16(q)) && (!k || aligned16(k));
+  const long long rows = static_cast<long long>(B) * C;
+  auto kern = vec ? li_scan_kernel<T, true, FEAT> : li_scan_kernel<T, false, FEAT>;
+  const long long cap = resident_cap(reinterpret_cast<const void*>(kern), THREADS, 0);
+  const long long grid = rows < cap ? rows : cap;
+  kern<<<static_cast<int>(grid), THREADS, 0, st>>>(static_cast<const T*>(q), static_cast<const T*>(k),
+                                                   static_cast<const T*>(v), static_cast<T*>(y), res, poles, np, gs,
+                                                   C, L, rows, feat, lhf);
+  return check_launch("li_scan_kernel");
+}
+
+}  // namespace lis
+}  // namespace hy
+
+using namespace hy;
+
+extern "C" HY_API int hy_li_scan_fwd(const void* q, const void* k, const void* v, void* y, const double* residues,
+                                     const double* poles, int npoles, int gs, int B, int C, int L, int dtype,
+                                     void* stream) {
+  if (!v || !y || !residues || !poles) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (B < 1 || C < 1 || L < 1 || gs < 1) return fail(HY_ERR_INVALID, "sizes must be >= 1");
+  if (C % gs != 0) return fail(HY_ERR_INVALID, "group_size %d does not divide channel count %d", gs, C);
+  if (npoles < 1 || npoles > lis::MAXP) return fail(HY_ERR_UNSUPPORTED, "modal scan supports 1..%d poles", lis::MAXP);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HY_F32) return lis::launch<float>(q, k, v, y, residues, poles, npoles, gs, B, C, L, st);
+  if (dtype == HY_BF16) return lis::launch<__nv_bfloat16>(q, k, v, y, residues, poles, npoles, gs, B, C, L, st);
+  if (dtype == HY_F64) return lis::launch<double>(q, k, v, y, residues, poles, npoles, gs, B, C, L, st);
+  return fail(HY_ERR_UNSUPPORTED, "hy_li_scan_fwd: unknown dtype %d", dtype);
+}
+
+// Fused LI mixer on the modal scan: featurizers (lhf <= 8) + u = k*v + implicit long conv + q gate
+// from the (B, 3C, L) projections, one pass (hyena.py:162-186 for variant LI).
+extern "C" HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf,
+                                           const double* residues, const double* poles, int npoles, int gs, int B,
+                                           int C, int L, int dtype, void* stream) {
+  if (!proj || !y || !feat_taps || !residues || !poles) return fail(HY_ERR_INVALID, "null pointer argument");
+  if (B < 1 || C < 1 || L < 1 || gs < 1) return fail(HY_ERR_INVALID, "sizes must be >= 1");
+  if (C % gs != 0) return fail(HY_ERR_INVALID, "group_size %d does not divide channel count %d", gs, C);
+  if (lhf < 1 || lhf > 8) return fail(HY_ERR_UNSUPPORTED, "fused modal-scan mixer needs featurizer length <= 8");
+  if (npoles < 1 || npoles > lis::MAXP) return fail(HY_ERR_UNSUPPORTED, "modal scan supports 1..%d poles", lis::MAXP);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == HY_F32)
+    return lis::launch<float, true>(proj, nullptr, nullptr, y, residues, poles, npoles, gs, B, C, L, st, feat_taps, lhf);
+  if (dtype == HY_BF16)
+    return lis::launch<__nv_bfloat16, true>(proj, nullptr, nullptr, y, residues, poles, npoles, gs, B, C, L, st,
+                                            feat_taps, lhf);
+  if (dtype == HY_F64)
+    return lis::launch<double, true>(proj, nullptr, nullptr, y, residues, poles, npoles, gs, B, C, L, st, feat_taps, lhf);
+  return fail(HY_ERR_UNSUPPORTED, "hy_li_scan_mixer_fwd: unknown dtype %d", dtype);
+}

@@ -148,6 +148,8 @@ struct Params {
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
+  int exp_shift;  // debug (HY_TS_SHIFT): T1 . U_prev read as the U buffer one row back (1: base
+                  // offset 0, 2: base offset = (addr >> 7) & 7) -- row-offset descriptor probe
   // implicit, non-fused only: rows stored as L / seg_len time segments, element (row, t) at
   // row * seg_len + (t / seg_len) * seg_stride + t % seg_len (the rank-major layout of an
   // all-to-all buffer); seg_len = 0: plain rows of L. seg_len is a multiple of TILE_T.
@@ -525,7 +527,13 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            mma_bf16_ts(d, t1a + ks * 8, desc_sw128(upa + bo), idesc_main, 1u);
+            uint64_t bd = desc_sw128(upa + bo);
+            if (p.exp_shift) {
+              const uint32_t a = ua - 128 + bo;
+              bd = desc_sw128(a);
+              if (p.exp_shift == 2) bd |= static_cast<uint64_t>((a >> 7) & 7) << 49;
+            }
+            mma_bf16_ts(d, t1a + ks * 8, bd, idesc_main, 1u);
           }
           if (last) mma_commit(t1free);
           mma_commit(&uempty[u]);
@@ -902,6 +910,8 @@ template <bool FEAT, bool GK, bool GQ, bool IMPL = false>
 static int launch(Params p, cudaStream_t st) {
   static const int tr = [] { const char* e = getenv("HY_TS_TRACE"); return e ? atoi(e) : 0; }();
   p.trace = tr;
+  const char* sh = getenv("HY_TS_SHIFT");  // read per launch: the probe flips it between calls
+  p.exp_shift = sh ? atoi(sh) : 0;
   if (p.lhf <= 9) return launch_ks<FEAT, GK, GQ, 1, IMPL>(p, st);
   return launch_ks<FEAT, GK, GQ, 2, IMPL>(p, st);
 }

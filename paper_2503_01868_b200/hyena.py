@@ -37,6 +37,7 @@ from .core import (
 )
 
 VARIANTS = ("SE", "MR", "LI")
+LI_SCAN_MAX_POLES = 64  # hy_li_scan_fwd
 BACKENDS = ("direct", "blocked", "fft")
 MAX_SHORT_FILTER = 14
 
@@ -179,9 +180,20 @@ class HyenaOperator:
         self.lh = inner.filter_len
         self.decay = None
         self.li_modes = None
+        self.li_scan_modes = None
         if isinstance(inner.filters[0], ImplicitFilter):
-            self.inner_taps = None  # materialised lazily (unfused / fp32 / fp64 paths only)
+            self.inner_taps = None  # materialised lazily (short-filter fused path only)
             npoles = {f.poles.size for f in inner.filters}
+            npmax = max(npoles)
+            if npmax <= LI_SCAN_MAX_POLES:
+                # (residues, poles) fp64 for the modal scan (hy_li_scan_fwd): the reference-
+                # precision LI path; ragged pole counts padded with R = 0, lam = 0 modes
+                res = np.zeros((inner.n_groups, npmax))
+                pol = np.zeros((inner.n_groups, npmax))
+                for g, f in enumerate(inner.filters):
+                    res[g, :f.poles.size] = f.residues
+                    pol[g, :f.poles.size] = f.poles
+                self.li_scan_modes = (torch.from_numpy(res).to(self.dev), torch.from_numpy(pol).to(self.dev))
             if dtype == torch.bfloat16 and len(npoles) == 1 and max(npoles) <= 8:
                 # (residues, poles) per group for the tcgen05 implicit-filter kernel
                 self.li_modes = (torch.tensor(np.stack([f.residues for f in inner.filters]), dtype=torch.float32,
@@ -214,6 +226,10 @@ class HyenaOperator:
         if self.li_modes is not None and proj.shape[-1] % 8 == 0:
             return ops.li_mixer(proj, self.feat_taps, self.li_modes[0], self.li_modes[1], self.gs,
                                 packed=self.feat_packed)
+        if self.li_scan_modes is not None and self.lhf <= 8:
+            # LI at the reference's precision (fp32 / fp64), > 8 poles or L % 8 != 0: featurizers,
+            # gates and exact per-mode state scans in one pass (no FFT, no length-L filter)
+            return ops.li_scan_mixer(proj, self.feat_taps, self.li_scan_modes[0], self.li_scan_modes[1], self.gs)
         if fused_mixer_eligible(self.dtype, self.lh, proj.shape[-1]):
             # LI keeps no explicit taps (modal form); a short LI filter is materialised once
             taps = self.inner_taps if self.inner_taps is not None else self.materialized_inner
@@ -223,6 +239,8 @@ class HyenaOperator:
         B, _, L = proj.shape
         feats = ops.causal_conv(proj, self.feat_taps.reshape(3 * D, self.lhf), 1)
         q, k, v = (feats[:, i * D:(i + 1) * D].contiguous() for i in range(3))
+        if self.li_scan_modes is not None:  # featurizers longer than 8 taps: exact modal scans
+            return ops.li_scan(v, self.li_scan_modes[0], self.li_scan_modes[1], self.gs, q=q, k=k)
         if self.lh > 129 or self.cfg.variant == "LI":
             if self.dtype != torch.float64 and getattr(self, "_spec_L", None) != L:
                 # the filter half of the FFT conv is a parameter transform: once per length
@@ -263,14 +281,14 @@ class HyenaOperator:
     def project(self, x3: torch.Tensor) -> torch.Tensor:
         """(B, 3D, L) = W_qkv^T x (hyena.py:122-124)."""
         if self.split3:
-            return blas.matmul_split3(self.w_qkv_parts, blas.split3(x3))
+            return blas.matmul_split3(self.w_qkv_parts, blas.split3_act(x3))
         return torch.matmul(self.w_qkv_t, x3)
 
     def out_project(self, mixed: torch.Tensor, acc: torch.Tensor | None = None) -> torch.Tensor:
         """y = W_out^T mixed (hyena.py:188); with acc: acc += W_out^T mixed in the GEMM epilogue
         (the residual of hyena.py:405), returned."""
         if self.split3:
-            return blas.matmul_split3(self.w_out_parts, blas.split3(mixed), out=acc, accumulate=acc is not None)
+            return blas.matmul_split3(self.w_out_parts, blas.split3_act(mixed), out=acc, accumulate=acc is not None)
         if acc is None:
             return torch.matmul(self.w_out_t, mixed)
         if acc.shape[0] == 1:
@@ -348,8 +366,12 @@ def hyena_forward_saved(x: SeqTensor, cfg: HyenaConfig):
     feats = ops.causal_conv(proj, op.feat_taps.reshape(3 * D, op.lhf), 1)
     q, k, v = (feats[i * D:(i + 1) * D].contiguous() for i in range(3))
     gated = k * v
-    conv_out = ops.long_conv(gated, op.materialized_inner, op.gs) if op.lh > 129 else \
-        ops.gated_conv(gated, op.materialized_inner, op.gs)
+    if op.li_scan_modes is not None:
+        conv_out = ops.li_scan(gated, op.li_scan_modes[0], op.li_scan_modes[1], op.gs)
+    elif op.lh > 129:
+        conv_out = ops.long_conv(gated, op.materialized_inner, op.gs)
+    else:
+        conv_out = ops.gated_conv(gated, op.materialized_inner, op.gs)
     mixed = q * conv_out
     y = op.out_project(mixed.unsqueeze(0))[0] if op.split3 else torch.matmul(op.w_out_t, mixed)
     h = lambda t: t.detach().cpu().numpy().astype(np.float64)  # noqa: E731

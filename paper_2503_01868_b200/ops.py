@@ -275,6 +275,56 @@ def li_conv(v: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_
     return y[0] if squeeze else y
 
 
+def li_scan(v: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_size: int = 1, q=None,
+            k=None) -> torch.Tensor:
+    """y = q * (h conv (k * v)), h_t = sum_n R_n lam_n^t, by exact per-mode state scans on CUDA
+    cores (hy_li_scan_fwd): fp32 / bf16 / fp64 activations, up to 64 poles, any L.
+    residues, poles: (n_groups, n_poles), kept in fp64."""
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    for name, gt in (("q", q3), ("k", k3)):
+        if gt is not None and (gt.shape != v3.shape or gt.dtype != v3.dtype):
+            raise ValueError(f"gate {name} shape/dtype {tuple(gt.shape)}/{gt.dtype} does not match input "
+                             f"{tuple(v3.shape)}/{v3.dtype}")
+    r = residues.to(device=v3.device, dtype=torch.float64).contiguous()
+    p = poles.to(device=v3.device, dtype=torch.float64).contiguous()
+    if r.shape != p.shape or r.dim() != 2:
+        raise ValueError("residues and poles must be matching (n_groups, n_poles) tensors")
+    B, C, L = v3.shape
+    if r.shape[0] * group_size != C:
+        raise ValueError(f"{r.shape[0]} filter groups of size {group_size} do not cover {C} channels")
+    y = torch.empty_like(v3)
+    lib = _lib.load()
+    _lib.check(lib.hy_li_scan_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), r.data_ptr(), p.data_ptr(),
+                                  p.shape[1], group_size, B, C, L, _dtype_code(v3), _stream()), "li_scan")
+    return y[0] if squeeze else y
+
+
+def li_scan_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor,
+                  group_size: int = 1) -> torch.Tensor:
+    """LI mixer on the modal scan (hy_li_scan_mixer_fwd): featurizers (lhf <= 8) + gates + the
+    implicit long conv from the (B, 3C, L) projections in one pass; fp32 / bf16 / fp64."""
+    _check_device(proj)
+    B, C3, L = proj.shape
+    if C3 % 3:
+        raise ValueError("proj must be (B, 3C, L)")
+    C = C3 // 3
+    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    if ft.shape[:2] != (3, C):
+        raise ValueError(f"feat_taps must be (3, {C}, lhf), got {tuple(ft.shape)}")
+    r = residues.to(device=proj.device, dtype=torch.float64).contiguous()
+    p = poles.to(device=proj.device, dtype=torch.float64).contiguous()
+    if r.shape != p.shape or r.dim() != 2 or r.shape[0] * group_size != C:
+        raise ValueError("residues / poles must be matching (n_groups, n_poles) tensors covering the channels")
+    y = torch.empty((B, C, L), device=proj.device, dtype=proj.dtype)
+    lib = _lib.load()
+    _lib.check(lib.hy_li_scan_mixer_fwd(proj.data_ptr(), y.data_ptr(), ft.data_ptr(), ft.shape[-1], r.data_ptr(),
+                                        p.data_ptr(), p.shape[1], group_size, B, C, L, _dtype_code(proj),
+                                        _stream()), "li_scan_mixer")
+    return y
+
+
 def li_conv_segmented(buf: torch.Tensor, residues: torch.Tensor, poles: torch.Tensor, group_size: int = 1,
                       out=None) -> torch.Tensor:
     """Ungated implicit long conv of a (n_seg, C, seg_len) buffer whose row c is the time

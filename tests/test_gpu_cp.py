@@ -72,7 +72,7 @@ def _gather(t: torch.Tensor) -> list:
         parts = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(parts, t)
         return parts
-    h = t.float().cpu()
+    h = t.float().cpu() if t.dtype == torch.bfloat16 else t.cpu()  # bf16 -> fp32 is exact
     parts = [torch.empty_like(h) for _ in range(world)]
     dist.all_gather(parts, h)
     return [p.to(t.device, t.dtype) for p in parts]
@@ -87,7 +87,7 @@ def _run(target, *args):
     procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=900)
+    res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=180)
         assert p.exitcode == 0

@@ -226,3 +226,33 @@ def test_mixer_routing_edge_lengths(variant, dtype, L):
         ocfg[n] = {"channels": g.channels, "group_size": g.group_size, "filters": fl}
     want = oracle.hyena_forward(x, ocfg)
     assert oracle.rel_err(y, want) < (1e-5 if dtype == "f32" else 1e-2)
+
+
+@pytest.mark.parametrize("dtype,L,n_poles", [("f32", 8192, 8), ("f64", 4096, 8), ("bf16", 8192, 12)])
+def test_li_operator_modal_scan_vs_oracle(dtype, L, n_poles):
+    """The LI operator on the modal-scan path: fp32 (the reference's precision; north-star bar
+    1e-5), fp64, and bf16 with more than 8 poles, through the drop-in hyena_forward."""
+    D = 32
+    cfg = hy.make_hyena_config("LI", D, hy.make_rng(8), seq_len=L, backend="fft", n_poles=n_poles)
+    if dtype == "bf16":
+        rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+        feats = {n: hy.GroupSpec(D, 1, tuple(hy.ExplicitFilter(bf16_round(f.taps)) for f in getattr(cfg, n).filters))
+                 for n in ("q_feat", "k_feat", "v_feat")}
+        cfg = hy.HyenaConfig(**{**cfg.__dict__, **rnd, **feats})
+    x = hy.make_rng(9).standard_normal((D, L))
+    if dtype == "bf16":
+        x = bf16_round(x)
+        y = hy.HyenaOperator(cfg, torch.bfloat16).forward(torch.from_numpy(x).to("cuda", torch.bfloat16))
+        y = y.double().cpu().numpy()
+    else:
+        x = x.astype(np.float32) if dtype == "f32" else x
+        y = hy.hyena_forward(hy.SeqTensor(x, dtype), cfg).data
+    ocfg = {"variant": "LI", "width": D, "block_size": 16, "backend": "fft",
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")},
+            **{n: {"channels": D, "group_size": 1, "filters": [("explicit", f.taps) for f in getattr(cfg, n).filters]}
+               for n in ("q_feat", "k_feat", "v_feat")},
+            "inner": {"channels": D, "group_size": 1,
+                      "filters": [("implicit", f.residues, f.poles, L) for f in cfg.inner.filters]}}
+    want = oracle.hyena_forward(x, ocfg)
+    tol = {"f32": 1e-5, "f64": 1e-10, "bf16": 1e-2}[dtype]
+    assert oracle.rel_err(y, want) < tol

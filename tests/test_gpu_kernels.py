@@ -447,3 +447,113 @@ def test_fir_stream_vs_oracle(dtype, B, C, L, lh, gs, gates):
         os.environ.pop("HY_FIR_TILED")
     assert float((y.double() - y2.double()).abs().max()) <= (2e-2 if dtype == "bf16" else 1e-5) * max(
         1.0, float(y2.double().abs().max()))
+
+
+@pytest.mark.parametrize("shape", [(2, 48, 256), (1, 7, 13), (3, 16, 4104)])
+def test_split3_cat_kernel_exact(shape):
+    """hy_split3_cat writes [X1; X2; X0; X1; X0] with X0 + X1 + X2 == x exactly (blas.py)."""
+    from paper_2503_01868_b200 import blas
+    g = torch.Generator(device="cuda").manual_seed(sum(shape))
+    x = torch.randn(shape, device="cuda", generator=g) * torch.logspace(-8, 8, shape[-1], device="cuda")
+    s = blas.split3_act(x)
+    B, K, N = shape
+    parts = s.cat.view(B, 5, K, N)
+    x0, x1, x2 = blas.split3(x)  # the eager restatement
+    assert torch.equal(parts[:, 0], x1) and torch.equal(parts[:, 1], x2) and torch.equal(parts[:, 2], x0)
+    assert torch.equal(parts[:, 3], x1) and torch.equal(parts[:, 4], x0) and torch.equal(s[0], x0)
+    assert torch.equal(x0.double() + x1.double() + x2.double(), x.double())
+
+
+def test_split3_matmul_fp32_parity():
+    """fp32 GEMM through the split kernel + six bf16 products vs fp64, within the fp32 bar."""
+    from paper_2503_01868_b200 import blas
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn((384, 4096), device="cuda", generator=g) / 64
+    x = torch.randn((2, 4096, 512), device="cuda", generator=g)
+    got = blas.matmul_split3(blas.split3_weight(a), blas.split3_act(x))
+    want = torch.matmul(a.double(), x.double())
+    err = float((got.double() - want).abs().max() / max(1.0, float(want.abs().max())))
+    assert err < 1e-5, err
+
+
+# ---------------------------------------------------------------- modal scan (LI at reference precision)
+
+
+@pytest.mark.parametrize("dtype,B,C,L,gs,np_,gated", [
+    ("f32", 1, 4, 8192, 1, 8, True),
+    ("f32", 2, 6, 1000, 2, 3, True),        # ragged L (scalar loads), groups, 3 poles
+    ("f32", 1, 3, 1, 1, 8, False),          # L = 1
+    ("f32", 1, 5, 131072, 1, 8, True),      # config C3's length, tail poles
+    ("f32", 1, 4, 20000, 1, 12, True),      # 12 poles: two mode blocks
+    ("f32", 1, 2, 9000, 1, 64, False),      # 64 poles
+    ("f64", 2, 3, 5000, 1, 8, True),
+    ("f64", 1, 2, 131072, 1, 8, False),
+    ("bf16", 1, 4, 12288, 1, 16, True),     # > 8 poles (the tcgen05 kernel's limit)
+    ("bf16", 1, 3, 1001, 3, 8, True),       # L % 8 != 0
+])
+def test_li_scan_vs_oracle(dtype, B, C, L, gs, np_, gated):
+    """hy_li_scan_fwd against the fp64 oracle's fft_conv on the materialised implicit filter
+    (fft.py:128-145, core.py:147-151): fp32 1e-5 and bf16 1e-2 (north star), fp64 1e-10."""
+    rng = np.random.default_rng(L + C + np_)
+    G = C // gs
+    poles = rng.uniform(-0.95, 0.95, (G, np_))
+    poles[0, :min(np_, 5)] = [1.0, -1.0, 0.9999, -0.9999, 0.0][:min(np_, 5)]
+    residues = rng.standard_normal((G, np_)) / np_
+    rnd = {"f32": lambda a: a.astype(np.float32).astype(np.float64), "f64": lambda a: a, "bf16": bf16_round}[dtype]
+    tdt = {"f32": torch.float32, "f64": torch.float64, "bf16": torch.bfloat16}[dtype]
+    v = rnd(rng.standard_normal((B, C, L)))
+    q = rnd(rng.standard_normal((B, C, L))) if gated else None
+    k = rnd(rng.standard_normal((B, C, L))) if gated else None
+    y = ops.li_scan(dev(v, tdt), torch.from_numpy(residues), torch.from_numpy(poles), gs,
+                    q=None if q is None else dev(q, tdt), k=None if k is None else dev(k, tdt)).double().cpu().numpy()
+    taps = oracle.bank_taps_per_channel(_implicit_bank(residues, poles, L, gs))
+    tol = {"f32": 1e-5, "f64": 1e-10, "bf16": 1e-2}[dtype]
+    for b in range(B):
+        u = v[b] * (k[b] if gated else 1.0)
+        want = oracle.fft_conv(u, taps) * (q[b] if gated else 1.0)
+        err = oracle.rel_err(y[b], want)
+        assert err < tol, (b, err)
+
+
+def test_li_scan_many_rows_and_errors():
+    """More rows than resident CTAs (each CTA re-initialises its tables and carries per row);
+    argument errors map to the reference's exception types."""
+    rng = np.random.default_rng(3)
+    C, L = 700, 4100
+    poles = rng.uniform(-0.99, 0.99, (C, 8))
+    residues = rng.standard_normal((C, 8)) / 8
+    v = rng.standard_normal((1, C, L)).astype(np.float32).astype(np.float64)
+    y = ops.li_scan(dev(v), torch.from_numpy(residues), torch.from_numpy(poles), 1).double().cpu().numpy()
+    sel = [0, 1, 295, 296, 597, 699]
+    taps = oracle.bank_taps_per_channel(_implicit_bank(residues[sel], poles[sel], L, 1))
+    assert oracle.rel_err(y[0][sel], oracle.fft_conv(v[0][sel], taps)) < 1e-5
+    with pytest.raises(NotImplementedError):
+        ops.li_scan(dev(v[:, :4]), torch.zeros((4, 65), dtype=torch.float64), torch.zeros((4, 65), dtype=torch.float64))
+    with pytest.raises(ValueError):
+        ops.li_scan(dev(v[:, :4]), torch.zeros((3, 8), dtype=torch.float64), torch.zeros((3, 8), dtype=torch.float64))
+
+
+@pytest.mark.parametrize("dtype,B,C,L,lhf,np_", [("f32", 2, 5, 8192, 7, 8), ("f32", 1, 3, 1000, 4, 3),
+                                                 ("bf16", 1, 4, 16384, 7, 12), ("f64", 1, 3, 3000, 8, 8),
+                                                 ("f32", 1, 2, 131072, 7, 8)])
+def test_li_scan_mixer_vs_oracle(dtype, B, C, L, lhf, np_):
+    """Fused LI mixer on the modal scan (featurizers + gates + implicit conv from the projections)
+    against the oracle's featurizer convs and fft_conv."""
+    rng = np.random.default_rng(L + lhf + np_)
+    poles = rng.uniform(-0.95, 0.95, (C, np_))
+    poles[0, :3] = [1.0, -0.9999, 0.0]
+    residues = rng.standard_normal((C, np_)) / np_
+    rnd = {"f32": lambda a: a.astype(np.float32).astype(np.float64), "f64": lambda a: a, "bf16": bf16_round}[dtype]
+    tdt = {"f32": torch.float32, "f64": torch.float64, "bf16": torch.bfloat16}[dtype]
+    proj = rnd(rng.standard_normal((B, 3 * C, L)))
+    feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
+    y = ops.li_scan_mixer(dev(proj, tdt), dev(feat), torch.from_numpy(residues), torch.from_numpy(poles), 1)
+    y = y.double().cpu().numpy()
+    taps = oracle.bank_taps_per_channel(_implicit_bank(residues, poles, L, 1))
+    tol = {"f32": 1e-5, "f64": 1e-10, "bf16": 1e-2}[dtype]
+    for b in range(B):
+        fq, fk, fv = (oracle.direct_causal_conv(proj[b, i * C:(i + 1) * C], explicit_bank_from_taps(feat[i], 1))
+                      for i in range(3))
+        want = fq * oracle.fft_conv(fk * fv, taps)
+        err = oracle.rel_err(y[b], want)
+        assert err < tol, (b, err)
