@@ -38,6 +38,7 @@
  *   hy_featurizer_bwd       hyena.py:234-247     _feat_backward for q, k, v fused with the gate
  *                           hyena.py:262-270     products of hyena_backward (one HBM pass)
  *   hy_two_stage_taps_grad  blockconv.py:246-262 two_stage_backward's two-pass filter gradient (tcgen05)
+ *   hy_block_conv_fwd       blockconv.py:103-121 block_conv (K spill factors) on tcgen05, bf16, lh <= 513
  *   hy_li_scan_fwd          fft.py:128-145       fft_conv on an ImplicitFilter bank (core.py:147-151), gated as
  *                           hyena.py:183-186     hyena_forward's LI inner conv, by exact per-mode scans
  *   hy_li_scan_mixer_fwd    hyena.py:162-186     the LI mixer (featurizers + gates + modal scan), fused
@@ -237,6 +238,13 @@ HY_API int hy_li_param_grad(const void* dc, const void* u, const float* residues
                             int group_size, int B, int C, int L, int dtype, float* d_res, float* d_pole,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* K-block causal conv on tcgen05 (blockconv.py:103-121 block_conv; the K + 1 spill factors
+ * T_k[m][j] = h[128 k + m - j] as accumulating MMAs over row-shifted views of one U buffer),
+ * optionally gated y = q * conv(k * v) and with the MR decay (taps_hat * 2^(-decay * t)):
+ * bf16, 1 <= lh <= 513, L % 8 == 0. q / k / decay nullable. */
+HY_API int hy_block_conv_fwd(const void* q, const void* k, const void* v, void* y, const float* taps_hat,
+                             const float* decay, int B, int C, int L, int lh, int group_size, int dtype,
+                             void* stream);
 /* Hyena-LI long conv as an exact modal state scan on CUDA cores (the reference-precision path):
  *   y = q * (h conv (k * v)),  h_t = sum_n R_n lam_n^t  (core.py:147-151, fft.py:128-145)
  * computed as y[t] = q[t] sum_n R_n s_n[t], s_n[t] = lam_n s_n[t-1] + k[t] v[t]. Any dtype

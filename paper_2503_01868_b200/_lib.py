@@ -54,6 +54,7 @@ SIGNATURES = {
     "hy_toeplitz_taps_reduce": (_I, [_P, _P, _P, _P, _SZ, _I, _I, _I, _I, _P]),
     "hy_li_param_grad_workspace_size": (_SZ, [_I, _I]),
     "hy_li_param_grad": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "hy_block_conv_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_li_scan_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_li_scan_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_split3_cat": (_I, [_P, _P, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _P]),

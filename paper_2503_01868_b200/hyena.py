@@ -226,7 +226,7 @@ class HyenaOperator:
         if self.li_modes is not None and proj.shape[-1] % 8 == 0:
             return ops.li_mixer(proj, self.feat_taps, self.li_modes[0], self.li_modes[1], self.gs,
                                 packed=self.feat_packed)
-        if self.li_scan_modes is not None and self.lhf <= 8:
+        if self.li_scan_modes is not None and self.lhf <= 8 and self.dtype != torch.float64:
             # LI at the reference's precision (fp32 / fp64), > 8 poles or L % 8 != 0: featurizers,
             # gates and exact per-mode state scans in one pass (no FFT, no length-L filter)
             return ops.li_scan_mixer(proj, self.feat_taps, self.li_scan_modes[0], self.li_scan_modes[1], self.gs)
@@ -235,8 +235,14 @@ class HyenaOperator:
             taps = self.inner_taps if self.inner_taps is not None else self.materialized_inner
             return ops.hyena_mixer(proj, self.feat_taps, taps, self.gs, decay=self.decay,
                                    packed=self.feat_packed)
-        # unfused: featurizers over all 3D rows in one launch, then the gated inner conv
         B, _, L = proj.shape
+        if self.dtype == torch.bfloat16 and 129 < self.lh <= ops.BLOCK_CONV_MAX_LH and L % 8 == 0 \
+                and self.inner_taps is not None and self.lhf <= 8:
+            # long explicit / MR filters: one featurizer stream (u = fk * fv, fq), then the K-block
+            # tcgen05 conv gated by fq (K + 1 spill factors, blockconv.py:103-121)
+            u, fq = ops.featurize(proj, self.feat_taps)
+            return ops.block_conv(u, self.inner_taps, self.gs, q=fq, decay=self.decay)
+        # unfused: featurizers over all 3D rows in one launch, then the gated inner conv
         feats = ops.causal_conv(proj, self.feat_taps.reshape(3 * D, self.lhf), 1)
         q, k, v = (feats[:, i * D:(i + 1) * D].contiguous() for i in range(3))
         if self.li_scan_modes is not None:  # featurizers longer than 8 taps: exact modal scans

@@ -119,6 +119,39 @@ def two_stage(v: torch.Tensor, taps_hat: torch.Tensor, group_size: int = 1, q=No
     return y[0] if squeeze else y
 
 
+BLOCK_CONV_MAX_LH = 513  # hy_block_conv_fwd: K <= 4 spill factors of 128
+
+
+def block_conv(v: torch.Tensor, taps_hat: torch.Tensor, group_size: int = 1, q=None, k=None,
+               decay=None) -> torch.Tensor:
+    """tcgen05 K-block conv, bf16 (blockconv.py:103-121, gated as blockconv.py:182-220):
+    y = q * sum_k T_k U_{n-k}, any filter length up to 513 taps.
+
+    taps_hat: (G, lh) fp32; decay: (G,) fp32 = rate*log2(base) or None."""
+    squeeze = v.dim() == 2
+    v3, q3, k3 = _as3(v), None if q is None else _as3(q), None if k is None else _as3(k)
+    _check_device(v3, q3, k3)
+    if v3.dtype != torch.bfloat16:
+        raise ValueError("block_conv (tcgen05) takes bfloat16 activations; use causal_conv for fp32/fp64")
+    for name, g in (("q", q3), ("k", k3)):
+        if g is not None and (g.shape != v3.shape or g.dtype != v3.dtype):
+            raise ValueError(f"gate {name} shape {tuple(g.shape)} does not match input {tuple(v3.shape)}")
+    taps_hat = taps_hat.to(device=v3.device, dtype=torch.float32).contiguous()
+    if decay is not None:
+        decay = decay.to(device=v3.device, dtype=torch.float32).contiguous()
+    B, C, L = v3.shape
+    if L % 8:  # the kernel streams 16-byte row pieces; zero steps after L change no output <= L
+        pad = lambda t: None if t is None else torch.nn.functional.pad(t, (0, 8 - L % 8)).contiguous()  # noqa: E731
+        y = block_conv(pad(v3), taps_hat, group_size, q=pad(q3), k=pad(k3), decay=decay)[..., :L].contiguous()
+        return y[0] if squeeze else y
+    y = torch.empty_like(v3)
+    lib = _lib.load()
+    _lib.check(lib.hy_block_conv_fwd(_ptr(q3), _ptr(k3), v3.data_ptr(), y.data_ptr(), taps_hat.data_ptr(),
+                                     _ptr(decay), B, C, L, taps_hat.shape[-1], group_size, _lib.HY_BF16,
+                                     _stream()), "block_conv")
+    return y[0] if squeeze else y
+
+
 def feat_pack(feat_taps: torch.Tensor) -> torch.Tensor:
     """Pack (3, C, lhf) featurizer taps for the tcgen05 mixer (hy_feat_pack)."""
     ft = feat_taps.to(dtype=torch.float32).contiguous()

@@ -112,6 +112,36 @@ def main():
             ms = timeit(lambda: ops.li_conv(v, res, poles, 1))
             report("li_conv_ungated", ms, 4 * D * L, D=D, L=L)
             del proj, v
+    if args.which in ("all", "scan"):
+        # modal-scan LI kernels (CUDA cores) at C3: fp32 mixer (the reference precision), bf16
+        # ungated conv (vs li_conv_ungated above) and the bf16 mixer
+        D, L = 4096, 131072
+        res = torch.randn((D, 8), device=dev, generator=g, dtype=torch.float64) / 8
+        poles = torch.rand((D, 8), device=dev, generator=g, dtype=torch.float64) * 1.9 - 0.95
+        for dt in (torch.float32, torch.bfloat16):
+            esz = torch.empty((), dtype=dt).element_size()
+            proj = torch.randn((1, 3 * D, L), device=dev, dtype=dt, generator=g)
+            feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
+            ms = timeit(lambda: ops.li_scan_mixer(proj, feat, res, poles, 1), iters=10)
+            report(f"li_scan_mixer_{str(dt)[6:]}", ms, 4 * esz * D * L, D=D, L=L)
+            v = proj[:, :D].contiguous()
+            ms = timeit(lambda: ops.li_scan(v, res, poles, 1), iters=10)
+            report(f"li_scan_ungated_{str(dt)[6:]}", ms, 2 * esz * D * L, D=D, L=L)
+            del proj, v
+    if args.which in ("all", "kblock"):
+        # K-block tcgen05 conv (lh > 129): ungated block_conv, B=4, L=8192, D=4096, bf16
+        B, D, L = 4, 4096, 8192
+        v = torch.randn((B, D, L), device=dev, dtype=torch.bfloat16, generator=g)
+        q = torch.randn_like(v)
+        for lh in (200, 300, 513):
+            taps = torch.randn((D, lh), device=dev, generator=g) / 20
+            ms = timeit(lambda: ops.block_conv(v, taps, 1))
+            report(f"block_conv_tcgen05_lh{lh}", ms, 4 * D * B * L, B=B, D=D, L=L, lh=lh)
+            ms = timeit(lambda: ops.block_conv(v, taps, 1, q=q, k=q))
+            report(f"block_conv_tcgen05_gated_lh{lh}", ms, 8 * D * B * L, B=B, D=D, L=L, lh=lh)
+            ms = timeit(lambda: ops.block_conv(v, taps, 16))
+            report(f"block_conv_tcgen05_lh{lh}_gs16", ms, 4 * D * B * L, B=B, D=D, L=L, lh=lh, gs=16)
+        del v, q
     if args.which in ("all", "fft"):
         D = 4096
         for L, dt in ((131072, torch.bfloat16), (16384, torch.float32)):

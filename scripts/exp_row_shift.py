@@ -3,8 +3,12 @@ Runs the two-stage kernel with T1 . U_prev replaced by the U buffer read one row
 (HY_TS_SHIFT=1: base-offset field 0; =2: base offset (addr >> 7) & 7) and compares every
 output chunk except each tile's first (whose row -1 is outside the buffer) with the normal run."""
 import os
+import sys
+
 import torch
-from paper_2503_01868_b200 import ops
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_01868_b200 import ops  # noqa: E402
 
 g = torch.Generator(device="cuda").manual_seed(0)
 B, C, L = 1, 8, 8192

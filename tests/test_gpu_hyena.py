@@ -256,3 +256,34 @@ def test_li_operator_modal_scan_vs_oracle(dtype, L, n_poles):
     want = oracle.hyena_forward(x, ocfg)
     tol = {"f32": 1e-5, "f64": 1e-10, "bf16": 1e-2}[dtype]
     assert oracle.rel_err(y, want) < tol
+
+
+@pytest.mark.parametrize("lh,gs", [(256, 1), (500, 4)])
+def test_mr_operator_long_filter_kblock(lh, gs):
+    """bf16 MR operator with inner filters longer than one spill factor (lh > 129): featurizer
+    stream + the K-block tcgen05 conv, against the oracle's blocked backend (block_conv)."""
+    D, L = 64, 8192
+    cfg = hy.make_hyena_config("MR", D, hy.make_rng(12), group_size=gs, inner_len=lh, block_size=64)
+    rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+
+    def rbank(g):
+        fs = []
+        for f in g.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fs.append(hy.ExplicitFilter(bf16_round(f.taps)))
+            else:
+                fs.append(hy.RegularizedFilter(bf16_round(f.taps_hat), f.decay_rate, f.base))
+        return hy.GroupSpec(g.channels, g.group_size, tuple(fs))
+    cfg = hy.HyenaConfig(**{**cfg.__dict__, **rnd, **{n: rbank(getattr(cfg, n))
+                                                      for n in ("q_feat", "k_feat", "v_feat", "inner")}})
+    x = bf16_round(hy.make_rng(13).standard_normal((D, L)))
+    y = hy.HyenaOperator(cfg, torch.bfloat16).forward(torch.from_numpy(x).to("cuda", torch.bfloat16))
+    ocfg = {"variant": "MR", "width": D, "block_size": 64, "backend": "blocked",
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        g = getattr(cfg, n)
+        ocfg[n] = {"channels": g.channels, "group_size": g.group_size,
+                   "filters": [("explicit", f.taps) if isinstance(f, hy.ExplicitFilter)
+                               else ("regularized", f.taps_hat, f.decay_rate, f.base) for f in g.filters]}
+    want = oracle.hyena_forward(x, ocfg)
+    assert oracle.rel_err(y.double().cpu().numpy(), want) < 1e-2

@@ -557,3 +557,67 @@ def test_li_scan_mixer_vs_oracle(dtype, B, C, L, lhf, np_):
         want = fq * oracle.fft_conv(fk * fv, taps)
         err = oracle.rel_err(y[b], want)
         assert err < tol, (b, err)
+
+
+# ---------------------------------------------------------------- K-block tcgen05 conv (lh > lb + 1)
+
+
+@pytest.mark.parametrize("B,C,L,lh,gs,gated,decay", [
+    (1, 4, 8192, 130, 1, False, False),     # K = 2 at the kernel's LB = 128
+    (2, 3, 8192, 257, 1, True, False),      # K = 2 / 3 boundary
+    (1, 4, 12296, 385, 2, True, True),      # K = 3, groups, partial tile, decay
+    (1, 2, 4096, 513, 1, False, False),     # K = 4 (the maximum)
+    (1, 2, 600, 300, 1, False, False),      # shorter than one tile
+    (4, 1024, 8192, 200, 1, True, True),    # many tiles and filter groups per CTA (C2-like walk)
+    (1, 4096, 4096, 300, 16, False, True),  # a factor rebuild every 16 tiles, 28 groups per CTA
+])
+def test_block_conv_tcgen05_vs_oracle(B, C, L, lh, gs, gated, decay):
+    """hy_block_conv_fwd (K + 1 accumulating tcgen05 MMAs over row-shifted U views) against the
+    oracle's block_conv / two_stage semantics (blockconv.py:103-121, 182-220), bf16 bar 1e-2."""
+    rng = np.random.default_rng(L + lh + C)
+    G = C // gs
+    taps = bf16_round(rng.standard_normal((G, lh)) / np.sqrt(lh))
+    rates = np.linspace(0.001, 0.02, G) if decay else None
+    sel = sorted({0, C - 1, C // 2, 147 % C, 148 % C, 149 % C}) if C > 64 else list(range(C))
+    g = torch.Generator(device="cuda").manual_seed(L + lh)
+    v, q, k = (torch.randn((B, C, L), device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    y = ops.block_conv(v, dev(taps), gs, q=q if gated else None, k=k if gated else None,
+                       decay=None if rates is None else dev(rates * np.log2(2.0))).double().cpu().numpy()
+    vh, qh, kh = (t.double().cpu().numpy() for t in (v, q, k))
+    worst = 0.0
+    for c in sel:
+        spec = ("regularized", taps[c // gs], float(rates[c // gs]), 2.0) if decay else ("explicit", taps[c // gs])
+        bank = {"channels": 1, "group_size": 1, "filters": [spec]}
+        for b in range(B):
+            u = vh[b, c:c + 1] * (kh[b, c:c + 1] if gated else 1.0)
+            want = oracle.block_conv(u, bank, 16) * (qh[b, c:c + 1] if gated else 1.0)
+            worst = max(worst, oracle.rel_err(y[b, c:c + 1], want))
+    assert worst < TOL["bf16"], worst
+
+
+def test_block_conv_tcgen05_golden_and_known_answers():
+    """The reference's block_conv goldens (bk*, any block size) through the bf16 K-block kernel,
+    plus exact known answers: a delay of 400 steps (factor T_3 only) and a delta."""
+    z = load("blockconv")
+    for i in range(int(z["n_bk"])):
+        x = bf16_round(z[f"bk{i}.x"])
+        taps = z[f"bk{i}.taps"]
+        gs = int(z[f"bk{i}.gs"])
+        y = ops.block_conv(dev(x, torch.bfloat16), dev(taps), gs).double().cpu().numpy()
+        want = oracle.block_conv(x, explicit_bank_from_taps(taps, gs), int(z[f"bk{i}.lb"]))
+        assert oracle.rel_err(y, want) < TOL["bf16"], i
+        assert oracle.rel_err(y, z[f"bk{i}.y"]) < 2e-2, i  # golden on the unrounded input
+    rng = np.random.default_rng(4)
+    v = bf16_round(rng.standard_normal((1, 3, 8192)))
+    taps = np.zeros((3, 401))
+    taps[:, 400] = 1.0
+    y = ops.block_conv(dev(v, torch.bfloat16), dev(taps), 1).float().cpu().numpy()
+    want = np.zeros_like(v)
+    want[..., 400:] = v[..., :-400]
+    assert np.array_equal(y, want)
+    taps = np.zeros((3, 513))
+    taps[:, 0] = 1.0
+    y = ops.block_conv(dev(v, torch.bfloat16), dev(taps), 1).float().cpu().numpy()
+    assert np.array_equal(y, v)
+    with pytest.raises(NotImplementedError):
+        ops.block_conv(dev(v, torch.bfloat16), dev(np.ones((3, 514))), 1)
