@@ -255,8 +255,9 @@ HY_API int hy_li_scan_fwd(const void* q, const void* k, const void* v, void* y, 
                           void* stream);
 /* The same modal scan fused with the featurizers (lhf <= 8) and gates: the LI mixer from the
  * projections proj (B, 3C, L) = [q; k; v] rows, y = Fq(pq) * (h conv (Fk(pk) * Fv(pv)))
- * (hyena.py:162-186), one pass. feat_taps fp32 (3, C, lhf); residues, poles fp64. */
-HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const double* residues,
+ * (hyena.py:162-186), one pass. feat_taps (3, C, lhf): fp32 for fp32 / bf16 rows, fp64 for fp64;
+ * residues, poles fp64. */
+HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf, const double* residues,
                                 const double* poles, int npoles, int group_size, int B, int C, int L, int dtype,
                                 void* stream);
 /* fp32 activation -> the K-concatenated bf16 operand of the split-bf16 fp32 GEMM (blas.py; the

@@ -16,4 +16,8 @@ int fft_fast_conv_spec(const void* q, const void* k, const void* v, void* y, con
 bool fir_stream_eligible(const void* q, const void* k, const void* v, const void* y, int lh, int L, int dtype);
 int fir_stream_fwd(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L,
                    int lh, int gs, int dtype, void* stream);
+// implicit-filter long conv on the staged-row tcgen05 kernel (block_conv_sm100.cu): 64-chunk
+// tiles; seg_len = 0 (plain rows) or a multiple of 8192
+int li_conv_tc_fwd(const void* q, const void* k, const void* v, void* y, const float* residues, const float* poles,
+                   int npoles, int gs, int B, int C, int L, int seg_len, long long seg_stride, void* stream);
 }  // namespace hy

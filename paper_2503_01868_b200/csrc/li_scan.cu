@@ -20,6 +20,8 @@
 //      R_n s_n[t] accumulated into y.
 // Powers of lam are evaluated in fp64 once per row (pow with integer exponents: exact sign,
 // 0^0 = 1 as numpy); states are fp32 for fp32 / bf16 rows, fp64 for fp64 rows.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace hy {
@@ -121,7 +123,10 @@ template <typename T, bool VEC, bool FEAT>
 __global__ void __launch_bounds__(THREADS, 2)
 li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ y,
                const double* __restrict__ res, const double* __restrict__ poles, int np, int gs, int C, int L,
-               long long rows, const float* __restrict__ feat, int lhf) {
+               long long rows, const void* __restrict__ feat_raw, int lhf) {
+  // featurizer taps: fp32 for fp32 / bf16 rows, fp64 for fp64 rows (the header's tap convention)
+  using FT = typename std::conditional<sizeof(T) == 8, double, float>::type;
+  const FT* feat = static_cast<const FT*>(feat_raw);
   using A = typename Cfg<T>::A;
   constexpr int S = Cfg<T>::S;
   constexpr int TILE = THREADS * S;
@@ -271,7 +276,7 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
 
 template <typename T, bool FEAT = false>
 int launch(const void* q, const void* k, const void* v, void* y, const double* res, const double* poles, int np,
-           int gs, int B, int C, int L, cudaStream_t st, const float* feat = nullptr, int lhf = 0) {
+           int gs, int B, int C, int L, cudaStream_t st, const void* feat = nullptr, int lhf = 0) {
   const bool vec = (static_cast<size_t>(L) * sizeof(T)) % 16 == 0 && aligned16(y) && (!v || aligned16(v)) &&
                    (!q || aligned16(q)) && (!k || aligned16(k));
   const long long rows = static_cast<long long>(B) * C;
@@ -305,7 +310,7 @@ extern "C" HY_API int hy_li_scan_fwd(const void* q, const void* k, const void* v
 
 // Fused LI mixer on the modal scan: featurizers (lhf <= 8) + u = k*v + implicit long conv + q gate
 // from the (B, 3C, L) projections, one pass (hyena.py:162-186 for variant LI).
-extern "C" HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const float* feat_taps, int lhf,
+extern "C" HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf,
                                            const double* residues, const double* poles, int npoles, int gs, int B,
                                            int C, int L, int dtype, void* stream) {
   if (!proj || !y || !feat_taps || !residues || !poles) return fail(HY_ERR_INVALID, "null pointer argument");

@@ -984,6 +984,13 @@ int hy::mr_mixer_fwd(const void* proj, void* y, const float* feat_taps, const vo
 
 // ---------------------------------------------------------------- implicit long filter (Hyena-LI)
 
+// HY_LI_LEGACY=1 keeps the ungated / gated implicit conv on the 32-chunk FEAT-capable kernel
+// (the mixer always runs there: its featurizers need the staged raw windows)
+static bool legacy_li() {
+  static const bool v = [] { const char* e = getenv("HY_LI_LEGACY"); return e && atoi(e) != 0; }();
+  return v;
+}
+
 static int check_impl(const void* residues, const void* poles, int npoles, int B, int C, int L, int gs) {
   if (!residues || !poles) return fail(HY_ERR_INVALID, "null residues / poles");
   if (npoles < 1 || npoles > ts::NPOLE) return fail(HY_ERR_UNSUPPORTED, "implicit filter needs 1..%d poles", ts::NPOLE);
@@ -1026,6 +1033,8 @@ extern "C" HY_API int hy_li_conv_fwd(const void* q, const void* k, const void* v
   if (s != HY_OK) return s;
   if (!aligned16(v) || !aligned16(y) || (q && !aligned16(q)) || (k && !aligned16(k)))
     return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  if (!legacy_li())  // 64-chunk tiles, deep staging ring (block_conv_sm100.cu)
+    return li_conv_tc_fwd(q, k, v, y, residues, poles, npoles, gs, B, C, L, 0, 0, stream);
   ts::Params p{};
   p.q = static_cast<const ts::bf16*>(q);
   p.k = static_cast<const ts::bf16*>(k);
@@ -1060,6 +1069,8 @@ extern "C" HY_API int hy_li_conv_segmented_fwd(const void* v, void* y, const flo
   if (seg_stride < static_cast<long long>(C) * seg_len)
     return fail(HY_ERR_INVALID, "segment stride %lld overlaps the %d rows of a segment", seg_stride, C);
   if (!aligned16(v) || !aligned16(y)) return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  if (!legacy_li() && seg_len % 8192 == 0)
+    return li_conv_tc_fwd(nullptr, nullptr, v, y, residues, poles, npoles, gs, 1, C, L, seg_len, seg_stride, stream);
   ts::Params p{};
   p.v = static_cast<const ts::bf16*>(v);
   p.y = static_cast<ts::bf16*>(y);

@@ -226,7 +226,7 @@ class HyenaOperator:
         if self.li_modes is not None and proj.shape[-1] % 8 == 0:
             return ops.li_mixer(proj, self.feat_taps, self.li_modes[0], self.li_modes[1], self.gs,
                                 packed=self.feat_packed)
-        if self.li_scan_modes is not None and self.lhf <= 8 and self.dtype != torch.float64:
+        if self.li_scan_modes is not None and self.lhf <= 8:
             # LI at the reference's precision (fp32 / fp64), > 8 poles or L % 8 != 0: featurizers,
             # gates and exact per-mode state scans in one pass (no FFT, no length-L filter)
             return ops.li_scan_mixer(proj, self.feat_taps, self.li_scan_modes[0], self.li_scan_modes[1], self.gs)

@@ -343,7 +343,7 @@ def li_scan_mixer(proj: torch.Tensor, feat_taps: torch.Tensor, residues: torch.T
     if C3 % 3:
         raise ValueError("proj must be (B, 3C, L)")
     C = C3 // 3
-    ft = feat_taps.to(device=proj.device, dtype=torch.float32).contiguous()
+    ft = feat_taps.to(device=proj.device, dtype=tap_dtype(proj.dtype)).contiguous()
     if ft.shape[:2] != (3, C):
         raise ValueError(f"feat_taps must be (3, {C}, lhf), got {tuple(ft.shape)}")
     r = residues.to(device=proj.device, dtype=torch.float64).contiguous()
