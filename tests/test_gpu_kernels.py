@@ -547,7 +547,8 @@ def test_li_scan_mixer_vs_oracle(dtype, B, C, L, lhf, np_):
     tdt = {"f32": torch.float32, "f64": torch.float64, "bf16": torch.bfloat16}[dtype]
     proj = rnd(rng.standard_normal((B, 3 * C, L)))
     feat = rnd(rng.standard_normal((3, C, lhf)) / np.sqrt(lhf))
-    y = ops.li_scan_mixer(dev(proj, tdt), dev(feat), torch.from_numpy(residues), torch.from_numpy(poles), 1)
+    y = ops.li_scan_mixer(dev(proj, tdt), dev(feat, torch.float64 if dtype == "f64" else torch.float32),
+                          torch.from_numpy(residues), torch.from_numpy(poles), 1)
     y = y.double().cpu().numpy()
     taps = oracle.bank_taps_per_channel(_implicit_bank(residues, poles, L, 1))
     tol = {"f32": 1e-5, "f64": 1e-10, "bf16": 1e-2}[dtype]
