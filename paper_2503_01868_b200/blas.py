@@ -14,8 +14,10 @@ K (Split3.cat, K' = 5K); the leading term A0 @ B0 follows, accumulated into the 
 output (cuBLAS beta = 1). The error is set by the fp32 accumulation inside a long-K
 tensor-core GEMM, so the leading term is accumulated in K chunks with fp32 adds between them.
 Measured on B200 at the C1 projection (M = 12288, K = N = 4096, `scripts/split3_err.py`):
-one K = 4096 pass 5.8e-6 relative to max, chunks of 2048 2.8e-6 (used: 1.73 ms), of 1024
-1.3e-6 (1.85 ms); cuBLAS's CUDA-core fp32 GEMM: 3.0e-6 at 6.27 ms.
+one K = 4096 pass 5.8e-6 relative to max, chunks of 2048 2.8e-6 (1.73 ms), of 1024 1.3e-6
+(1.85 ms, used: the operator composes two GEMMs and three gated rows, and with 2048-chunks the
+C1 / fp32-C3 operator parity measured 8.5-8.8e-6 against the 1e-5 bar); cuBLAS's CUDA-core
+fp32 GEMM: 3.0e-6 at 6.27 ms.
 """
 
 from __future__ import annotations
@@ -23,7 +25,7 @@ from __future__ import annotations
 import torch
 
 _PAIRS = ((1, 1), (0, 2), (2, 0), (0, 1), (1, 0))  # smallest terms first; A0 @ B0 last, K-chunked
-_KC = 2048
+_KC = 1024
 
 
 class Split3(tuple):
