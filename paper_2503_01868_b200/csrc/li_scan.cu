@@ -96,6 +96,29 @@ __device__ __forceinline__ void fir8(const A* raw, const A* h, A* out) {
     out[t] = acc;
   }
 }
+// fp32: the same FIR on output pairs (t, t+1) as packed FFMA2; the odd-aligned input pairs
+// (raw[i], raw[i+1]) for odd i are formed once (S / 2 + 4 register moves) and reused by every tap
+template <int S>
+__device__ __forceinline__ void fir8_pairs(const float* raw, const float* h, float* out) {
+  float2 ev[(S + 8) / 2], od[(S + 8) / 2];  // ev[i] = (raw[2i], raw[2i+1]); od[i] = (raw[2i+1], raw[2i+2])
+#pragma unroll
+  for (int i = 0; i < (S + 8) / 2; ++i) {
+    ev[i] = make_float2(raw[2 * i], raw[2 * i + 1]);
+    od[i] = make_float2(raw[2 * i + 1], 2 * i + 2 < S + 8 ? raw[2 * i + 2] : 0.f);
+  }
+#pragma unroll
+  for (int t = 0; t < S; t += 2) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i0 = 8 + t - j;  // first input of the pair
+      const float2 x = (i0 & 1) ? od[i0 >> 1] : ev[i0 >> 1];
+      acc = __ffma2_rn(make_float2(h[j], h[j]), x, acc);
+    }
+    out[t] = acc.x;
+    out[t + 1] = acc.y;
+  }
+}
 
 template <typename T, int S, bool VEC>
 __device__ __forceinline__ void store_seg(T* __restrict__ p, int nv, const typename Cfg<T>::A* in) {
@@ -420,14 +443,18 @@ li_scan_pipe_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
       A u[S], fq[S];
       if constexpr (FEAT) {
         A raw[S + 8], fk[S];
+        auto fir = [&](const A* r, const A* h, A* o) {
+          if constexpr (PAIR) fir8_pairs<S>(r, h, o);
+          else fir8<A, S>(r, h, o);
+        };
         read(2, raw, true);
-        fir8<A, S>(raw, fh[2], u);
+        fir(raw, fh[2], u);
         read(1, raw, true);
-        fir8<A, S>(raw, fh[1], fk);
+        fir(raw, fh[1], fk);
 #pragma unroll
         for (int j = 0; j < S; ++j) u[j] *= fk[j];
         read(0, raw, true);
-        fir8<A, S>(raw, fh[0], fq);
+        fir(raw, fh[0], fq);
       } else {
         read(2, u, false);
         if (gk) {
@@ -441,6 +468,11 @@ li_scan_pipe_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
       A yv[S];
 #pragma unroll
       for (int j = 0; j < S; ++j) yv[j] = A(0);
+      float2 uu[PAIR ? S : 1];  // (u, u): the packed FFMA2 addend, built once per tile
+      if constexpr (PAIR) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) uu[j] = make_float2(u[j], u[j]);
+      }
       for (int b = 0; b < nb; ++b) {
         const int buf = (it * nb + b) & 1;
         A lam[MB], st[MB];
@@ -453,7 +485,7 @@ li_scan_pipe_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
             const float2 l2 = make_float2(lam[n], lam[n + 1]);
             float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int j = 0; j < S; ++j) s2 = ffma2(l2, s2, make_float2(u[j], u[j]));
+            for (int j = 0; j < S; ++j) s2 = ffma2(l2, s2, uu[j]);
             st[n] = s2.x;
             st[n + 1] = s2.y;
           }
@@ -515,7 +547,7 @@ li_scan_pipe_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
             float2 s2 = make_float2(st[n], st[n + 1]);
 #pragma unroll
             for (int j = 0; j < S; ++j) {
-              s2 = ffma2(l2, s2, make_float2(u[j], u[j]));
+              s2 = ffma2(l2, s2, uu[j]);
               y2[j] = ffma2(r2, s2, y2[j]);
             }
           }
@@ -550,8 +582,12 @@ int launch(const void* q, const void* k, const void* v, void* y, const double* r
   const bool vec = (static_cast<size_t>(L) * sizeof(T)) % 16 == 0 && aligned16(y) && (!v || aligned16(v)) &&
                    (!q || aligned16(q)) && (!k || aligned16(k));
   const long long rows = static_cast<long long>(B) * C;
-  static const bool oneshot = [] { const char* e = getenv("HY_LI_SCAN_ONESHOT"); return e && atoi(e) != 0; }();
-  if (vec && np <= PMAXP && !oneshot) {
+  // the pipelined kernel wins for bf16 rows (1.80 vs 2.20 ms for the C3 mixer); fp32 rows stay on
+  // the one-shot kernel (2.60 vs 2.87 ms: with fp32 slots its shared-memory ring caps the SM at
+  // 12 warps, and the kernel turns issue-latency bound, ncu mio / short-scoreboard stalls)
+  static const int mode = [] { const char* e = getenv("HY_LI_SCAN_PIPE"); return e ? atoi(e) : -1; }();
+  const bool pipe = mode < 0 ? sizeof(T) == 2 : mode != 0;
+  if (vec && np <= PMAXP && pipe) {
     auto pk = li_scan_pipe_kernel<T, FEAT>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(pk), PipeCfg<T>::SMEM);
     if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
