@@ -611,11 +611,15 @@ class HyenaCP:
       or, for LI, by the two all-to-all rounds to channel slabs and back.
     """
 
-    def __init__(self, cfg, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None, n_pipe: int | None = None):
+    def __init__(self, cfg, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None, n_pipe: int | None = None,
+                 layout: str = "sequential"):
         from .hyena import HyenaOperator
+        if layout not in LAYOUTS:
+            raise ValueError(f"layout must be one of {LAYOUTS}, got {layout!r}")
         self.op = HyenaOperator(cfg, dtype)
         self.cfg = cfg
         self.grp = grp or CPGroup()
+        self.layout = layout
         # LI: channel segments pipelined through the all-to-all
         self.n_pipe = n_pipe if n_pipe is not None else int(os.environ.get("HY_CP_NPIPE", "4"))
 
@@ -813,6 +817,8 @@ class HyenaCP:
         op, grp = self.op, self.grp
         if grp.n_ranks == 1:  # one rank: the whole sequence is local, the fused operator applies
             return op.forward(x_local, events=events, accumulate_into=accumulate_into)
+        if self.layout == "zigzag":
+            return self._forward_zigzag(x_local, events, accumulate_into)
         x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
         B, D, m = x3.shape
         if self._fused(m) and m >= _lib.MIXER_HISTORY:
@@ -879,6 +885,109 @@ class HyenaCP:
     __call__ = forward
 
 
+    # ------------------------------------------------------------ zigzag layout (cpsim.py:282-319)
+    def _forward_zigzag(self, x_local: torch.Tensor, events=None, accumulate_into=None) -> torch.Tensor:
+        """Rank r holds chunks r and 2N-1-r of the sequence ([half A | half B] in local time).
+        Both halves run as one batch of 2B through the token-local projections and the mixers;
+        each half's causal history comes from the rank holding its predecessor chunk
+        (_zigzag_history): half A from rank r-1's half A, half B from rank r+1's half B (rank
+        N-1's half B continues its own half A). The LI long conv uses the zigzag all-to-all."""
+        from . import _lib, ops
+        op, grp = self.op, self.grp
+        x3 = x_local.unsqueeze(0) if x_local.dim() == 2 else x_local
+        B, D, m = x3.shape
+        if m % 2:
+            raise ValueError(f"zigzag shard length {m} is not two equal chunks")
+        h = m // 2
+        halves = (x3[..., :h], x3[..., h:])
+        ft = op.feat_taps
+        if self._fused(h) and h >= _lib.MIXER_HISTORY:
+            H = _lib.MIXER_HISTORY
+            tails = op.project(torch.cat([halves[0][..., h - H:], halves[1][..., h - H:]], dim=0).contiguous())
+            hist = _zigzag_history(tails[:B], tails[B:], grp, "cp_zigzag_hist")
+            proj = torch.cat([op.project(halves[0].contiguous()), op.project(halves[1].contiguous())], dim=0)
+            if events is not None:
+                events[0].record()
+            mixed = ops.hyena_mixer(proj, ft, op.inner_taps, op.gs, decay=op.decay, packed=op.feat_packed, hist=hist)
+            if events is not None:
+                events[1].record()
+        else:
+            if op.lhf > 8:
+                raise NotImplementedError("zigzag context parallel needs featurizers of <= 8 taps")
+            proj = torch.cat([op.project(halves[0].contiguous()), op.project(halves[1].contiguous())], dim=0)
+            rh = _zigzag_history(proj[:B, :, h - 8:].contiguous(), proj[B:, :, h - 8:].contiguous(), grp,
+                                 "cp_zigzag_feat")
+            u, fq = ops.featurize(proj, ft, rhist=rh)  # (2B, D, h) each
+            if self.cfg.variant == "LI":
+                slab = self._zigzag_slab_conv()
+                u_local = torch.cat([u[:B], u[B:]], dim=-1)  # (B, D, m): the rank's zigzag shard
+                conv = torch.stack([a2a_conv(u_local[b].contiguous(), self.cfg.inner, grp, "zigzag", conv_slab=slab)
+                                    for b in range(B)])
+                conv = torch.cat([conv[..., :h], conv[..., h:]], dim=0)
+            else:
+                lh = op.lh
+                taps = op.materialized_inner
+                uh = _zigzag_history(u[:B, :, h - (lh - 1):].contiguous(), u[B:, :, h - (lh - 1):].contiguous(), grp,
+                                     "cp_zigzag_inner") if lh > 1 else None
+                ext = torch.cat([uh, u], dim=-1) if uh is not None else u
+                conv = (ops.long_conv(ext.contiguous(), taps, op.gs) if lh > 129
+                        else ops.gated_conv(ext.contiguous(), taps, op.gs))[..., lh - 1:]
+            mixed = fq * conv
+        y2 = op.out_project(mixed.contiguous())  # (2B, D, h)
+        y = torch.cat([y2[:B], y2[B:]], dim=-1)
+        if accumulate_into is not None:
+            acc = accumulate_into.unsqueeze(0) if x_local.dim() == 2 else accumulate_into
+            acc.add_(y)
+            y = acc
+        return y[0] if x_local.dim() == 2 else y
+
+    def _zigzag_slab_conv(self):
+        """Natural-order slab conv for the zigzag all-to-all: the implicit filter's tcgen05
+        kernel (bf16, <= 8 poles, L % 8 == 0) or the modal scan, else the materialised taps."""
+        from . import ops
+        op = self.op
+        if op.li_modes is not None:
+            res, poles = op.li_modes
+
+            def conv(natural, slab_groups):
+                g0 = _group_index(op.cfg.inner, slab_groups)
+                ng = slab_groups.n_groups
+                if natural.shape[-1] % 8 == 0:
+                    return ops.li_conv(natural.contiguous(), res[g0:g0 + ng], poles[g0:g0 + ng], slab_groups.group_size)
+                return ops.li_scan(natural.contiguous(), op.li_scan_modes[0][g0:g0 + ng],
+                                   op.li_scan_modes[1][g0:g0 + ng], slab_groups.group_size)
+            return conv
+        if op.li_scan_modes is not None:
+            return _li_scan_slab_conv(op)
+        return None
+
+
+def _zigzag_history(tail_a: torch.Tensor, tail_b: torch.Tensor, grp: CPGroup, scheme: str) -> torch.Tensor:
+    """Causal histories of a zigzag shard's two halves (cpsim.py:282-319 layout; rank r holds
+    chunks r and 2N-1-r): half A's predecessor chunk r-1 is rank r-1's half A (rank 0: none,
+    zeros); half B's predecessor chunk 2N-2-r is rank r+1's half B, except on rank N-1, whose
+    half B (chunk N) continues its own half A (chunk N-1). tail_a / tail_b: this rank's last
+    steps of each half, (B, C, H). Returns (2B, C, H) = [history of A; history of B]."""
+    n, r = grp.n_ranks, grp.rank
+    chans = int(np.prod(tail_a.shape[:-1]))
+    for src in range(n - 1):  # every rank tallies every message: A tails go up, B tails go down
+        grp._send(scheme, src, src + 1, chans * tail_a.shape[-1])
+        grp._send(scheme, src + 1, src, chans * tail_b.shape[-1])
+    hist_a = torch.zeros_like(tail_a)
+    hist_b = tail_a.clone() if r == n - 1 else torch.empty_like(tail_b)
+    ops_ = []
+    if r < n - 1:
+        ops_.append(("send", tail_a.contiguous(), r + 1))
+        ops_.append(("recv", hist_b, r + 1))
+    if r > 0:
+        ops_.append(("send", tail_b.contiguous(), r - 1))
+        ops_.append(("recv", hist_a, r - 1))
+    for q in _batch_p2p(grp, ops_):
+        q.wait()
+    grp.count_rounds(scheme, 1)
+    return torch.cat([hist_a, hist_b], dim=0).contiguous()
+
+
 def _li_slab_conv(op, events=None):
     """Implicit long conv of a channel slab over the full sequence, read and written in the
     rank-major all-to-all layout (tcgen05 li_conv_segmented); events: optional (start, end)
@@ -940,9 +1049,10 @@ class LayoutCP:
     from the first layer to the last. Layers share the group's peer buffers (CPGroup.peer)."""
 
     def __init__(self, stack, dtype: torch.dtype = torch.bfloat16, grp: CPGroup | None = None,
-                 n_pipe: int | None = None):
+                 n_pipe: int | None = None, layout: str = "sequential"):
         self.grp = grp or CPGroup()
-        self.layers = [HyenaCP(cfg, dtype, self.grp, n_pipe) for cfg in stack.layers]
+        self.layout = layout
+        self.layers = [HyenaCP(cfg, dtype, self.grp, n_pipe, layout) for cfg in stack.layers]
         self.residual = stack.residual
 
     def forward(self, x_local: torch.Tensor) -> torch.Tensor:
@@ -957,6 +1067,7 @@ class LayoutCP:
     __call__ = forward
 
 
-def layout_forward_cp(x_local: torch.Tensor, stack, grp: CPGroup | None = None) -> torch.Tensor:
-    """layout_forward (hyena.py:386) on this rank's sequential shard of x."""
-    return LayoutCP(stack, x_local.dtype, grp).forward(x_local)
+def layout_forward_cp(x_local: torch.Tensor, stack, grp: CPGroup | None = None,
+                      layout: str = "sequential") -> torch.Tensor:
+    """layout_forward (hyena.py:386) on this rank's shard of x (sequential or zigzag layout)."""
+    return LayoutCP(stack, x_local.dtype, grp, layout=layout).forward(x_local)

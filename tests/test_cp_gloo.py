@@ -244,3 +244,55 @@ def test_p2p_fft_matches_reference_simulator(world):
         assert out["acct"] == out["want_acct"], (r, out)
         assert out.get("causal", 0.0) < 1e-10 and out.get("trunc", 0.0) < 1e-10, (r, out)
         assert out.get("raises", True), (r, out)
+
+
+def _zigzag_worker(rank, world, port, q):
+    import oracle
+    from paper_2503_01868_b200 import SeqTensor, cp
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        C, L, lh = 3, 32 * world, 5
+        taps = rng.standard_normal((C, lh))
+        x = rng.standard_normal((C, L))
+        bank = explicit_bank_from_taps(taps, 1)
+        local = cp.shard(SeqTensor(x), world, "zigzag").shards[rank]
+        h, H = local.shape[1] // 2, lh - 1
+        grp = cp.CPGroup()
+        a, b = torch.from_numpy(local[:, :h].copy()), torch.from_numpy(local[:, h:].copy())
+        hist = cp._zigzag_history(a[None, :, h - H:].contiguous(), b[None, :, h - H:].contiguous(), grp, "zz")
+        outs = []
+        for half, hh in ((a, hist[0]), (b, hist[1])):
+            ext = np.concatenate([hh.numpy(), half.numpy()], axis=1)
+            outs.append(oracle.direct_causal_conv(ext, bank)[:, H:])
+        q.put((rank, np.concatenate(outs, axis=1), grp.total_messages("zz"), grp.scheme_rounds.get("zz", 0)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_zigzag_history_host_logic(world):
+    """The zigzag layout's two causal halos (cp._zigzag_history): each half, convolved after
+    its history, reproduces its chunk of the unsharded conv; 2 (N - 1) messages, one round."""
+    import oracle
+    from paper_2503_01868_b200 import SeqTensor, cp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zigzag_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(3)
+    C, L, lh = 3, 32 * world, 5
+    taps = rng.standard_normal((C, lh))
+    x = rng.standard_normal((C, L))
+    want = oracle.direct_causal_conv(x, explicit_bank_from_taps(taps, 1))
+    got = cp.gather(cp.ShardedSeq(tuple(r[1] for r in res), "zigzag")).data
+    assert np.max(np.abs(got - want)) < 1e-12
+    assert all(r[2] == 2 * (world - 1) and r[3] == 1 for r in res)
