@@ -56,9 +56,17 @@ constexpr int HROWS = 8;                  // U rows before the tile's first chun
 constexpr int UROWS = NCH + HROWS;        // 72 rows: 9 groups of 8
 constexpr int NPOLE = 8;                  // IMPL: modes per group (zero padded)
 constexpr int NBUF = 3;
-constexpr int N_CONV_WARPS = 4, N_EPI_WARPS = 8, N_TB_WARPS = 4;
-constexpr int W_CONV0 = 0, W_EPI0 = 4, W_TB0 = 12, W_SCAN = 16, W_MMA = 17, W_PROD = 18, THREADS = 19 * 32;
-constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
+constexpr int N_EPI_WARPS = 8, N_TB_WARPS = 4;
+constexpr int TB_THREADS = N_TB_WARPS * 32;
+// Warp roles; FEAT (the fused mixers: featurizer FIRs on the converter warps) doubles the
+// converter warps
+template <bool FEAT>
+struct Roles {
+  static constexpr int N_CONV = FEAT ? 8 : 4;
+  static constexpr int W_EPI0 = N_CONV, W_TB0 = W_EPI0 + N_EPI_WARPS, W_SCAN = W_TB0 + N_TB_WARPS,
+                       W_MMA = W_SCAN + 1, W_PROD = W_MMA + 1, THREADS = (W_PROD + 1) * 32,
+                       CONV_THREADS = N_CONV * 32;
+};
 constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
 // TMEM columns: accumulators [NBUF] x 64; explicit factors T_k at TM_F + 64 k; IMPL: T_0 of
 // group buffer b at TM_F + 64 b, mode inputs E [2] x 64 at TM_E
@@ -67,23 +75,31 @@ static_assert(TM_F + 64 * (KMAX + 1) <= 512 && TM_E + 2 * NCH <= 512, "TMEM budg
 static_assert(HROWS >= KMAX && UROWS % 8 == 0, "U rows");
 
 constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
+constexpr int FH = 8;                                      // FEAT: featurizer history steps
 constexpr int RING_BYTES = 8 * (TILE_T + KMAX * LB) * 2;  // 139264: 8 ungated / 4 gated windows
+// FEAT: 2 stages of q / k / v windows, then the featurized q of each accumulator buffer
+constexpr int FEAT_WIN_BYTES = (TILE_T + FH) * 2;          // IMPL mixer window (the K-block one is larger)
+constexpr int FQ_BYTES = TILE_T * 2;
 constexpr int U_ATOM = UROWS * 128;                        // one 64-element K atom of the U matrix
 constexpr int U_BYTES = 2 * U_ATOM;
 constexpr int OFF_ST = 0;
-constexpr int OFF_U = round_up(RING_BYTES, 1024);
+// FEAT stages hold one chunk of explicit history at most (the fused MR mixer, K <= 1)
+constexpr int OFF_U = round_up(2 * 3 * (TILE_T + LB + FH) * 2 + NBUF * FQ_BYTES, 1024);
+static_assert(OFF_U >= RING_BYTES, "ring");
 constexpr int HP_N = 1024;                                 // hpad[i + 128] = h[i], i in [-128, 896)
 constexpr int OFF_HP = OFF_U + NBUF * U_BYTES;             // two tap buffers (this group / next)
 constexpr int OFF_L = round_up(OFF_HP + 2 * HP_N * 2, 1024);  // IMPL: Lam[2] (bf16 SW128, 8 rows)
 constexpr int OFF_P = OFF_L + 2 * 2048;                    // IMPL: P[2] (tf32, 128 x 8)
 constexpr int OFF_S = OFF_P + 2 * 4096;                    // IMPL: S_prev[NBUF] (tf32, 64 x 8)
 constexpr int OFF_BAR = OFF_S + NBUF * NCH * NPOLE * 4;
-constexpr int N_BARS = 2 * 8 + 4 * NBUF + 10;
+constexpr int N_BARS = 2 * 8 + 5 * NBUF + 10;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 struct Params {
+  const bf16* proj;       // FEAT: (B, 3C, L) projections [q; k; v]
+  const float* feat;      // FEAT: (3, C, lhf) featurizer taps, lhf <= 8
   const bf16* q;
   const bf16* k;
   const bf16* v;
@@ -93,7 +109,7 @@ struct Params {
   const float* poles;     // IMPL: (n_groups, npoles)
   const float* residues;
   int npoles;
-  int B, C, L, lh, K, gs;
+  int B, C, L, lh, K, gs, lhf;
   int tiles_per_seq, total_tiles;
   // rows stored as L / seg_len time segments: element (row, t) at row * seg_len +
   // (t / seg_len) * seg_stride + t % seg_len (the rank-major all-to-all buffer); 0 = plain rows
@@ -135,20 +151,66 @@ __device__ __forceinline__ uint32_t sw_off(int row, int j) {  // 16-byte unit j 
   return (j >> 3) * U_ATOM + row * 128 + (((j & 7) ^ (row & 7)) << 4);
 }
 
+__device__ __forceinline__ int4 pack8(const float* in) {
+  int4 raw;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(in[2 * i], in[2 * i + 1]);
+  return raw;
+}
+
+// Featurizer FIR (hyena.py:122-126, taps zero padded to 8) of the 8 steps at window offset off:
+// out[e] = sum_j h[j] w[off + e - j], from the unit before (history) and the unit itself, as
+// packed FFMA2 on output pairs (the odd-aligned input pairs are formed once)
+__device__ __forceinline__ void feat_unit(const unsigned char* win, int off, const float* h, float* out) {
+  const int4 a = *reinterpret_cast<const int4*>(win + (off - 8) * 2);
+  const int4 b = *reinterpret_cast<const int4*>(win + off * 2);
+  float2 ev[8];  // ev[i] = (w[off - 8 + 2i], w[off - 7 + 2i])
+  const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ev[i] = __bfloat1622float2(pa[i]);
+    ev[4 + i] = __bfloat1622float2(pb[i]);
+  }
+  float2 od[7];  // od[i] = (w[off - 7 + 2i], w[off - 6 + 2i])
+#pragma unroll
+  for (int i = 0; i < 7; ++i) od[i] = make_float2(ev[i].y, ev[i + 1].x);
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i0 = 8 + e - j;  // window index (relative to off - 8) of the pair's first input
+      const float2 x = (i0 & 1) ? od[(i0 - 1) >> 1] : ev[i0 >> 1];
+      acc = __ffma2_rn(make_float2(h[j], h[j]), x, acc);
+    }
+    out[e] = acc.x;
+    out[e + 1] = acc.y;
+  }
+}
+
 // No-swizzle K-major descriptor with explicit leading / stride byte offsets.
 __device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (static_cast<uint64_t>((saddr >> 4) & 0x3FFF)) | (static_cast<uint64_t>(lbo >> 4) << 16) |
          (static_cast<uint64_t>(sbo >> 4) << 32) | (static_cast<uint64_t>(1) << 46);
 }
 
-template <bool GK, bool GQ, bool IMPL>
-__global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) {
-  constexpr int KH = IMPL ? 0 : KMAX;           // history chunks staged before the tile
-  constexpr int WIN = TILE_T + KH * LB;         // staged window per tensor (steps)
+template <bool GK, bool GQ, bool IMPL, bool FEAT>
+__global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(const Params p) {
+  using R = Roles<FEAT>;
+  constexpr int W_EPI0 = R::W_EPI0, W_TB0 = R::W_TB0, W_SCAN = R::W_SCAN, W_MMA = R::W_MMA, W_PROD = R::W_PROD;
+  constexpr int CONV_THREADS = R::CONV_THREADS;
+  constexpr int KH = IMPL ? 0 : (FEAT ? 1 : KMAX);  // history chunks staged before the tile
+  constexpr int HS = KH * LB + (FEAT ? FH : 0); // history steps staged before the tile
+  constexpr int WIN = TILE_T + HS;              // staged window per tensor (steps)
   constexpr int WIN_BYTES = WIN * 2;
-  constexpr int STAGE_BYTES = (GK ? 2 : 1) * WIN_BYTES;
-  constexpr int STAGES = RING_BYTES / STAGE_BYTES;
-  static_assert(STAGES >= 4 && STAGES <= 8, "ring depth");
+  constexpr int NWIN = FEAT ? 3 : (GK ? 2 : 1); // windows per stage: [v, k] or FEAT [v, k, q]
+  constexpr int STAGE_BYTES = NWIN * WIN_BYTES;
+  constexpr int STAGES = FEAT ? 2 : RING_BYTES / STAGE_BYTES;
+  constexpr int OFF_FQ = STAGES * STAGE_BYTES;  // FEAT: featurized q [NBUF]
+  static_assert(FEAT || (STAGES >= 4 && STAGES <= 8), "ring depth");
+  static_assert(!FEAT || OFF_FQ + NBUF * FQ_BYTES <= OFF_U, "FEAT ring");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -163,6 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
   uint64_t* tfreep = tfree + 2;      // [2] IMPL scan commit: last P . S_prev of buffer b retired
   uint64_t* efull = tfreep + 2;      // [2] IMPL: MMA commit -> scan (E in TMEM)
   uint64_t* eempty = efull + 2;      // [2] IMPL: scan -> converter (E drained)
+  uint64_t* qfull = eempty + 2;      // [NBUF] FEAT: converter -> epilogue (featurized q in SMEM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,6 +245,7 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
       mbar_init(&uempty[i], 1);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
+      mbar_init(&qfull[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tready[i], 1);
@@ -206,19 +270,15 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
       const int s = it % STAGES;
       mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
       unsigned char* st = smem + OFF_ST + s * STAGE_BYTES;
-      bf16* vbuf = reinterpret_cast<bf16*>(st);
-      bf16* kbuf = reinterpret_cast<bf16*>(st + WIN_BYTES);
-      const int ws = t.t0 - KH * LB, we = t.t0 + TILE_T;
+      const int ws = t.t0 - HS, we = t.t0 + TILE_T;
       const int vs = max(ws, 0), ve = min(we, p.L);
-      if (vs != ws || ve != we) {  // zero the window outside [0, L) (whole 16-byte units)
+      if (vs != ws || ve != we) {  // zero the windows outside [0, L) (whole 16-byte units)
         const int4 z = make_int4(0, 0, 0, 0);
-        for (int i = lane * 8; i < vs - ws; i += 256) {
-          *reinterpret_cast<int4*>(vbuf + i) = z;
-          if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
-        }
-        for (int i = (ve - ws) + lane * 8; i < WIN; i += 256) {
-          *reinterpret_cast<int4*>(vbuf + i) = z;
-          if (GK) *reinterpret_cast<int4*>(kbuf + i) = z;
+#pragma unroll
+        for (int x = 0; x < NWIN; ++x) {
+          bf16* wb = reinterpret_cast<bf16*>(st + x * WIN_BYTES);
+          for (int i = lane * 8; i < vs - ws; i += 256) *reinterpret_cast<int4*>(wb + i) = z;
+          for (int i = (ve - ws) + lane * 8; i < WIN; i += 256) *reinterpret_cast<int4*>(wb + i) = z;
         }
         fence_proxy_async();
       }
@@ -227,10 +287,18 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
         // a window never crosses a segment of the segmented layout (seg_len % TILE_T == 0, and
         // the explicit history is used with plain rows only)
         const uint32_t bytes = static_cast<uint32_t>(ve - vs) * 2;
-        const size_t off = elem_off(p, t.b * p.C + t.c, vs);
-        mbar_arrive_expect_tx(&full[s], bytes * (GK ? 2 : 1));
-        bulk_g2s(vbuf + (vs - ws), p.v + off, bytes, &full[s]);
-        if (GK) bulk_g2s(kbuf + (vs - ws), p.k + off, bytes, &full[s]);
+        mbar_arrive_expect_tx(&full[s], bytes * NWIN);
+        if (FEAT) {
+          const size_t r0 = (static_cast<size_t>(t.b) * 3 * p.C + t.c) * p.L + vs;  // q row
+          const size_t cl = static_cast<size_t>(p.C) * p.L;
+          bulk_g2s(st + (vs - ws) * 2, p.proj + r0 + 2 * cl, bytes, &full[s]);                  // v
+          bulk_g2s(st + WIN_BYTES + (vs - ws) * 2, p.proj + r0 + cl, bytes, &full[s]);          // k
+          bulk_g2s(st + 2 * WIN_BYTES + (vs - ws) * 2, p.proj + r0, bytes, &full[s]);           // q
+        } else {
+          const size_t off = elem_off(p, t.b * p.C + t.c, vs);
+          bulk_g2s(st + (vs - ws) * 2, p.v + off, bytes, &full[s]);
+          if (GK) bulk_g2s(st + WIN_BYTES + (vs - ws) * 2, p.k + off, bytes, &full[s]);
+        }
       }
       __syncwarp();
     }
@@ -289,10 +357,22 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
     }
   } else if (warp < W_EPI0) {
     // ------------------------------------------------------------ converters
-    const int ctid = threadIdx.x - W_CONV0 * 32;
-    for (int it = 0; it < ntiles; ++it) {
+    const int ctid = threadIdx.x;
+    Tile t;
+    t.init(tb, p);
+    int fc = -1;
+    float fh[3][8];  // FEAT: [q, k, v] featurizer taps of the tile's channel
+    for (int it = 0; it < ntiles; ++it, t.next(p)) {
       const int s = it % STAGES, u = it % NBUF;
       const uint32_t uph = (it / NBUF) & 1;
+      if (FEAT && t.c != fc) {
+        fc = t.c;
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            fh[x][j] = j < p.lhf ? p.feat[(static_cast<size_t>(x) * p.C + t.c) * p.lhf + j] : 0.f;
+      }
       mbar_wait(&full[s], (it / STAGES) & 1);
       mbar_wait(&uempty[u], uph ^ 1);
       const unsigned char* st = smem + OFF_ST + s * STAGE_BYTES;
@@ -300,7 +380,31 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
       // U rows HROWS - K .. UROWS - 1 = chunks -K .. NCH - 1 of the tile (rows above are unread)
       const int r0 = HROWS - (IMPL ? 0 : p.K);
       const int nunits = (UROWS - r0) * 16;
-      for (int i = ctid; i < nunits; i += CONV_THREADS) {
+      if (FEAT) {
+        // u = Fk(pk) * Fv(pv) per 8-step unit from the raw windows (8 steps of history each)
+        for (int i = ctid; i < nunits; i += CONV_THREADS) {
+          const int row = r0 + (i >> 4), jj = i & 15;
+          const int off = (row - HROWS) * LB + KH * LB + FH + jj * 8;  // window offset of the unit
+          float fv[8], fk[8];
+          feat_unit(st, off, fh[2], fv);
+          feat_unit(st + WIN_BYTES, off, fh[1], fk);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) fv[e] *= fk[e];
+          *reinterpret_cast<int4*>(ub + sw_off(row, jj)) = pack8(fv);
+        }
+        // featurized q of the tile -> FQ[u] (natural order), once the epilogue drained buffer u
+        if (ctid == 0) mbar_wait(&tempty[u], uph ^ 1);
+        named_bar_sync(BAR_CONV, CONV_THREADS);
+        bf16* fqb = reinterpret_cast<bf16*>(smem + OFF_FQ + u * FQ_BYTES);
+        for (int i = ctid; i < TILE_T / 8; i += CONV_THREADS) {
+          float fq[8];
+          feat_unit(st + 2 * WIN_BYTES, KH * LB + FH + i * 8, fh[0], fq);
+          *reinterpret_cast<int4*>(fqb + i * 8) = pack8(fq);
+        }
+        named_bar_sync(BAR_CONV, CONV_THREADS);
+        if (ctid == 0) mbar_arrive(&qfull[u]);
+      }
+      for (int i = FEAT ? nunits : ctid; i < nunits; i += CONV_THREADS) {
         const int row = r0 + (i >> 4), jj = i & 15;
         const int off = (row - HROWS + KH) * LB + jj * 8;  // element offset in the window
         int4 vv = *reinterpret_cast<const int4*>(st + off * 2);
@@ -320,7 +424,7 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
       named_bar_sync(BAR_CONV, CONV_THREADS);
       if (ctid == 0) {
         mbar_arrive(&empty[s]);
-        mbar_wait(&tempty[u], uph ^ 1);                             // accumulator u drained
+        if (!FEAT) mbar_wait(&tempty[u], uph ^ 1);                  // accumulator u drained
         if (IMPL) mbar_wait(&eempty[it & 1], ((it >> 1) & 1) ^ 1);  // E buffer drained by the scan
         mbar_arrive(&ufull[u]);
       }
@@ -338,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
       const int nt = min(TILE_T, p.L - t.t0);
       const size_t roff = elem_off(p, row, t.t0);  // a tile never crosses a segment
       float qv[32];
-      if (GQ) {  // gate loads in flight while the MMAs run
+      if (GQ && !FEAT) {  // gate loads in flight while the MMAs run
 #pragma unroll
         for (int n = 0; n < 32; ++n) {
           const int tt = (colh * 32 + n) * LB + tout;
@@ -352,14 +456,24 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
                          acc);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
+      if (!FEAT && lane == 0) mbar_arrive(&tempty[a]);
       bf16* yrow = p.y + roff;
+      if (FEAT) {  // gate with the featurized q the converters left in FQ[a]
+        mbar_wait(&qfull[a], (it / NBUF) & 1);
+        const bf16* fqb = reinterpret_cast<const bf16*>(smem + OFF_FQ + a * FQ_BYTES);
+#pragma unroll
+        for (int n = 0; n < 32; ++n) qv[n] = __bfloat162float(fqb[(colh * 32 + n) * LB + tout]);
+      }
 #pragma unroll
       for (int n = 0; n < 32; ++n) {
         const int tt = (colh * 32 + n) * LB + tout;
         float val = acc[n];
-        if (GQ) val *= qv[n];
+        if (GQ || FEAT) val *= qv[n];
         if (tt < nt) yrow[tt] = __float2bfloat16_rn(val);
+      }
+      if (FEAT) {  // accumulator and FQ[a] both free
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
       }
     }
   } else if (warp < W_SCAN) {
@@ -545,9 +659,9 @@ __global__ void __launch_bounds__(THREADS, 1) block_conv_kernel(const Params p) 
   if (warp == W_MMA) tmem_dealloc<512>(tmem_base);
 }
 
-template <bool GK, bool GQ, bool IMPL>
+template <bool GK, bool GQ, bool IMPL, bool FEAT = false>
 static int launch(const Params& p, cudaStream_t st) {
-  auto kern = block_conv_kernel<GK, GQ, IMPL>;
+  auto kern = block_conv_kernel<GK, GQ, IMPL, FEAT>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), SMEM_BYTES);
   if (e != cudaSuccess) return fail(HY_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   int dev = 0, sms = 148;
@@ -555,7 +669,7 @@ static int launch(const Params& p, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = IMPL ? p.total_tiles / p.tiles_per_seq : p.total_tiles;  // IMPL: whole sequences
   const int grid = units < sms ? units : sms;
-  kern<<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  kern<<<grid, Roles<FEAT>::THREADS, SMEM_BYTES, st>>>(p);
   return check_launch("block_conv_kernel");
 }
 
@@ -568,6 +682,33 @@ static int dispatch(const Params& p, bool q, bool k, cudaStream_t st) {
 }
 
 }  // namespace kb
+
+// Fused mixers on the staged-row kernel (FEAT): featurizers (lhf <= 8) on the converter warps,
+// u = k * v, the long conv (implicit filter when residues / poles are given, else the K-block
+// explicit conv with the MR decay), q gate -- from the (B, 3C, L) projections, one pass.
+int mixer_tc_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const float* taps_hat,
+                 const float* decay, int lh, const float* residues, const float* poles, int npoles, int gs, int B,
+                 int C, int L, void* stream) {
+  kb::Params p{};
+  p.proj = static_cast<const kb::bf16*>(proj);
+  p.feat = feat_taps;
+  p.lhf = lhf;
+  p.y = static_cast<kb::bf16*>(y);
+  p.taps_hat = taps_hat;
+  p.decay = decay;
+  p.poles = poles;
+  p.residues = residues;
+  p.npoles = npoles;
+  p.B = B, p.C = C, p.L = L, p.gs = gs;
+  p.lh = residues ? 1 : lh;
+  p.K = residues ? 0 : (lh - 1 + kb::LB - 1) / kb::LB;
+  if (p.K > 1) return fail(HY_ERR_UNSUPPORTED, "fused staged-row mixer holds one spill factor (lh <= 129)");
+  p.tiles_per_seq = (L + kb::TILE_T - 1) / kb::TILE_T;
+  p.total_tiles = p.tiles_per_seq * B * C;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (residues) return kb::launch<true, true, true, true>(p, st);
+  return kb::launch<true, true, false, true>(p, st);
+}
 
 // Implicit-filter long conv on the staged-row tcgen05 kernel (two_stage_sm100.cu's li_conv
 // entry points route here): plain rows (seg_len = 0) or the segmented all-to-all layout.

@@ -20,4 +20,8 @@ int fir_stream_fwd(const void* q, const void* k, const void* v, void* y, const f
 // tiles; seg_len = 0 (plain rows) or a multiple of 8192
 int li_conv_tc_fwd(const void* q, const void* k, const void* v, void* y, const float* residues, const float* poles,
                    int npoles, int gs, int B, int C, int L, int seg_len, long long seg_stride, void* stream);
+// fused mixers (featurizers + gates + implicit / K-block conv) on the staged-row tcgen05 kernel
+int mixer_tc_fwd(const void* proj, void* y, const float* feat_taps, int lhf, const float* taps_hat,
+                 const float* decay, int lh, const float* residues, const float* poles, int npoles, int gs, int B,
+                 int C, int L, void* stream);
 }  // namespace hy

@@ -11,6 +11,8 @@
 // Persistent warps walk the blocks row by row and prefetch the next block's rows into
 // registers before computing the current one. HBM traffic is the 3 projected rows in and y
 // out (16 B/token/channel at fp32, 8 at bf16).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
@@ -784,6 +786,10 @@ extern "C" int hy_hyena_mixer_fwd(const void* proj, void* y, const void* feat_ta
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float* ft = static_cast<const float*>(feat_taps);
   const float* it = static_cast<const float*>(inner_taps);
+  static const bool kb_mixer = [] { const char* e = getenv("HY_MR_KB"); return e && atoi(e) != 0; }();
+  if (dtype == HY_BF16 && L % 8 == 0 && aligned16(proj) && aligned16(y) && !hist && lhf <= 8 && kb_mixer &&
+      lh <= 129)  // HY_MR_KB=1: the MR mixer on the staged-row kernel (CUDA-core featurizers, 64-chunk tiles)
+    return mixer_tc_fwd(proj, y, ft, lhf, it, inner_decay, lh, nullptr, nullptr, 0, gs, B, C, L, stream);
   if (dtype == HY_BF16 && lh <= 129 && L % 8 == 0 && aligned16(proj) && aligned16(y) && feat_pack)
     return mr_mixer_fwd(proj, y, ft, feat_pack, hist, lhf, it, inner_decay, lh, gs, B, C, L, stream);
   if (hist) return fail(HY_ERR_UNSUPPORTED, "projection history (context parallel) needs the tcgen05 mixer path");

@@ -1008,6 +1008,8 @@ extern "C" HY_API int hy_li_mixer_fwd(const void* proj, void* y, const float* fe
   if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
   if (!aligned16(proj) || !aligned16(y) || !aligned16(feat_pack))
     return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
+  if (!legacy_li() && lhf <= 8)  // 64-chunk tiles, CUDA-core featurizers (block_conv_sm100.cu)
+    return mixer_tc_fwd(proj, y, feat_taps, lhf, nullptr, nullptr, 1, residues, poles, npoles, gs, B, C, L, stream);
   ts::Params p{};
   p.proj = static_cast<const ts::bf16*>(proj);
   p.y = static_cast<ts::bf16*>(y);
