@@ -78,7 +78,6 @@ constexpr int round_up(int a, int m) { return (a + m - 1) / m * m; }
 constexpr int FH = 8;                                      // FEAT: featurizer history steps
 constexpr int RING_BYTES = 8 * (TILE_T + KMAX * LB) * 2;  // 139264: 8 ungated / 4 gated windows
 // FEAT: 2 stages of q / k / v windows, then the featurized q of each accumulator buffer
-constexpr int FEAT_WIN_BYTES = (TILE_T + FH) * 2;          // IMPL mixer window (the K-block one is larger)
 constexpr int FQ_BYTES = TILE_T * 2;
 constexpr int U_ATOM = UROWS * 128;                        // one 64-element K atom of the U matrix
 constexpr int U_BYTES = 2 * U_ATOM;

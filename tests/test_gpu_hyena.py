@@ -287,3 +287,63 @@ def test_mr_operator_long_filter_kblock(lh, gs):
                                else ("regularized", f.taps_hat, f.decay_rate, f.base) for f in g.filters]}
     want = oracle.hyena_forward(x, ocfg)
     assert oracle.rel_err(y.double().cpu().numpy(), want) < 1e-2
+
+
+def _mha_ref(x: np.ndarray, w_qkv: np.ndarray, w_out: np.ndarray, heads: int) -> np.ndarray:
+    """Causal multi-head attention in float64 (the math of stripe.MHALayer): x (D, L)."""
+    D, L = x.shape
+    hd = D // heads
+    qkv = (x.T @ w_qkv).reshape(L, 3, heads, hd)
+    out = np.empty((L, heads, hd))
+    mask = np.triu(np.ones((L, L), dtype=bool), 1)
+    for h in range(heads):
+        q, k, v = qkv[:, 0, h], qkv[:, 1, h], qkv[:, 2, h]
+        s = q @ k.T / np.sqrt(hd)
+        s[mask] = -np.inf
+        p = np.exp(s - s.max(axis=1, keepdims=True))
+        out[:, h] = (p / p.sum(axis=1, keepdims=True)) @ v
+    return (out.reshape(L, D) @ w_out).T
+
+
+def test_stripe_vs_oracle_and_mha_reference():
+    """Config C4's stripe (SE -> MR -> LI -> MHA, residual): the Hyena layers against the oracle's
+    residual layout, the MHA layer (cuBLAS projections + PyTorch SDPA, library compute: the
+    reference has no attention) against a float64 restatement of causal softmax attention on the
+    same bf16 weights. bf16 end to end, 2e-2 over the chained bf16 roundings of four layers."""
+    from paper_2503_01868_b200.stripe import Stripe
+    D, L, heads = 64, 2048, 4
+    rng = hy.make_rng(21)
+    cfgs = [hy.make_hyena_config("SE", D, rng, block_size=128),
+            hy.make_hyena_config("MR", D, rng, inner_len=128, block_size=128),
+            hy.make_hyena_config("LI", D, rng, seq_len=L, backend="fft")]
+
+    def rcfg(cfg):
+        rnd = {n: bf16_round(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+        fs = {n: hy.GroupSpec(D, 1, tuple(hy.ExplicitFilter(bf16_round(f.taps)) for f in getattr(cfg, n).filters))
+              for n in ("q_feat", "k_feat", "v_feat")}
+        return hy.HyenaConfig(**{**cfg.__dict__, **rnd, **fs})
+    cfgs = [rcfg(c) for c in cfgs]
+    st = Stripe(cfgs, torch.bfloat16, heads=heads)
+    x = bf16_round(hy.make_rng(22).standard_normal((D, L)))
+    y = st.forward(torch.from_numpy(x)[None].to("cuda", torch.bfloat16))[0].double().cpu().numpy()
+
+    def ocfg(cfg):
+        d = {"variant": cfg.variant, "width": D, "block_size": cfg.block_size, "backend": cfg.backend,
+             **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+        for n in ("q_feat", "k_feat", "v_feat", "inner"):
+            g = getattr(cfg, n)
+            fl = []
+            for f in g.filters:
+                if isinstance(f, hy.ExplicitFilter):
+                    fl.append(("explicit", f.taps))
+                elif isinstance(f, hy.RegularizedFilter):
+                    fl.append(("regularized", f.taps_hat, f.decay_rate, f.base))
+                else:
+                    fl.append(("implicit", f.residues, f.poles, f.length))
+            d[n] = {"channels": g.channels, "group_size": g.group_size, "filters": fl}
+        return d
+    cur = oracle.layout_forward(x, [ocfg(c) for c in cfgs], residual=True)
+    w_qkv = st.mha.w_qkv.double().cpu().numpy()
+    w_out = st.mha.w_out.double().cpu().numpy()
+    want = cur + _mha_ref(bf16_round(cur), w_qkv, w_out, heads)
+    assert oracle.rel_err(y, want) < 2e-2
