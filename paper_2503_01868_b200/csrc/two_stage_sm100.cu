@@ -1008,7 +1008,11 @@ extern "C" HY_API int hy_li_mixer_fwd(const void* proj, void* y, const float* fe
   if (lhf < 1 || lhf > ts::MAX_LHF) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > 16", lhf);
   if (!aligned16(proj) || !aligned16(y) || !aligned16(feat_pack))
     return fail(HY_ERR_UNSUPPORTED, "needs 16-byte aligned tensors");
-  if (!legacy_li() && lhf <= 8)  // 64-chunk tiles, CUDA-core featurizers (block_conv_sm100.cu)
+  // HY_LI_MIXER_KB=1: the staged-row kernel's FEAT mode (CUDA-core featurizers, 64-chunk tiles).
+  // Measured slower at C3 (1.51 ms vs 0.81 ms: the converter warps' FIRs set its tile period),
+  // so the tensor-core featurizers of this kernel stay the default for the fused mixer.
+  static const bool kb_mixer = [] { const char* e = getenv("HY_LI_MIXER_KB"); return e && atoi(e) != 0; }();
+  if (kb_mixer && lhf <= 8)
     return mixer_tc_fwd(proj, y, feat_taps, lhf, nullptr, nullptr, 1, residues, poles, npoles, gs, B, C, L, stream);
   ts::Params p{};
   p.proj = static_cast<const ts::bf16*>(proj);
