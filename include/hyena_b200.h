@@ -42,6 +42,7 @@
  *   hy_li_scan_fwd          fft.py:128-145       fft_conv on an ImplicitFilter bank (core.py:147-151), gated as
  *                           hyena.py:183-186     hyena_forward's LI inner conv, by exact per-mode scans
  *   hy_li_scan_mixer_fwd    hyena.py:162-186     the LI mixer (featurizers + gates + modal scan), fused
+ *   hy_fft_c2c              fft.py:116-125       fft / ifft; cpsim.py:596-615 the distributed FFT's local transform
  *   hy_split3_cat           hyena.py:124,188     the fp32 projections' operand split (split-bf16 GEMM)
  *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
  *                           core.py:255-268      the tap correlation it consumes
@@ -260,6 +261,14 @@ HY_API int hy_li_scan_fwd(const void* q, const void* k, const void* v, void* y, 
 HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const void* feat_taps, int lhf, const double* residues,
                                 const double* poles, int npoles, int group_size, int B, int C, int L, int dtype,
                                 void* stream);
+/* Batched complex FFT of rows of power-of-two length n, natural order in and out (radix-2 Stockham;
+ * one CTA per row in shared memory up to 8192 (complex128) / 16384 (complex64) points, one stage
+ * per launch through the workspace above): x, y (batch, n) complex64 (dtype HY_F32) or complex128
+ * (HY_F64), out of place; inverse != 0 flips the twiddle sign and does NOT scale (fft.py:116-125's
+ * ifft carries the 1/n). ws: hy_fft_c2c_workspace_size bytes (0 for short rows). */
+HY_API size_t hy_fft_c2c_workspace_size(long long batch, long long n, int dtype);
+HY_API int hy_fft_c2c(const void* x, void* y, long long batch, long long n, int inverse, int dtype, void* ws,
+                      size_t ws_bytes, void* stream);
 /* fp32 activation -> the K-concatenated bf16 operand of the split-bf16 fp32 GEMM (blas.py; the
  * fp32 projections of hyena.py:124,188 on tensor cores): x (batch, K, N) fp32, out
  * (batch, 5K, N) bf16 = [X1; X2; X0; X1; X0] with X0 = bf16(x), X1 = bf16(x - X0),

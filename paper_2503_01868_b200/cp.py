@@ -501,6 +501,16 @@ def _stage_twiddle(g: int, half: int, m: int, length: int, sign: float, like: to
     return torch.polar(torch.ones_like(ang), ang).to(like.device, like.dtype)
 
 
+def _local_fft(x: torch.Tensor, inverse: bool) -> torch.Tensor:
+    """The per-rank transform after the cross-rank stages: the hand-written Stockham kernel on
+    device tensors (hy_fft_c2c); host tensors (the gloo CPU tests of the scheme's host logic)
+    use torch.fft."""
+    if x.is_cuda:
+        from .ops import fft_c2c
+        return fft_c2c(x, inverse=inverse)
+    return torch.fft.ifft(x) if inverse else torch.fft.fft(x)
+
+
 def p2p_fft_forward(local: torch.Tensor, grp: CPGroup, scheme: str = "p2p_fft_conv") -> torch.Tensor:
     """This rank's spectrum slice of the sequentially sharded signal (cpsim.py:547-566, 596-604):
     stage s pairs rank r with r +- half inside groups of N >> (s-1) ranks; the low half keeps
@@ -528,14 +538,14 @@ def p2p_fft_forward(local: torch.Tensor, grp: CPGroup, scheme: str = "p2p_fft_co
             x = (other - x) * _stage_twiddle(g, half, m, length, -1.0, x)
         grp.note_resident(r, m)
     grp.count_rounds(scheme, stages)
-    return torch.fft.fft(x)
+    return _local_fft(x, inverse=False)
 
 
 def p2p_fft_inverse(spec: torch.Tensor, grp: CPGroup, scheme: str = "p2p_fft_conv") -> torch.Tensor:
     """Inverse of p2p_fft_forward (cpsim.py:569-590, 607-615): local inverse FFT, then the
     stages in reverse with conjugate twiddles and a factor 1/2; restores the sequential shard."""
     n, r = grp.n_ranks, grp.rank
-    x = torch.fft.ifft(spec)
+    x = _local_fft(spec, inverse=True)
     m = x.shape[-1]
     total = m * n
     elems = int(x.numel())

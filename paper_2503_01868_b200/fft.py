@@ -4,8 +4,7 @@
 axis, zero padded so there is no wraparound, float64 result (through ops.long_conv). The
 transform building blocks keep their reference names and semantics (last axis, power-of-two
 lengths, complex128, `fft` unnormalised, `ifft` carrying 1/l) and run on the device: the
-standalone transforms through cuFFT (torch.fft, a library call like cuBLAS for the GEMMs —
-the convolution hot path uses the hand-written kernels of csrc/fft_fast.cu), the radix-2
+standalone transforms through the hand-written Stockham kernel (csrc/fft_c2c.cu), the radix-2
 stages, permutations and O(l^2) oracles as device tensor ops. Results come back as numpy
 arrays like the reference's.
 """
@@ -146,17 +145,20 @@ def _dif_passes(x) -> np.ndarray:
 
 
 def fft(x) -> np.ndarray:
-    """Natural-order FFT of the last axis, power-of-two length, no scale (fft.py:116-118)."""
+    """Natural-order FFT of the last axis, power-of-two length, no scale (fft.py:116-118), by the
+    hand-written Stockham kernel (hy_fft_c2c)."""
+    from .ops import fft_c2c
     t = _dev(x)
     require_pow2(t.shape[-1])
-    return _host(torch.fft.fft(t, dim=-1))
+    return _host(fft_c2c(t))
 
 
 def ifft(y) -> np.ndarray:
-    """Inverse transform carrying the full 1/l (fft.py:121-125)."""
+    """Inverse transform carrying the full 1/l (fft.py:121-125) (hy_fft_c2c)."""
+    from .ops import fft_c2c
     t = _dev(y)
     require_pow2(t.shape[-1])
-    return _host(torch.fft.ifft(t, dim=-1))
+    return _host(fft_c2c(t, inverse=True))
 
 
 def circular_conv_oracle(x, h) -> np.ndarray:

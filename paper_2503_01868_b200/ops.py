@@ -283,6 +283,27 @@ def long_conv(v: torch.Tensor, taps: torch.Tensor, group_size: int = 1, q=None, 
         return gated_conv(v, taps, group_size, q=q, k=k)
 
 
+def fft_c2c(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    """Complex FFT of the last axis (power-of-two length, natural order) by the hand-written
+    Stockham kernel (hy_fft_c2c): forward unnormalised, inverse carrying 1/n (fft.py:116-125).
+    complex64 / complex128 CUDA tensors."""
+    if not x.is_cuda:
+        raise ValueError("paper_2503_01868_b200 ops need CUDA tensors (there is no CPU path)")
+    if x.dtype not in (torch.complex64, torch.complex128):
+        raise ValueError(f"fft_c2c takes complex64 / complex128, got {x.dtype}")
+    n = x.shape[-1]
+    xc = x.contiguous()
+    batch = xc.numel() // max(n, 1)
+    y = torch.empty_like(xc)
+    code = _lib.HY_F64 if x.dtype == torch.complex128 else _lib.HY_F32
+    lib = _lib.load()
+    nbytes = int(lib.hy_fft_c2c_workspace_size(batch, n, code))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=x.device)
+    _lib.check(lib.hy_fft_c2c(xc.data_ptr(), y.data_ptr(), batch, n, int(inverse), code, ws.data_ptr(), nbytes,
+                              _stream()), "fft_c2c")
+    return y / n if inverse else y
+
+
 def _modes(residues: torch.Tensor, poles: torch.Tensor, dev):
     r = residues.to(device=dev, dtype=torch.float32).contiguous()
     p = poles.to(device=dev, dtype=torch.float32).contiguous()
