@@ -943,7 +943,16 @@ class HyenaCP:
                 conv = (ops.long_conv(ext.contiguous(), taps, op.gs) if lh > 129
                         else ops.gated_conv(ext.contiguous(), taps, op.gs))[..., lh - 1:]
             mixed = fq * conv
-        y2 = op.out_project(mixed.contiguous())  # (2B, D, h)
+        mixed = mixed.contiguous()
+        if accumulate_into is not None and not op.split3:
+            # residual stacks: each half's out projection accumulates into its strided view of the
+            # caller's buffer inside the GEMM (cuBLAS beta = 1, ldc = m), as the sequential layout
+            acc = accumulate_into.unsqueeze(0) if x_local.dim() == 2 else accumulate_into
+            for i in range(2):
+                for b in range(B):
+                    acc[b, :, i * h:(i + 1) * h].addmm_(op.w_out_t, mixed[i * B + b])
+            return acc[0] if x_local.dim() == 2 else acc
+        y2 = op.out_project(mixed)  # (2B, D, h)
         y = torch.cat([y2[:B], y2[B:]], dim=-1)
         if accumulate_into is not None:
             acc = accumulate_into.unsqueeze(0) if x_local.dim() == 2 else accumulate_into
