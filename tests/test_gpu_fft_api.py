@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 from paper_2503_01868_b200 import fft
