@@ -273,6 +273,11 @@ def _zigzag_worker(rank, world, port, variant, stack, q):
         if rank == 0:
             y = _zigzag_merge(parts, world).float()
             y_ref = ref().float()
+            d = (y - y_ref).abs()
+            t = int(d.amax(dim=(0, 1)).argmax())
+            print(f"zigzag {variant}: rel {float(d.max() / max(1.0, float(y_ref.abs().max()))):.3e} at t={t} "
+                  f"(chunk {t // (L // (2 * world))}, offset {t % (L // (2 * world))}), max|y| "
+                  f"{float(y_ref.abs().max()):.2f}", flush=True)
             q.put(float((y - y_ref).abs().max() / max(1.0, float(y_ref.abs().max()))))
     finally:
         dist.destroy_process_group()

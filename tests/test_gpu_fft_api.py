@@ -117,6 +117,9 @@ def test_fft_c2c_kernel_vs_dft(dtype, n, batch):
     y = ops.fft_c2c(xd).cpu().numpy()
     want = oracle.fft(x.astype(np.complex64 if dtype == torch.complex64 else np.complex128))
     tol = 1e-12 if dtype == torch.complex128 else 1e-5
-    assert oracle.rel_err(y, want) < tol
+
+    def cerr(a, b):  # rel_err (testing.py:57-62) on complex values: inf-norm of the difference
+        return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1.0))
+    assert cerr(y, want) < tol
     back = ops.fft_c2c(torch.from_numpy(y).to("cuda", dtype), inverse=True).cpu().numpy()
-    assert oracle.rel_err(back, x) < tol
+    assert cerr(back, x) < tol
