@@ -290,4 +290,9 @@ def test_zigzag_cp_matches_single_gpu(variant, stack):
     predecessor chunk, LI runs the zigzag all-to-all; HyenaCP and a residual SE-MR-LI
     LayoutCP stack equal the single-GPU forward."""
     err = _run(_zigzag_worker, variant, stack)
-    assert err < 2e-2, err
+    # SE / MR are bitwise equal to the single-GPU forward; LI gates and rounds u / the conv output
+    # in separate bf16 passes around the all-to-all (the single-GPU mixer rounds once): ~1-2 bf16
+    # ulps per layer, and the three-layer residual stack grows to |y| ~ 180, where one ulp is 0.55%
+    assert err < (3e-2 if stack else 2e-2), err
+    if variant in ("MR", "SE"):
+        assert err == 0.0, err
