@@ -105,12 +105,21 @@ class ClockSampler:
         smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         while not self.stop_flag.is_set():
             try:
+                t = time.perf_counter()
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, smax, [n for n, b in bits.items() if r & b]))
+                self.samples.append((t, sm, smax, [n for n, b in bits.items() if r & b]))
             except Exception:  # noqa: BLE001 - sampling is best effort
                 pass
             time.sleep(self.INTERVAL_S)
+
+    def region(self, begin: bool) -> None:
+        """Mark the timed region's start / end (host time; the device work is synchronised on
+        both sides of the region, so host and device windows coincide)."""
+        if begin:
+            self.t_begin = time.perf_counter()
+        else:
+            self.t_end = time.perf_counter()
 
     def start(self):
         try:
@@ -132,12 +141,23 @@ class ClockSampler:
         if self.thread is not None:
             self.stop_flag.set()
             self.thread.join(timeout=2)
-            sm = [s[0] for s in self.samples]
-            reasons = sorted({r for s in self.samples for r in s[2]})
+            t0 = getattr(self, "t_begin", float("-inf"))
+            t1 = getattr(self, "t_end", float("inf"))
+            inside = [s for s in self.samples if t0 <= s[0] <= t1]
+            nearest = False
+            if not inside and self.samples:  # region shorter than one NVML round trip: nearest samples
+                before = [s for s in self.samples if s[0] < t0]
+                after = [s for s in self.samples if s[0] > t1]
+                inside = before[-1:] + after[:1]
+                nearest = True
+            sm = [s[1] for s in inside]
+            reasons = sorted({r for s in inside for r in s[3]})
+            gaps = [b[0] - a[0] for a, b in zip(self.samples, self.samples[1:])]
             return {"sm_mhz": statistics.median(sm) if sm else None,
-                    "sm_max_mhz": max(s[1] for s in self.samples) if sm else None,
+                    "sm_max_mhz": max(s[2] for s in inside) if sm else None,
                     "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
-                    "interval_ms": self.INTERVAL_S * 1e3, "source": "NVML"}
+                    "nearest_to_region": nearest, "region_ms": (t1 - t0) * 1e3 if t1 > t0 > float("-inf") else None,
+                    "sample_period_ms": statistics.median(gaps) * 1e3 if gaps else None, "source": "NVML"}
         return self._stop_smi()
 
     def _start_smi(self):
@@ -370,11 +390,13 @@ def run_ours(args, wl):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
+    sampler.region(True)
     t0.record(stream)
     for i in range(args.steps):
         run.step(evs[i])
     t1.record(stream)
     torch.cuda.synchronize()
+    sampler.region(False)
     launches = _lib.launch_count() - launches0
     clocks = sampler.stop()
     # parity sample: batch element 0 of this rank's input and of one more step's output
