@@ -722,10 +722,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         const int fb = gi & 1;
         const int eb = j & 1;
         mbar_wait(&efull[eb], (j >> 1) & 1);
-        // the tile's T0 . U (which starts the accumulator P . S_prev adds into) landed. Waited here,
-        // before eempty releases the converter: the T0 issuer cannot run two tiles ahead of this
-        // wait, so t0done's phase parity never aliases
-        mbar_wait(&t0done[eb], (j >> 1) & 1);
         if (lane == 0) trace(p, j, 9);
         tc_fence_after();
         float ev[NCH];
@@ -744,6 +740,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) trace(p, j, 10);
+        mbar_wait(&t0done[eb], (j >> 1) & 1);  // the tile's T0 . U (which starts the accumulator) landed
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
