@@ -76,10 +76,7 @@ constexpr int N_PROD_WARPS = 2;
 template <bool IMPL>
 struct Warps {
   static constexpr int SCAN = IMPL ? W_TB0 + N_TB_WARPS : -1;
-  // IMPL: the mode-input MMAs (Lam . U) have an issuing warp of their own, so the T0 . U
-  // issuer's tile period is 8 MMAs instead of 16
-  static constexpr int LMMA = IMPL ? SCAN + 1 : -1;
-  static constexpr int FMMA = W_TB0 + N_TB_WARPS + (IMPL ? 2 : 0), MMA = FMMA + 1, PROD = MMA + 1;
+  static constexpr int FMMA = W_TB0 + N_TB_WARPS + (IMPL ? 1 : 0), MMA = FMMA + 1, PROD = MMA + 1;
   static constexpr int THREADS = (PROD + N_PROD_WARPS) * 32;
 };
 constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
@@ -128,7 +125,7 @@ struct Layout {
   static constexpr int OFF_P2 = OFF_UP, OFF_L2 = OFF_UP + 8192;
   static_assert(OFF_L2 % 1024 == 0 && OFF_L2 + 4096 <= OFF_FQ, "implicit factor buffers");
   static constexpr int OFF_BAR = OFF_L + 2048;
-  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 10;
+  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 6;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -246,7 +243,7 @@ template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL>
 __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(const Params p) {
   using LY = Layout<KS>;
   constexpr int W_SCAN = Warps<IMPL>::SCAN, W_FMMA = Warps<IMPL>::FMMA, W_MMA = Warps<IMPL>::MMA,
-                W_PROD = Warps<IMPL>::PROD, W_LMMA = Warps<IMPL>::LMMA;
+                W_PROD = Warps<IMPL>::PROD;
   constexpr int STAGES = LY::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // keep the pointer in the shared window (offset arithmetic, not an integer round trip)
@@ -272,8 +269,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
   // explicit modes: T0 is double-buffered (tready[b] / tfree[b] per T0 buffer), T1 is single
   uint64_t* t1ready = tfreep + 2;        // [1] T builder -> MMA: T1 of the current group
   uint64_t* t1free = t1ready + 1;        // [1] MMA commit: last T1 . U_prev of a group retired
-  uint64_t* t0done = t1free + 1;         // [2] IMPL: MMA commit -> scan (the tile's T0 . U landed)
-  uint64_t* tfreel = t0done + 2;         // [2] IMPL: LMMA commit: last Lam . U of buffer b retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -298,7 +293,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], IMPL ? 2 : 1);  // IMPL: U is read by the T0 and the Lam MMA issuers
+      mbar_init(&uempty[i], 1);
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], N_EPI_WARPS);
       mbar_init(&tfull[i], 1);
@@ -311,10 +306,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     }
     mbar_init(t1ready, 1);
     mbar_init(t1free, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&t0done[i], 1);
-      mbar_init(&tfreel[i], 1);
-    }
     fence_mbar_init();
   }
   if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
@@ -454,8 +445,10 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
     const uint32_t t0a = tmem_base + TM_T0, t1a = tmem_base + TM_T1;
     if (IMPL) {
-      // per tile j: T0 . U (commit -> scan, which adds P . S_prev once the states are known);
-      // E = Lam . U is issued by the LMMA warp
+      // per tile j: T0 . U and E = Lam . U (one commit -> scan warp); the inter-chunk term
+      // P . S_prev of tile j is issued by the scan warp itself once the states are in SMEM
+      // (its efull wait orders it after this tile's T0 . U), keeping this loop short
+      const uint32_t la0 = smem_u32(smem + LY::OFF_L2);
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -468,20 +461,31 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         if (first) ++gi;
         g_prev = g;
         mbar_wait(&ufull[u], ph);  // U written and accumulator u drained (converter)
+        if (lane == 0) trace(p, j, 16);
+        if (lane == 0) trace(p, j, 17);
         if (lane == 0) trace(p, j, 4);
         const int fb = gi & 1;  // this group's factor buffer
         if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
+        if (lane == 0) trace(p, j, 18);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
+        const uint32_t de = tmem_base + TM_E + (j & 1) * NCH;
         const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
         const uint32_t ta = tmem_base + (fb ? TM_T0B : TM_T0);
+        const uint32_t la = la0 + fb * 2048;
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
             mma_bf16_ts(d, ta + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
           }
-          mma_commit(&t0done[j & 1]);
+#pragma unroll
+          for (int ks = 0; ks < LB / 16; ++ks) {
+            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
+            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_main,
+                     ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&efull[j & 1]);
           mma_commit(&uempty[u]);
           if (last) mma_commit(&tfree[fb]);
           trace(p, j, 7);
@@ -655,41 +659,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       if (lane == 0) mbar_arrive(&qempty[a]);
       if (quarter == 0 && lane == 0) trace(p, it, 6);
     }
-  } else if (IMPL && warp == W_LMMA) {
-    // ------------------------------------------------------------ IMPL mode-input MMA issuer
-    // E[n][chunk] = Lam . U (A = Lam[n][t] in SMEM, 8 rows re-read through a zero group stride)
-    constexpr uint32_t idesc_main = idesc_bf16_f32<LB, NCH>();
-    const uint32_t la0 = smem_u32(smem + LY::OFF_L2);
-    int gi = -1, g_prev = -1;
-    Tile t;
-    t.init(tb, p);
-    for (int j = 0; j < ntiles; ++j, t.next(p)) {
-      const int u = j % NBUF;
-      const int g = t.c / p.gs;
-      const bool first = g != g_prev;
-      const bool last = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
-      if (first) ++gi;
-      g_prev = g;
-      mbar_wait(&ufull[u], (j / NBUF) & 1);  // U written; E buffer j & 1 drained by the scan
-      const int fb = gi & 1;
-      if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
-      tc_fence_after();
-      const uint32_t de = tmem_base + TM_E + (j & 1) * NCH;
-      const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
-      const uint32_t la = la0 + fb * 2048;
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < LB / 16; ++ks) {
-          const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-          mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_main,
-                   ks > 0 ? 1u : 0u);
-        }
-        mma_commit(&efull[j & 1]);
-        mma_commit(&uempty[u]);
-        if (last) mma_commit(&tfreel[fb]);
-      }
-      __syncwarp();
-    }
   } else if (warp == W_SCAN) {
     // ------------------------------------------------------------ IMPL state scan
     // (lane n < NPOLE = mode n): E[n][chunk] from TMEM, then the sequential state
@@ -740,7 +709,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) trace(p, j, 10);
-        mbar_wait(&t0done[eb], (j >> 1) & 1);  // the tile's T0 . U (which starts the accumulator) landed
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + LY::OFF_S + (j % NBUF) * NCH * NPOLE * 4);
@@ -816,8 +784,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     auto build_impl = [&](int gb) {
       const int b = gb & 1;
       if (gb >= 2) {
-        mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);   // T0 of buffer b: last reader retired
-        mbar_wait(&tfreel[b], ((gb - 2) >> 1) & 1);  // Lam of buffer b
+        mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);   // T0 / Lam of buffer b: last readers retired
         mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);  // P of buffer b
       }
       float hv = 0.f, pm[NPOLE];
