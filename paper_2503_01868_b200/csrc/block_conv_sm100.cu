@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t a = ub + (ks >> 2) * U_ATOM + HROWS * 128 + (ks & 3) * 32;
-            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(a), idesc,
-                     ks > 0 ? 1u : 0u);
+            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(a),
+                     idesc_bf16_f32<64, NCH>(), ks > 0 ? 1u : 0u);  // M = 64: half the Lam re-reads
           }
           mma_commit(&efull[j & 1]);
           mma_commit(&uempty[u]);

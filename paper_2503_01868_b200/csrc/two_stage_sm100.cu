@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       // P . S_prev of tile j is issued by the scan warp itself once the states are in SMEM
       // (its efull wait orders it after this tile's T0 . U), keeping this loop short
       const uint32_t la0 = smem_u32(smem + LY::OFF_L2);
+      constexpr uint32_t idesc_e = idesc_bf16_f32<64, NCH>();
       int gi = -1, g_prev = -1;
       Tile t;
       t.init(tb, p);
@@ -482,7 +483,10 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
             const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_main,
+            // M = 64: the 8 mode rows are re-read through the zero group stride 8 times instead of
+            // 16 (half the shared-memory A traffic of an M = 128 MMA); rows 0..7 of D land in TMEM
+            // lanes 0..7 either way, where the scan warp reads them
+            mma_bf16(de, desc_sw128_sbo(la + (ks >> 2) * 1024 + (ks & 3) * 32, 0), desc_sw128(ua + bo), idesc_e,
                      ks > 0 ? 1u : 0u);
           }
           mma_commit(&efull[j & 1]);
