@@ -108,7 +108,13 @@ struct Layout {
   static constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES + F_SET;
   static constexpr int OFF_ST = 0;  // stages first: window over-reads stay inside SMEM
   static constexpr int OFF_U = round_up(OFF_ST + STAGES * STAGE_BYTES, 1024);  // U[NBUF]
-  static constexpr int OFF_UP = OFF_U + NBUF * NCH * LB * 2;   // U_prev[NBUF]
+  // explicit modes: U holds chunks -1 .. NCH-1 as rows 0 .. NCH (UROWS_X rows, 5 groups of 8), and
+  // T1 . U_prev reads it through a descriptor one row (128 B) earlier than T0 . U -- a shifted
+  // view, not a copy (the swizzle is a function of the address). It spills into the U_prev
+  // region below, which only the implicit mode uses (for its P / Lam double buffers)
+  static constexpr int UROWS_X = NCH + 8;
+  static constexpr int OFF_UP = OFF_U + NBUF * NCH * LB * 2;   // IMPL: P / Lam buffers
+  static_assert(NBUF * UROWS_X * LB * 2 <= 2 * NBUF * NCH * LB * 2, "explicit U buffers");
   static constexpr int OFF_FQ = OFF_UP + NBUF * NCH * LB * 2;  // featurized q, bf16 [NBUF]
   static constexpr int OFF_HP = OFF_FQ + NBUF * NCH * LB * 2;  // padded taps, bf16 [512]
   // implicit (LI) mode: P[m][n] = R_n lam_n^(m+1) (tf32 A operand, 128 x 8), per-chunk mode
@@ -148,8 +154,6 @@ struct Params {
   int B, C, L, lh, gs, lhf;
   int tiles_per_seq, total_tiles;
   int trace;
-  int exp_shift;  // debug (HY_TS_SHIFT): T1 . U_prev read as the U buffer one row back (1: base
-                  // offset 0, 2: base offset = (addr >> 7) & 7) -- row-offset descriptor probe
   // implicit, non-fused only: rows stored as L / seg_len time segments, element (row, t) at
   // row * seg_len + (t / seg_len) * seg_stride + t % seg_len (the rank-major layout of an
   // all-to-all buffer); seg_len = 0: plain rows of L. seg_len is a multiple of TILE_T.
@@ -514,14 +518,14 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         if (first) mbar_wait(&tready[fb], (gi >> 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + TM_ACC + u * NCH;
-        const uint32_t ua = smem_u32(smem + LY::OFF_U + u * NCH * LB * 2);
-        const uint32_t upa = smem_u32(smem + LY::OFF_UP + u * NCH * LB * 2);
+        constexpr int UR = LY::UROWS_X;
+        const uint32_t ua = smem_u32(smem + LY::OFF_U + u * UR * LB * 2);  // row 0 = chunk -1
         const uint32_t ta = fb ? tmem_base + TM_T0B : t0a;
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
-            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            mma_bf16_ts(d, ta + ks * 8, desc_sw128(ua + bo), idesc_main, ks > 0 ? 1u : 0u);
+            const uint32_t bo = (ks >> 2) * (UR * 128) + (ks & 3) * 32;
+            mma_bf16_ts(d, ta + ks * 8, desc_sw128(ua + 128 + bo), idesc_main, ks > 0 ? 1u : 0u);
           }
           if (last) mma_commit(&tfree[fb]);
           if (first) {
@@ -530,14 +534,8 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
           }
 #pragma unroll
           for (int ks = 0; ks < LB / 16; ++ks) {
-            const uint32_t bo = (ks >> 2) * (NCH * 128) + (ks & 3) * 32;
-            uint64_t bd = desc_sw128(upa + bo);
-            if (p.exp_shift) {
-              const uint32_t a = ua - 128 + bo;
-              bd = desc_sw128(a);
-              if (p.exp_shift == 2) bd |= static_cast<uint64_t>((a >> 7) & 7) << 49;
-            }
-            mma_bf16_ts(d, t1a + ks * 8, bd, idesc_main, 1u);
+            const uint32_t bo = (ks >> 2) * (UR * 128) + (ks & 3) * 32;
+            mma_bf16_ts(d, t1a + ks * 8, desc_sw128(ua + bo), idesc_main, 1u);  // rows 0..NCH-1: U_{n-1}
           }
           if (last) mma_commit(t1free);
           mma_commit(&uempty[u]);
@@ -587,8 +585,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       //    m/16 - 1, 16-byte unit m%16
       mbar_wait(&uempty[u], uph ^ 1);
       if (ctid == 0) trace(p, it, 2);
-      unsigned char* ub = smem + LY::OFF_U + u * NCH * LB * 2;
-      unsigned char* upb = smem + LY::OFF_UP + u * NCH * LB * 2;
+      unsigned char* ub = smem + LY::OFF_U + u * (IMPL ? NCH : LY::UROWS_X) * LB * 2;
 #pragma unroll
       for (int i = 0; i < KVB_PER; ++i) {
         const int b = half + 2 * i;
@@ -601,8 +598,11 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
           uv[e] = GK ? __uint_as_float(rv[i][e]) * __uint_as_float(rk[i][e]) : __uint_as_float(rv[i][e]);
         if (m < KV_WIN) {
           const int4 packed = pack8(uv);
-          if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
-          if (!IMPL && n + 1 < NCH) *reinterpret_cast<int4*>(upb + sw128_off(n + 1, j, NCH)) = packed;
+          if (IMPL) {
+            if (n >= 0) *reinterpret_cast<int4*>(ub + sw128_off(n, j, NCH)) = packed;
+          } else {  // chunk n at row n + 1 (row 0 = the chunk before the tile)
+            *reinterpret_cast<int4*>(ub + sw128_off(n + 1, j, LY::UROWS_X)) = packed;
+          }
         }
       }
       fence_proxy_async();
@@ -914,8 +914,6 @@ template <bool FEAT, bool GK, bool GQ, bool IMPL = false>
 static int launch(Params p, cudaStream_t st) {
   static const int tr = [] { const char* e = getenv("HY_TS_TRACE"); return e ? atoi(e) : 0; }();
   p.trace = tr;
-  const char* sh = getenv("HY_TS_SHIFT");  // read per launch: the probe flips it between calls
-  p.exp_shift = sh ? atoi(sh) : 0;
   if (p.lhf <= 9) return launch_ks<FEAT, GK, GQ, 1, IMPL>(p, st);
   return launch_ks<FEAT, GK, GQ, 2, IMPL>(p, st);
 }
