@@ -79,86 +79,111 @@ def load_peaks():
 
 
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled every 10 ms during the timed region
-    by a host thread over NVML (the library nvidia-smi reads); falls back to nvidia-smi's own
-    50 ms logging when NVML is unavailable."""
+    """SM clock and clock-event (throttle) reasons sampled every 5 ms during the timed region by
+    a separate sampler process over NVML (the library nvidia-smi reads; a process, so the bench's
+    Python thread never starves it of the GIL). Samples carry wall-clock stamps; the record keeps
+    the ones inside the timed region (or the nearest ones when the region is shorter than a
+    sampling period). Falls back to nvidia-smi's 50 ms logging when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
-    INTERVAL_S = 0.010
+    INTERVAL_S = 0.005
+    SAMPLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+bits = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+        ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+        ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+        ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+with open(sys.argv[2], "w", buffering=1) as out:
+    while True:
+        t = time.time()
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        out.write(f"{t:.6f},{sm},{smax}," + "|".join(n for n, b in bits if r & b) + "\n")
+        time.sleep(float(sys.argv[3]))
+"""
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
-        self.thread = None
-        self.samples = []
-        self.stop_flag = threading.Event()
-
-    def _nvml_loop(self, nv, h):
-        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
-                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
-                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
-                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
-                "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
-        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self.stop_flag.is_set():
-            try:
-                t = time.perf_counter()
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((t, sm, smax, [n for n, b in bits.items() if r & b]))
-            except Exception:  # noqa: BLE001 - sampling is best effort
-                pass
-            time.sleep(self.INTERVAL_S)
-
-    def region(self, begin: bool) -> None:
-        """Mark the timed region's start / end (host time; the device work is synchronised on
-        both sides of the region, so host and device windows coincide)."""
-        if begin:
-            self.t_begin = time.perf_counter()
-        else:
-            self.t_end = time.perf_counter()
+        self.nvml = False
+        self.t_begin = self.t_end = None
 
     def start(self):
+        import tempfile
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        # NVML enumerates physical GPUs; map through CUDA_VISIBLE_DEVICES when it is set
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = self.gpu
+        if vis and vis.split(",")[self.gpu].strip().isdigit():
+            idx = int(vis.split(",")[self.gpu])
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            # NVML enumerates physical GPUs; map through CUDA_VISIBLE_DEVICES when it is set
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[self.gpu].isdigit() else self.gpu
-            h = nv.nvmlDeviceGetHandleByIndex(idx)
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
-            self.thread.start()
-            time.sleep(0.05)
-            return
+            import pynvml  # noqa: F401
+            self.proc = subprocess.Popen([sys.executable, "-c", self.SAMPLER, str(idx), self.path,
+                                          str(self.INTERVAL_S)], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            self.nvml = True
+            for _ in range(200):  # wait for the first samples (process start-up)
+                time.sleep(0.01)
+                if os.path.getsize(self.path) > 0 or self.proc.poll() is not None:
+                    break
+            if self.proc.poll() is None:
+                return
         except Exception:  # noqa: BLE001
-            self.thread = None
+            pass
+        self.nvml = False
         self._start_smi()
 
+    def region(self, begin: bool) -> None:
+        """Mark the timed region's start / end (the device work is synchronised on both sides of
+        the region, so the host and device windows coincide)."""
+        if begin:
+            self.t_begin = time.time()
+        else:
+            self.t_end = time.time()
+
     def stop(self):
-        if self.thread is not None:
-            self.stop_flag.set()
-            self.thread.join(timeout=2)
-            t0 = getattr(self, "t_begin", float("-inf"))
-            t1 = getattr(self, "t_end", float("inf"))
-            inside = [s for s in self.samples if t0 <= s[0] <= t1]
-            nearest = False
-            if not inside and self.samples:  # region shorter than one NVML round trip: nearest samples
-                before = [s for s in self.samples if s[0] < t0]
-                after = [s for s in self.samples if s[0] > t1]
-                inside = before[-1:] + after[:1]
-                nearest = True
-            sm = [s[1] for s in inside]
-            reasons = sorted({r for s in inside for r in s[3]})
-            gaps = [b[0] - a[0] for a, b in zip(self.samples, self.samples[1:])]
-            return {"sm_mhz": statistics.median(sm) if sm else None,
-                    "sm_max_mhz": max(s[2] for s in inside) if sm else None,
-                    "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
-                    "nearest_to_region": nearest, "region_ms": (t1 - t0) * 1e3 if t1 > t0 > float("-inf") else None,
-                    "sample_period_ms": statistics.median(gaps) * 1e3 if gaps else None, "source": "NVML"}
-        return self._stop_smi()
+        if not self.nvml:
+            return self._stop_smi()
+        time.sleep(2 * self.INTERVAL_S)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for ln in fh:
+                    parts = ln.strip().split(",")
+                    if len(parts) == 4:
+                        rows.append((float(parts[0]), float(parts[1]), float(parts[2]),
+                                     [x for x in parts[3].split("|") if x]))
+            os.unlink(self.path)
+        except (OSError, ValueError):
+            pass
+        t0 = self.t_begin if self.t_begin is not None else float("-inf")
+        t1 = self.t_end if self.t_end is not None else float("inf")
+        inside = [r for r in rows if t0 <= r[0] <= t1]
+        nearest = False
+        if not inside and rows:
+            inside = [r for r in rows if r[0] < t0][-1:] + [r for r in rows if r[0] > t1][:1]
+            nearest = True
+        sm = [r[1] for r in inside]
+        gaps = [b[0] - a[0] for a, b in zip(rows, rows[1:])]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(r[2] for r in inside) if sm else None,
+                "sm_mhz_min": min(sm) if sm else None, "reasons": sorted({x for r in inside for x in r[3]}),
+                "samples": len(sm), "nearest_to_region": nearest,
+                "region_ms": (t1 - t0) * 1e3 if self.t_begin is not None and self.t_end is not None else None,
+                "sample_period_ms": statistics.median(gaps) * 1e3 if gaps else None,
+                "source": "NVML (sampler process)"}
 
     def _start_smi(self):
         import tempfile
