@@ -43,6 +43,7 @@
  *                           hyena.py:183-186     hyena_forward's LI inner conv, by exact per-mode scans
  *   hy_li_scan_mixer_fwd    hyena.py:162-186     the LI mixer (featurizers + gates + modal scan), fused
  *   hy_fft_c2c              fft.py:116-125       fft / ifft; cpsim.py:596-615 the distributed FFT's local transform
+ *   hy_gate_mul             hyena.py:186         q * conv_out (the CP LI layer's gate after the return all-to-all)
  *   hy_split3_cat           hyena.py:124,188     the fp32 projections' operand split (split-bf16 GEMM)
  *   hy_li_param_grad        hyena.py:193-211     filter_param_grads(ImplicitFilter, dtaps) fused with
  *                           core.py:255-268      the tap correlation it consumes
@@ -269,6 +270,9 @@ HY_API int hy_li_scan_mixer_fwd(const void* proj, void* y, const void* feat_taps
 HY_API size_t hy_fft_c2c_workspace_size(long long batch, long long n, int dtype);
 HY_API int hy_fft_c2c(const void* x, void* y, long long batch, long long n, int inverse, int dtype, void* ws,
                       size_t ws_bytes, void* stream);
+/* out = a * b elementwise over n contiguous elements (bf16 / fp32 / fp64, fp32 arithmetic for
+ * bf16): the LI context-parallel layer's q gate on the returned slab (hyena.py:186). */
+HY_API int hy_gate_mul(const void* a, const void* b, void* out, long long n, int dtype, void* stream);
 /* fp32 activation -> the K-concatenated bf16 operand of the split-bf16 fp32 GEMM (blas.py; the
  * fp32 projections of hyena.py:124,188 on tensor cores): x (batch, K, N) fp32, out
  * (batch, 5K, N) bf16 = [X1; X2; X0; X1; X0] with X0 = bf16(x), X1 = bf16(x - X0),

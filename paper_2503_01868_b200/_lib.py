@@ -59,6 +59,7 @@ SIGNATURES = {
     "hy_li_scan_mixer_fwd": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hy_fft_c2c_workspace_size": (_SZ, [ctypes.c_longlong, ctypes.c_longlong, _I]),
     "hy_fft_c2c": (_I, [_P, _P, ctypes.c_longlong, ctypes.c_longlong, _I, _I, _P, _SZ, _P]),
+    "hy_gate_mul": (_I, [_P, _P, _P, ctypes.c_longlong, _I, _P]),
     "hy_split3_cat": (_I, [_P, _P, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _P]),
 }
 

@@ -748,7 +748,7 @@ class HyenaCP:
                     else:
                         back = torch.empty((n, slab, m), dtype=x3.dtype, device=x3.device)
                         _all_to_all(grp, back, y_slab)
-                    torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
+                    ops.gate_mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
                     if peer is not None:
                         peer[1].release(k)
                 u_s.record_stream(comm)
@@ -808,7 +808,7 @@ class HyenaCP:
             fq_s, _, kb = live.pop(s)
             for b in range(B):
                 back = peer[1].wait(*kb[b])
-                torch.mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
+                ops.gate_mul(fq_s[b], back.view(seg, m), out=mixed[b, s * seg:(s + 1) * seg])
                 peer[1].release(*kb[b])
 
         for it in range(self.n_pipe + 2):

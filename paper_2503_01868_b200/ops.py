@@ -304,6 +304,19 @@ def fft_c2c(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
     return y / n if inverse else y
 
 
+def gate_mul(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = a * b (hy_gate_mul): contiguous CUDA tensors of one dtype and element count."""
+    _check_device(a, b, out)
+    if a.numel() != b.numel() or a.dtype != b.dtype or (out is not None and (out.numel() != a.numel()
+                                                                             or out.dtype != a.dtype)):
+        raise ValueError("gate_mul operands must match in size and dtype")
+    out = torch.empty_like(a) if out is None else out
+    lib = _lib.load()
+    _lib.check(lib.hy_gate_mul(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _dtype_code(a), _stream()),
+               "gate_mul")
+    return out
+
+
 def _modes(residues: torch.Tensor, poles: torch.Tensor, dev):
     r = residues.to(device=dev, dtype=torch.float32).contiguous()
     p = poles.to(device=dev, dtype=torch.float32).contiguous()

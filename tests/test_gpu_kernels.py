@@ -622,3 +622,14 @@ def test_block_conv_tcgen05_golden_and_known_answers():
     assert np.array_equal(y, v)
     with pytest.raises(NotImplementedError):
         ops.block_conv(dev(v, torch.bfloat16), dev(np.ones((3, 514))), 1)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("n", [1, 7, 4096, 100003])
+def test_gate_mul(dtype, n):
+    """hy_gate_mul (the CP LI layer's q gate): bitwise the rounding of the fp32 / fp64 product."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    a = torch.randn(n, device="cuda", generator=g).to(dtype)
+    b = torch.randn(n, device="cuda", generator=g).to(dtype)
+    want = (a.double() * b.double()).to(dtype) if dtype != torch.float64 else a * b
+    assert torch.equal(ops.gate_mul(a, b), want)
