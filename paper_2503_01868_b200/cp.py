@@ -885,7 +885,7 @@ class HyenaCP:
                 conv = p2p_conv_overlapped(u, self.cfg.inner, grp,
                                            conv=lambda z: ops.gated_conv(z.contiguous(), taps, op.gs),
                                            correct=lambda h, y: _correct(h, y, taps, op.gs))
-            mixed = q * conv
+            mixed = ops.gate_mul(q, conv.contiguous())
         acc = None
         if accumulate_into is not None:
             acc = accumulate_into.unsqueeze(0) if x_local.dim() == 2 else accumulate_into
@@ -942,8 +942,7 @@ class HyenaCP:
                 ext = torch.cat([uh, u], dim=-1) if uh is not None else u
                 conv = (ops.long_conv(ext.contiguous(), taps, op.gs) if lh > 129
                         else ops.gated_conv(ext.contiguous(), taps, op.gs))[..., lh - 1:]
-            mixed = fq * conv
-        mixed = mixed.contiguous()
+            mixed = ops.gate_mul(fq, conv.contiguous())
         if accumulate_into is not None and not op.split3:
             # residual stacks: each half's out projection accumulates into its strided view of the
             # caller's buffer inside the GEMM (cuBLAS beta = 1, ldc = m), as the sequential layout
