@@ -112,6 +112,16 @@ def main():
             ms = timeit(lambda: ops.li_conv(v, res, poles, 1))
             report("li_conv_ungated", ms, 4 * D * L, D=D, L=L)
             del proj, v
+        # the CP layer's per-segment slab conv at L = 1M (the all-to-all's rank-major layout):
+        # N = 2 / 4 ranks, n_pipe = 4 segments -> 512 / 256 channels of the full sequence
+        for n in (2, 4):
+            C, m = D // (4 * n), (1 << 20) // n
+            buf = torch.randn((n, C, m), device=dev, dtype=torch.bfloat16, generator=g)
+            res = torch.randn((C, 8), device=dev, generator=g) / 8
+            poles = torch.rand((C, 8), device=dev, generator=g) * 1.9 - 0.95
+            ms = timeit(lambda: ops.li_conv_segmented(buf, res, poles, 1))
+            report(f"li_conv_segmented_cp{n}", ms, 4 * C * (1 << 20), C=C, L=1 << 20, n_seg=n)
+            del buf
     if args.which in ("all", "scan"):
         # modal-scan LI kernels (CUDA cores) at C3: fp32 mixer (the reference precision), bf16
         # ungated conv (vs li_conv_ungated above) and the bf16 mixer
