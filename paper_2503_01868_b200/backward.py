@@ -228,12 +228,17 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         poles = torch.tensor(np.stack([f.poles for f in inner.filters]), dtype=torch.float32, device=x3.device)
     ts_ok = op.dtype == torch.bfloat16 and op.lh <= 129 and L % 8 == 0 and op.inner_taps is not None \
         and not implicit
+    # longer explicit / MR filters: the K-block tcgen05 conv (forward c and the reversed-time du)
+    kb_ok = op.dtype == torch.bfloat16 and 129 < op.lh <= ops.BLOCK_CONV_MAX_LH and L % 8 == 0 \
+        and op.inner_taps is not None and not implicit
 
     def inner_conv(a):
         if modal:
             return ops.li_conv(a, res, poles, op.gs)
         if ts_ok:
             return ops.two_stage(a, op.inner_taps, op.gs, decay=op.decay)
+        if kb_ok:
+            return ops.block_conv(a, op.inner_taps, op.gs, decay=op.decay)
         if op.cfg.variant == "LI" and op.li_scan_modes is not None:
             return ops.li_scan(a, op.li_scan_modes[0], op.li_scan_modes[1], op.gs)  # exact modal scans
         if op.lh > 129 or op.cfg.variant == "LI":
@@ -251,7 +256,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
 
     dmixed = wt_mm("_w_out_bwd_parts", op.w_out_t, dy3)
     fused = op.dtype != torch.float64 and op.lhf <= 8 and L % 8 == 0
-    rev = fused and (modal or ts_ok)  # du runs as the causal tcgen05 conv of the reversed dc
+    rev = fused and (modal or ts_ok or kb_ok)  # du runs as the causal tcgen05 conv of the reversed dc
     dc_rev = None
     if fused:
         # featurizers recomputed in-stream: u = fk * fv and dc = dmixed * fq, one pass
@@ -260,7 +265,7 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
         else:
             u, dc = ops.mixer_bwd_prep(proj, dmixed, op.feat_taps)
         c = inner_conv(u)
-        mixed = op.mixer(proj) if (modal or ts_ok) else None  # fused tcgen05 forward mixer
+        mixed = op.mixer(proj) if (modal or ts_ok or kb_ok) else None  # fused tcgen05 forward mixer
         if mixed is None:
             mixed = ops.causal_conv(proj[:, :D].contiguous(), op.feat_taps[0], 1) * c
     else:
@@ -301,6 +306,16 @@ def operator_backward(op, x: torch.Tensor, dy: torch.Tensor, proj: torch.Tensor 
             mark("inner_taps", 0)
             dtaps = ops.two_stage_taps_grad(dc, u, op.lh, op.gs)  # tcgen05, both passes fused
             mark("inner_taps", 1)
+        elif kb_ok:
+            # du as the causal K-block conv of the reversed dc (the transposed factors are the
+            # forward factors on reversed time); the tap gradient by the generic correlation
+            rdc = dc_rev if rev else torch.flip(dc, dims=[-1]).contiguous()
+            rdu = ops.block_conv(rdc, op.inner_taps, op.gs, decay=op.decay)
+            if rev:
+                du_rev = rdu
+            else:
+                du = torch.flip(rdu, dims=[-1])
+            _, dtaps = ops.causal_conv_bwd(dc, u, op.lh, op.gs, want_dx=False)
         else:
             du, dtaps = ops.causal_conv_bwd(dc, u, taps, op.gs)
         if implicit:  # fp64: pull the tap gradient back through h_t = sum_n R_n lam_n^t

@@ -152,11 +152,14 @@ def _oracle_cfg_of(cfg):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("variant,D,L,gs", [("SE", 16, 1024, 1), ("MR", 16, 2048, 2), ("LI", 16, 4096, 1)])
+@pytest.mark.parametrize("variant,D,L,gs", [("SE", 16, 1024, 1), ("MR", 16, 2048, 2), ("LI", 16, 4096, 1),
+                                             ("MR300", 16, 2048, 1)])
 def test_operator_backward_vs_oracle(dtype, variant, D, L, gs):
     B = 2
     rng = hy.make_rng(77)
-    kw = {"seq_len": L} if variant == "LI" else {"inner_len": 128 if variant == "MR" else None}
+    lh = 300 if variant == "MR300" else 128  # MR300: bf16 forward / du on the K-block tcgen05 conv
+    variant = "MR" if variant == "MR300" else variant
+    kw = {"seq_len": L} if variant == "LI" else {"inner_len": lh if variant == "MR" else None}
     cfg = hy.make_hyena_config(variant, D, rng, group_size=gs, block_size=128 if variant == "MR" else 16, **kw)
     rnd = _bf16 if dtype == "bf16" else (lambda a: np.asarray(a, dtype=np.float32).astype(np.float64))
     cfg = _rounded_cfg(cfg, rnd)
