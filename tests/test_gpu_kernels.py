@@ -633,3 +633,24 @@ def test_gate_mul(dtype, n):
     b = torch.randn(n, device="cuda", generator=g).to(dtype)
     want = (a.double() * b.double()).to(dtype) if dtype != torch.float64 else a * b
     assert torch.equal(ops.gate_mul(a, b), want)
+
+
+def test_new_kernels_edge_cases():
+    """Edge shapes of this round's kernels: K-block conv with lh = 1 (only T_0), L = 1 and L < 8
+    (padded rows), groups; modal scan with L = 1 and a single pole; FFT over more rows than a
+    grid dimension holds."""
+    rng = np.random.default_rng(17)
+    for B, C, L, lh, gs in ((2, 4, 1, 1, 2), (1, 3, 5, 200, 3), (3, 2, 8, 130, 1)):
+        v = bf16_round(rng.standard_normal((B, C, L)))
+        taps = bf16_round(rng.standard_normal((C // gs, lh)) / np.sqrt(lh))
+        y = ops.block_conv(dev(v, torch.bfloat16), dev(taps), gs).double().cpu().numpy()
+        for b in range(B):
+            want = oracle.block_conv(v[b], explicit_bank_from_taps(taps, gs), 16)
+            assert oracle.rel_err(y[b], want) < TOL["bf16"], (B, C, L, lh)
+    v = rng.standard_normal((2, 3, 1))
+    y = ops.li_scan(dev(v), torch.tensor([[0.5]] * 3, dtype=torch.float64), torch.tensor([[0.9]] * 3, dtype=torch.float64))
+    assert np.allclose(y.double().cpu().numpy(), 0.5 * v.astype(np.float32), rtol=1e-6)
+    x = torch.randn((70000, 4), dtype=torch.complex64, device="cuda")
+    got = ops.fft_c2c(x).cpu().numpy()
+    want = np.fft.fft(x.cpu().numpy(), axis=-1)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-5
