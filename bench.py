@@ -387,6 +387,99 @@ class Runner:
         return self.fwd(self.x, ev)
 
 
+def kernel_info(run, kern_ms, peaks, wl, ws) -> list:
+    """Roofline entries of the workload's hand-written kernels from their in-step event times."""
+    kinfo = []
+    for kd, ms in zip(run.kernels, kern_ms):
+        if isinstance(kd, dict):  # explicit kernel description (train workloads)
+            if kd["bound"] == "hbm":
+                ach, peak = kd["work"] / (ms * 1e-3) / 1e9, peaks["hbm_gbs"]
+                extra = {"algorithmic_bytes_per_launch": kd["work"]}
+            else:
+                ach = kd["work"] / (ms * 1e-3) / 1e12
+                peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+                extra = {"algorithmic_flops_per_launch": kd["work"],
+                         "peak_source_note": "derived FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 x sm_max_mhz"}
+            kinfo.append({"kernel": kd["kernel"], "label": kd["label"], "bound": kd["bound"], "achieved": ach,
+                          "peak": peak, "unit": kd["unit"], "frac": ach / peak, **extra, "launch_ms": ms})
+            continue
+        label, variant, nbytes = kd
+        ach = nbytes / (ms * 1e-3) / 1e9
+        kinfo.append({"kernel": MIXER_KERNEL[variant] if (wl["kind"] != "cp" or ws == 1) else
+                      "block_conv_kernel<IMPL> (hy_li_conv_segmented_fwd: implicit long conv of the rank's channel "
+                      "slab, 64-chunk staged-row tcgen05 kernel)",
+                      "label": label, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                      "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": nbytes, "launch_ms": ms})
+    return kinfo
+
+
+# The other BASELINE configs, measured device-side in the same run as the headline line (the
+# driver runs only the default workload): N = 1 -> C1, C3 (bf16 and the reference's fp32), C4 and
+# C5's single-GPU operator at L = 1M; N > 1 -> the C5 context-parallel LI layer at L = 1M.
+EXTRA_N1 = ("se", "li", "li_f32", "stripe", "li_cp")
+EXTRA_NN = ("li_cp",)
+
+
+def measure_extra(names, args, ws, rank, local) -> dict:
+    """Device-side lines of the other configs: W' = 2 warm-up and K' = min(K, 5) timed steps
+    each (barrier + synchronize on both sides, max over ranks), in-step kernel rooflines and
+    clocks; no e2e / CPU legs (those are the headline's). Failures are recorded, not raised."""
+    import gc
+
+    import torch
+    import torch.distributed as dist
+    out = {}
+    steps = max(3, min(args.steps, 5))
+    peaks, _ = load_peaks()
+    for name in names:
+        wl = WORKLOADS[name]
+        if ws == 1 and wl["kind"] == "cp":  # one rank: the fused single-GPU operator at L = 1M
+            wl = dict(wl, kind="op", desc=wl["desc"] + "; N = 1: the fused single-GPU operator")
+        run = None
+        try:
+            run = Runner(wl, ws, rank)
+            for _ in range(2):
+                run.step()
+            torch.cuda.synchronize()
+            if dist.is_initialized():
+                dist.barrier()
+            nk = len(run.kernels)
+            evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nk)]
+                   for _ in range(steps)]
+            sampler = ClockSampler(local)
+            sampler.start()
+            stream = torch.cuda.current_stream()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            sampler.region(True)
+            t0.record(stream)
+            for i in range(steps):
+                run.step(evs[i])
+            t1.record(stream)
+            torch.cuda.synchronize()
+            sampler.region(False)
+            clocks = sampler.stop()
+            ms = _max_over_ranks(t0.elapsed_time(t1), ws) / steps
+            kern_ms = [statistics.mean(evs[i][j][0].elapsed_time(evs[i][j][1]) for i in range(steps)) for j in range(nk)]
+            kinfo = kernel_info(run, kern_ms, peaks, wl, ws)
+            dom = max(kinfo, key=lambda k: k["launch_ms"]) if kinfo else None
+            out[name] = {"workload": wl["desc"], "value": run.tokens_step / (ms * 1e-3), "unit": "tokens/s",
+                         "ms_per_step": ms, "steps": steps, "warmup": 2, "dtype": wl["dtype"],
+                         "scaling": "strong" if wl["kind"] == "cp" else "weak", "parallelism": run.parallelism,
+                         "roofline": None if dom is None else {k: dom[k] for k in ("kernel", "label", "bound", "achieved",
+                                                                                   "peak", "unit", "frac", "launch_ms")},
+                         "roofline_operator_frac": operator_roofline(run.op_flops / ws / (ms * 1e-3) / 1e12, peaks,
+                                                                     wl["dtype"], run.op_flops // ws)["frac"],
+                         "clocks": clocks}
+        except Exception as e:  # noqa: BLE001 - the headline line must survive an extra config
+            out[name] = {"workload": wl["desc"], "error": f"{type(e).__name__}: {e}"}
+        finally:
+            del run
+            gc.collect()
+            torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
@@ -456,26 +549,7 @@ def run_ours(args, wl):
     e2e_ms = _max_over_ranks(e0.elapsed_time(e1), ws)
 
     peaks, peaks_kind = load_peaks()
-    kinfo = []
-    for kd, ms in zip(run.kernels, kern_ms):
-        if isinstance(kd, dict):  # explicit kernel description (train workloads)
-            if kd["bound"] == "hbm":
-                ach, peak = kd["work"] / (ms * 1e-3) / 1e9, peaks["hbm_gbs"]
-                extra = {"algorithmic_bytes_per_launch": kd["work"]}
-            else:
-                ach = kd["work"] / (ms * 1e-3) / 1e12
-                peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-                extra = {"algorithmic_flops_per_launch": kd["work"],
-                         "peak_source_note": "derived FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 x sm_max_mhz"}
-            kinfo.append({"kernel": kd["kernel"], "label": kd["label"], "bound": kd["bound"], "achieved": ach,
-                          "peak": peak, "unit": kd["unit"], "frac": ach / peak, **extra, "launch_ms": ms})
-            continue
-        label, variant, nbytes = kd
-        ach = nbytes / (ms * 1e-3) / 1e9
-        kinfo.append({"kernel": MIXER_KERNEL[variant] if (wl["kind"] != "cp" or ws == 1) else
-                      "two_stage_kernel<IMPL> (hy_li_conv_fwd: implicit long conv of the rank's channel slab)",
-                      "label": label, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                      "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": nbytes, "launch_ms": ms})
+    kinfo = kernel_info(run, kern_ms, peaks, wl, ws)
     dom = max(kinfo, key=lambda k: k["launch_ms"])
     dom = dict(dom, traffic=ncu_traffic(args.workload), peak_source=peaks_kind)
     op_tf = run.op_flops / ws / (ms_step * 1e-3) / 1e12
@@ -513,6 +587,9 @@ def run_ours(args, wl):
         "clocks": clocks,
         "gpu_launches": launches,
     }
+    if not args.no_extra_configs and args.workload == "mr":
+        del run, pipe, xh, yh
+        result["other_configs"] = measure_extra(EXTRA_N1 if ws == 1 else EXTRA_NN, args, ws, rank, local)
     if dist.is_initialized():
         dist.destroy_process_group()
     return result, rank, parity_io
@@ -714,6 +791,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="mr", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="skip the other BASELINE configs measured after the headline line")
     ap.add_argument("--group-size", type=int, default=1, help="filter group size d_g (1 = reference default)")
     args = ap.parse_args()
     global GROUP_SIZE
