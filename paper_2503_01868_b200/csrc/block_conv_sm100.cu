@@ -91,7 +91,7 @@ constexpr int OFF_L = round_up(OFF_HP + 2 * HP_N * 2, 1024);  // IMPL: Lam[2] (b
 constexpr int OFF_P = OFF_L + 2 * 2048;                    // IMPL: P[2] (tf32, 128 x 8)
 constexpr int OFF_S = OFF_P + 2 * 4096;                    // IMPL: S_prev[NBUF] (tf32, 64 x 8)
 constexpr int OFF_BAR = OFF_S + NBUF * NCH * NPOLE * 4;
-constexpr int N_BARS = 2 * 8 + 5 * NBUF + 12;
+constexpr int N_BARS = 2 * 8 + 5 * NBUF + 10;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
   uint64_t* efull = tfreep + 2;      // [2] IMPL: MMA commit -> scan (E in TMEM)
   uint64_t* eempty = efull + 2;      // [2] IMPL: scan -> converter (E drained)
   uint64_t* qfull = eempty + 2;      // [NBUF] FEAT: converter -> epilogue (featurized q in SMEM)
-  uint64_t* pready = qfull + NBUF;   // [2] IMPL: builder -> scan: P of buffer b written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -253,7 +252,6 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
       mbar_init(&tfreep[i], 1);
       mbar_init(&efull[i], 1);
       mbar_init(&eempty[i], 1);
-      mbar_init(&pready[i], 1);
     }
     fence_mbar_init();
   }
@@ -525,28 +523,19 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
       // retired: T_0 from h[t] = sum_n R_n lam_n^t (t < 128) in TMEM; P[m][n] = R_n lam_n^(m+1)
       // (tf32 A operand, element (m, n) at (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes);
       // Lam[n][t] = lam_n^(127 - t) (bf16, SW128 K-major, 8 rows)
-      // The T0 / Lam half of a build waits only for the MMA issuer's last use of the buffer
-      // (tfree), the P half also for the scan's (tfreep, which trails by about a tile); split
-      // (tready -> MMA issuer, pready -> scan) the issuer never waits on the scan's lag, which
-      // left about one tile of slack per group and made short sequences (L = 16384: two tiles
-      // per group at gs = 1) build-bound. The next group's modes are prefetched into registers.
-      float pf_pole[NPOLE], pf_res[NPOLE];
-      auto prefetch = [&](int g) {
-#pragma unroll
-        for (int n = 0; n < NPOLE; ++n) {
-          const bool ok = n < p.npoles;
-          pf_pole[n] = ok ? p.poles[static_cast<size_t>(g) * p.npoles + n] : 0.f;
-          pf_res[n] = ok ? p.residues[static_cast<size_t>(g) * p.npoles + n] : 0.f;
-        }
-      };
-      auto build_impl = [&](int gb) {
+      auto build_impl = [&](int gb, int g) {
         const int b = gb & 1;
-        if (gb >= 2) mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);
+        if (gb >= 2) {
+          mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);
+          mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);
+        }
         float hv = 0.f, pm[NPOLE];
         unsigned char* lrow = smem + OFF_L + b * 2048 + (bt >> 6) * 1024 + (bt & 7) * 2;
 #pragma unroll
         for (int n = 0; n < NPOLE; ++n) {
-          const float lam = pf_pole[n], res = pf_res[n];
+          const bool ok = n < p.npoles;
+          const float lam = ok ? p.poles[static_cast<size_t>(g) * p.npoles + n] : 0.f;
+          const float res = ok ? p.residues[static_cast<size_t>(g) * p.npoles + n] : 0.f;
           const float la = log2f(fabsf(lam));
           // lam^e for integer e as exp2(e log2|lam|) with the sign of lam^e (0^0 = 1)
           auto ipow = [&](int e) {
@@ -564,6 +553,9 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
         bf16* hb = hpad + HP_N * b;
         hb[bt] = __float2bfloat16_rn(0.f);
         hb[128 + bt] = __float2bfloat16_rn(hv);
+        float* pa = reinterpret_cast<float*>(smem + OFF_P + b * 4096 + (bt & 7) * 16 + (bt >> 3) * 256);
+        *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
+        *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
         fence_proxy_async();
         named_bar_sync(BAR_TB, TB_THREADS);
         tc_fence_after();
@@ -572,28 +564,14 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
         tc_fence_before();
         named_bar_sync(BAR_TB, TB_THREADS);
         if (bt == 0) mbar_arrive(&tready[b]);
-        if (gb >= 2) mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);
-        float* pa = reinterpret_cast<float*>(smem + OFF_P + b * 4096 + (bt & 7) * 16 + (bt >> 3) * 256);
-        *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
-        *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
-        fence_proxy_async();
-        named_bar_sync(BAR_TB, TB_THREADS);
-        if (bt == 0) mbar_arrive(&pready[b]);
       };
       int gi = 0, g_prev = -1;
       for (int j = 0; j < ntiles; ++j, t.next(p)) {
         const int g = t.c / p.gs;
         if (g == g_prev) continue;
         g_prev = g;
-        if (gi == 0) {
-          prefetch(g);
-          build_impl(0);
-          if (g < g_end) prefetch(g + 1);
-        }
-        if (g < g_end) {
-          build_impl(gi + 1);  // the next group, into the other buffer
-          if (g + 1 < g_end) prefetch(g + 2);
-        }
+        if (gi == 0) build_impl(0, g);
+        if (g < g_end) build_impl(gi + 1, g + 1);  // the next group, into the other buffer
         ++gi;
       }
     } else {
@@ -636,15 +614,13 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) block_conv_kernel(con
       for (int j = 0; j < ntiles; ++j, t.next(p)) {
         const int g = t.c / p.gs;
         const bool lst = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
-        const bool newgrp = g != g_prev;
-        if (newgrp) {
+        if (g != g_prev) {
           g_prev = g;
           ++gi;
           lam128 = powf(pf, 128.f);
           if (g < g_end) pf = pole(g + 1);
         }
         const int fb = gi & 1, eb = j & 1, a = j % NBUF;
-        if (newgrp) mbar_wait(&pready[fb], (gi >> 1) & 1);  // P of this group written
         mbar_wait(&efull[eb], (j >> 1) & 1);
         tc_fence_after();
         float ev[NCH];

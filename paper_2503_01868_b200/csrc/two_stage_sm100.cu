@@ -131,7 +131,7 @@ struct Layout {
   static constexpr int OFF_P2 = OFF_UP, OFF_L2 = OFF_UP + 8192;
   static_assert(OFF_L2 % 1024 == 0 && OFF_L2 + 4096 <= OFF_FQ, "implicit factor buffers");
   static constexpr int OFF_BAR = OFF_L + 2048;
-  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 8;
+  static constexpr int N_BARS = 2 * STAGES + 8 + 7 * NBUF + 6;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-byte alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -273,7 +273,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
   // explicit modes: T0 is double-buffered (tready[b] / tfree[b] per T0 buffer), T1 is single
   uint64_t* t1ready = tfreep + 2;        // [1] T builder -> MMA: T1 of the current group
   uint64_t* t1free = t1ready + 1;        // [1] MMA commit: last T1 . U_prev of a group retired
-  uint64_t* pready = t1free + 1;         // [2] IMPL: builder -> scan: P of factor buffer b written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::OFF_TMEM);
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
@@ -311,8 +310,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     }
     mbar_init(t1ready, 1);
     mbar_init(t1free, 1);
-    mbar_init(&pready[0], 1);
-    mbar_init(&pready[1], 1);
     fence_mbar_init();
   }
   if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
@@ -689,8 +686,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       for (int j = 0; j < ntiles; ++j, t.next(p)) {
         const int g = t.c / p.gs;
         const bool lst = j + 1 < ntiles && t.last_of_channel(p) && (t.c + 1) / p.gs != g;
-        const bool newgrp = g != g_prev;
-        if (newgrp) {
+        if (g != g_prev) {
           g_prev = g;
           ++gi;
           lam128 = powf(pf, 128.f);
@@ -698,7 +694,6 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
         }
         const int fb = gi & 1;
         const int eb = j & 1;
-        if (newgrp) mbar_wait(&pready[fb], (gi >> 1) & 1);  // P of this group written
         mbar_wait(&efull[eb], (j >> 1) & 1);
         if (lane == 0) trace(p, j, 9);
         tc_fence_after();
@@ -790,13 +785,12 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     // h[t] = sum_n R_n lam_n^t for t < 128 (T0 only; longer lags go through the states),
     // P[m][n] = R_n lam_n^(m+1) as the tf32 A operand (element (m, n) at
     // (m%8)*16 + (m/8)*256 + (n%4)*4 + (n/4)*128 bytes) and Lam[n][t] = lam_n^(127 - t)
-    // The T0 / Lam half of a build waits only for the MMA issuer's last use of the buffer
-    // (tfree); the P half also for the scan's (tfreep, which trails by about a tile) and is
-    // signalled separately (pready), so the MMA issuer never waits on the scan's lag -- with
-    // four tiles per group (L = 16384, gs = 1) that lag made the mixer build-bound.
     auto build_impl = [&](int gb) {
       const int b = gb & 1;
-      if (gb >= 2) mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);  // T0 / Lam of buffer b: last readers retired
+      if (gb >= 2) {
+        mbar_wait(&tfree[b], ((gb - 2) >> 1) & 1);   // T0 / Lam of buffer b: last readers retired
+        mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);  // P of buffer b
+      }
       float hv = 0.f, pm[NPOLE];
       unsigned char* lrow = smem + LY::OFF_L2 + b * 2048 + (bt >> 6) * 1024 + (bt & 7) * 2;
 #pragma unroll
@@ -820,16 +814,12 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       hpad[128 + bt] = __float2bfloat16_rn(hv);
       hpad[256 + bt] = __float2bfloat16_rn(0.f);
       hpad[384 + bt] = __float2bfloat16_rn(0.f);
-      fence_proxy_async();
-      named_bar_sync(BAR_TB, TB_THREADS);
-      build(0, b ? TM_T0B : TM_T0, &tready[b], hpad);
-      if (gb >= 2) mbar_wait(&tfreep[b], ((gb - 2) >> 1) & 1);  // P of buffer b: the scan's last use
       float* pa = reinterpret_cast<float*>(smem + LY::OFF_P2 + b * 4096 + (bt & 7) * 16 + (bt >> 3) * 256);
       *reinterpret_cast<float4*>(pa) = make_float4(pm[0], pm[1], pm[2], pm[3]);
       *reinterpret_cast<float4*>(pa + 32) = make_float4(pm[4], pm[5], pm[6], pm[7]);
       fence_proxy_async();
       named_bar_sync(BAR_TB, TB_THREADS);
-      if (bt == 0) mbar_arrive(&pready[b]);
+      build(0, b ? TM_T0B : TM_T0, &tready[b], hpad);
     };
     int gi = 0, g_prev = -1;
     Tile t;
