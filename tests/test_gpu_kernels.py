@@ -309,10 +309,12 @@ def test_li_conv_many_sequences_per_cta():
     assert oracle.rel_err(y[0][sel], want) < TOL["bf16"]
 
 
-def test_li_conv_segmented_equals_natural():
+@pytest.mark.parametrize("m", [8192, 4096])
+def test_li_conv_segmented_equals_natural(m):
     # the all-to-all buffer layout (n_seg, C, seg_len): row c = buf[0, c] | buf[1, c] | ...
+    # (segments of 8192: the 64-chunk kernel; 4096: the 32-chunk kernel's segmented mode)
     rng = np.random.default_rng(12)
-    n, C, m = 3, 40, 8192
+    n, C = 3, 40
     poles = dev(rng.uniform(-0.99, 0.99, (C, 8)))
     residues = dev(rng.standard_normal((C, 8)) / 8)
     v = dev(bf16_round(rng.standard_normal((C, n * m))), torch.bfloat16)
