@@ -39,6 +39,8 @@
  *                           hyena.py:262-270     products of hyena_backward (one HBM pass)
  *   hy_two_stage_taps_grad  blockconv.py:246-262 two_stage_backward's two-pass filter gradient (tcgen05)
  *   hy_block_conv_fwd       blockconv.py:103-121 block_conv (K spill factors) on tcgen05, bf16, lh <= 513
+ *   hy_qkv_feat_gemm        hyena.py:122-126,184 W_qkv projections with _featurize and k * v in the GEMM
+ *                                                epilogue (tcgen05)
  *   hy_li_scan_fwd          fft.py:128-145       fft_conv on an ImplicitFilter bank (core.py:147-151), gated as
  *                           hyena.py:183-186     hyena_forward's LI inner conv, by exact per-mode scans
  *   hy_li_scan_mixer_fwd    hyena.py:162-186     the LI mixer (featurizers + gates + modal scan), fused
@@ -239,6 +241,16 @@ HY_API size_t hy_li_param_grad_workspace_size(int B, int C);
 HY_API int hy_li_param_grad(const void* dc, const void* u, const float* residues, const float* poles, int npoles,
                             int group_size, int B, int C, int L, int dtype, float* d_res, float* d_pole,
                             void* ws, size_t ws_bytes, void* stream);
+
+/* The q/k/v projection GEMM with the featurizers in its epilogue (hyena.py:122-126, the gate
+ * product of hyena.py:184): out (B, 2D, L) = [fq; u],
+ * fq = h_q * (W_q^T x), u = (h_k * (W_k^T x)) (h_v * (W_v^T x)), causal FIRs of lhf <= 8 taps on
+ * the fp32 accumulators. tcgen05 / TMA, bf16 x (B, D, L) and w_perm (3D, D) — [W_q; W_k; W_v]^T
+ * with rows regrouped as D/128 tiles of q rows then D/64 tiles of [64 k rows; the same channels'
+ * 64 v rows] (ops.qkv_weight_permute); feat_taps fp32 (3, D, lhf). D % 128 == 0, L % 256 == 0.
+ * segments: time segments per 128-row tile (0 = chosen for the grid). */
+HY_API int hy_qkv_feat_gemm(const void* w_perm, const void* x, const float* feat_taps, int lhf, void* fq, void* u,
+                            int B, int D, int L, int segments, int dtype, void* stream);
 
 /* K-block causal conv on tcgen05 (blockconv.py:103-121 block_conv; the K + 1 spill factors
  * T_k[m][j] = h[128 k + m - j] as accumulating MMAs over row-shifted views of one U buffer),

@@ -61,6 +61,7 @@ SIGNATURES = {
     "hy_fft_c2c": (_I, [_P, _P, ctypes.c_longlong, ctypes.c_longlong, _I, _I, _P, _SZ, _P]),
     "hy_gate_mul": (_I, [_P, _P, _P, ctypes.c_longlong, _I, _P]),
     "hy_split3_cat": (_I, [_P, _P, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _P]),
+    "hy_qkv_feat_gemm": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _P]),
 }
 
 _lib = None

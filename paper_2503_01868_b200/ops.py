@@ -317,6 +317,41 @@ def gate_mul(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) 
     return out
 
 
+def qkv_weight_permute(w_qkv_t: torch.Tensor) -> torch.Tensor:
+    """Row order of hy_qkv_feat_gemm's weight: the (3D, D) [W_q; W_k; W_v]^T rows regrouped as
+    D/128 tiles of 128 q rows, then D/64 tiles of [64 k rows; the same channels' 64 v rows]."""
+    D = w_qkv_t.shape[1]
+    if w_qkv_t.shape[0] != 3 * D or D % 128:
+        raise ValueError("w_qkv_t must be (3D, D) with D % 128 == 0")
+    kv = torch.stack([w_qkv_t[D:2 * D].reshape(D // 64, 64, D), w_qkv_t[2 * D:].reshape(D // 64, 64, D)], dim=1)
+    return torch.cat([w_qkv_t[:D], kv.reshape(2 * D, D)]).contiguous()
+
+
+def qkv_feat_gemm(x: torch.Tensor, w_perm: torch.Tensor, feat_taps: torch.Tensor, segments: int = 0):
+    """(fq, u), each (B, D, L): the featurizers of W_qkv^T x with u = fk * fv, in one tcgen05 GEMM
+    whose epilogue runs the FIRs (hyena.py:122-126, 184). bf16,
+    D % 128 == 0, L % 256 == 0, featurizers <= 8 taps; w_perm from qkv_weight_permute;
+    segments = time segments per 128-row tile (0: chosen for the grid)."""
+    _check_device(x, w_perm)
+    x3 = _as3(x)
+    B, D, L = x3.shape
+    if x3.dtype != torch.bfloat16 or w_perm.dtype != torch.bfloat16:
+        raise ValueError("qkv_feat_gemm takes bfloat16 activations and weights")
+    if tuple(w_perm.shape) != (3 * D, D):
+        raise ValueError(f"w_perm must be (3D, D) = ({3 * D}, {D})")
+    if feat_taps.dim() != 3 or tuple(feat_taps.shape[:2]) != (3, D):
+        raise ValueError("feat_taps must be (3, D, lhf)")
+    taps = feat_taps.to(device=x3.device, dtype=torch.float32).contiguous()
+    fq = torch.empty_like(x3)
+    u = torch.empty_like(x3)
+    lib = _lib.load()
+    _lib.check(lib.hy_qkv_feat_gemm(w_perm.data_ptr(), x3.data_ptr(), taps.data_ptr(), taps.shape[2], fq.data_ptr(),
+                                    u.data_ptr(), B, D, L, segments, _dtype_code(x3), _stream()), "qkv_feat_gemm")
+    if x.dim() == 2:
+        return fq[0], u[0]
+    return fq, u
+
+
 def _modes(residues: torch.Tensor, poles: torch.Tensor, dev):
     r = residues.to(device=dev, dtype=torch.float32).contiguous()
     p = poles.to(device=dev, dtype=torch.float32).contiguous()

@@ -1,0 +1,104 @@
+"""The projection GEMM with the featurizers in its epilogue (hy_qkv_feat_gemm, SURVEY §8(f)
+rank 2) against a float64 restatement of hyena.py:122-126 + the gate product of hyena.py:184,
+and the operator route that consumes it (HY_QKV_FUSED) against the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2503_01868_b200 as hy
+from paper_2503_01868_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _conv(x, h):
+    return np.convolve(x, h)[: x.shape[-1]]
+
+
+def _case(B, D, L, lhf, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn((B, D, L), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((3 * D, D), device="cuda", generator=g) / np.sqrt(D)).to(torch.bfloat16)
+    taps = torch.randn((3, D, lhf), device="cuda", generator=g) / 2.65
+    return x, w, taps
+
+
+def _want(x, w, taps, b, c):
+    """fq and u of channel c, sequence b, in float64 from the same bf16 inputs."""
+    D = x.shape[1]
+    xb = x[b].double().cpu().numpy()
+    rows = [w[i * D + c].double().cpu().numpy() @ xb for i in range(3)]
+    th = taps.double().cpu().numpy()
+    fq, fk, fv = (_conv(rows[i], th[i, c]) for i in range(3))
+    return fq, fk * fv
+
+
+@pytest.mark.parametrize("segments", [0, 1, 3, 5])
+def test_qkv_feat_gemm_vs_float64(segments):
+    """B = 2, D = 256, L = 1024: every tile kind (q tiles, k|v tiles), units that start
+    mid-sequence (segments 3, 5: the N = 64 halo accumulation) and units that cross a sequence
+    boundary; channels from every tile and both halves of the k|v tiles."""
+    B, D, L = 2, 256, 1024
+    x, w, taps = _case(B, D, L, 7, 1)
+    out = torch.cat(ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), taps, segments=segments), dim=1)
+    assert out.shape == (B, 2 * D, L)
+    for b in range(B):
+        for c in (0, 1, 63, 64, 100, 127, 128, 191, 200, 255):
+            fq, u = _want(x, w, taps, b, c)
+            assert oracle.rel_err(out[b, c].double().cpu().numpy(), fq) < 1e-2, (b, c)
+            assert oracle.rel_err(out[b, D + c].double().cpu().numpy(), u) < 1e-2, (b, c)
+
+
+def test_qkv_feat_gemm_segments_agree():
+    """The halo accumulation (N = 64) reproduces the main tile's columns: every segmentation
+    gives the same result within fp32 accumulation-order noise (bf16 outputs, 1 ulp)."""
+    x, w, taps = _case(1, 384, 4096, 7, 2)
+    wp = ops.qkv_weight_permute(w)
+    ref = torch.cat(ops.qkv_feat_gemm(x, wp, taps, segments=1), dim=1).float()
+    for s in (2, 3, 7, 16):
+        got = torch.cat(ops.qkv_feat_gemm(x, wp, taps, segments=s), dim=1).float()
+        assert torch.allclose(got, ref, rtol=1e-2, atol=1e-3), s
+
+
+@pytest.mark.parametrize("lhf", [1, 3, 8])
+def test_qkv_feat_gemm_filter_lengths(lhf):
+    B, D, L = 1, 128, 512
+    x, w, taps = _case(B, D, L, lhf, 3 + lhf)
+    out = torch.cat(ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), taps, segments=2), dim=1)
+    for c in (0, 77, 127):
+        fq, u = _want(x, w, taps, 0, c)
+        assert oracle.rel_err(out[0, c].double().cpu().numpy(), fq) < 1e-2
+        assert oracle.rel_err(out[0, D + c].double().cpu().numpy(), u) < 1e-2
+
+
+def test_qkv_feat_gemm_c2_size_properties():
+    """C2 size (B = 4, D = 4096, L = 8192): scaling x by 2 scales fq by 2 and u by 4 bitwise
+    (fp32 accumulation and the FIRs scale exactly), causality per 256-column tile, and sampled
+    channels against float64."""
+    B, D, L = 4, 4096, 8192
+    x, w, taps = _case(B, D, L, 7, 4)
+    wp = ops.qkv_weight_permute(w)
+    y = torch.cat(ops.qkv_feat_gemm(x, wp, taps), dim=1)
+    y2 = torch.cat(ops.qkv_feat_gemm(2 * x, wp, taps), dim=1)
+    assert torch.equal(y2[:, :D], 2 * y[:, :D])
+    assert torch.equal(y2[:, D:], 4 * y[:, D:])
+    xp = x.clone()
+    xp[:, :, 5000] += 1.0
+    yp = torch.cat(ops.qkv_feat_gemm(xp, wp, taps), dim=1)
+    assert torch.equal(yp[..., :5000], y[..., :5000])
+    for b, c in ((0, 0), (1, 2047), (3, 4095), (2, 1234)):
+        fq, u = _want(x, w, taps, b, c)
+        assert oracle.rel_err(y[b, c].double().cpu().numpy(), fq) < 1e-2, (b, c)
+        assert oracle.rel_err(y[b, D + c].double().cpu().numpy(), u) < 1e-2, (b, c)
+
+
+def test_qkv_feat_gemm_rejects():
+    x, w, taps = _case(1, 128, 512, 7, 5)
+    with pytest.raises(ValueError):
+        ops.qkv_feat_gemm(x[..., :300].contiguous(), ops.qkv_weight_permute(w), taps)
+    with pytest.raises(NotImplementedError):
+        ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), torch.zeros((3, 128, 9), device="cuda"))
