@@ -208,6 +208,29 @@ class HyenaOperator:
         else:
             self.inner_taps = torch.from_numpy(inner.materialized()).to(self.dev, tdt)
         self._mat_taps = None
+        # the projection GEMM with the featurizers and u = fk * fv in its
+        # epilogue (hy_qkv_feat_gemm), then the gated inner conv reads (fq, u); HY_QKV_FUSED=1
+        # selects it (cuBLAS + the fused mixer stays the default: DESIGN §3.6)
+        self.qkv_fused = os.environ.get("HY_QKV_FUSED", "0") == "1"
+        self._w_perm = None
+
+    def qkv_fused_eligible(self, L: int) -> bool:
+        if self.dtype != torch.bfloat16 or self.cfg.width % 128 or L % 256 or self.lhf > 8:
+            return False
+        return self.li_modes is not None or (self.inner_taps is not None and self.lh <= ops.BLOCK_CONV_MAX_LH)
+
+    def project_featurized(self, x3: torch.Tensor):
+        """(fq, u), each (B, D, L): hyena.py:122-126 and the gate product k * v of :184 in one
+        tcgen05 GEMM whose epilogue runs the featurizer FIRs (bf16)."""
+        if self._w_perm is None:
+            self._w_perm = ops.qkv_weight_permute(self.w_qkv_t)
+        return ops.qkv_feat_gemm(x3, self._w_perm, self.feat_taps)
+
+    def inner_gated(self, u: torch.Tensor, fq: torch.Tensor) -> torch.Tensor:
+        """fq * inner(u) (hyena.py:183-186) on the fused projections."""
+        if self.li_modes is not None:
+            return ops.li_conv(u, self.li_modes[0], self.li_modes[1], self.gs, q=fq)
+        return ops.block_conv(u, self.inner_taps, self.gs, q=fq, decay=self.decay)
 
     @property
     def materialized_inner(self) -> torch.Tensor:
@@ -270,10 +293,16 @@ class HyenaOperator:
                 f"LI inner filter length {self.lh} must equal the sequence length {x3.shape[2]}")
         if x3.dtype != self.dtype:
             raise ValueError(f"operator packed for {self.dtype}, got {x3.dtype}")
-        proj = self.project(x3)
-        if events is not None:
-            events[0].record()
-        mixed = self.mixer(proj)
+        if self.qkv_fused and self.qkv_fused_eligible(x3.shape[2]):
+            fq, u = self.project_featurized(x3)
+            if events is not None:
+                events[0].record()
+            mixed = self.inner_gated(u, fq)
+        else:
+            proj = self.project(x3)
+            if events is not None:
+                events[0].record()
+            mixed = self.mixer(proj)
         if events is not None:
             events[1].record()
         acc = None

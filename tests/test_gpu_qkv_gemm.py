@@ -102,3 +102,66 @@ def test_qkv_feat_gemm_rejects():
         ops.qkv_feat_gemm(x[..., :300].contiguous(), ops.qkv_weight_permute(w), taps)
     with pytest.raises(NotImplementedError):
         ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), torch.zeros((3, 128, 9), device="cuda"))
+
+
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).double().numpy()
+
+
+def _rounded_cfg(variant, D, L, seed, **kw):
+    cfg = hy.make_hyena_config(variant, D, hy.make_rng(seed), seq_len=L, **kw)
+    rnd = {n: _bf16(getattr(cfg, n)) for n in ("w_q", "w_k", "w_v", "w_out")}
+
+    def rbank(g):
+        fs = []
+        for f in g.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fs.append(hy.ExplicitFilter(_bf16(f.taps)))
+            elif isinstance(f, hy.RegularizedFilter):
+                fs.append(hy.RegularizedFilter(_bf16(f.taps_hat), f.decay_rate, f.base))
+            else:
+                fs.append(f)
+        return hy.GroupSpec(g.channels, g.group_size, tuple(fs))
+    return hy.HyenaConfig(**{**cfg.__dict__, **rnd, **{n: rbank(getattr(cfg, n))
+                                                      for n in ("q_feat", "k_feat", "v_feat", "inner")}})
+
+
+def _oracle_cfg(cfg):
+    ocfg = {"variant": cfg.variant, "width": cfg.width, "block_size": cfg.block_size, "backend": cfg.backend,
+            **{n: getattr(cfg, n) for n in ("w_q", "w_k", "w_v", "w_out")}}
+    for n in ("q_feat", "k_feat", "v_feat", "inner"):
+        g = getattr(cfg, n)
+        fs = []
+        for f in g.filters:
+            if isinstance(f, hy.ExplicitFilter):
+                fs.append(("explicit", f.taps))
+            elif isinstance(f, hy.RegularizedFilter):
+                fs.append(("regularized", f.taps_hat, f.decay_rate, f.base))
+            else:
+                fs.append(("implicit", f.residues, f.poles, f.length))
+        ocfg[n] = {"channels": g.channels, "group_size": g.group_size, "filters": fs}
+    return ocfg
+
+
+@pytest.mark.parametrize("variant,B,D,L,kw", [
+    ("MR", 2, 256, 2048, {"inner_len": 128, "block_size": 128}),
+    ("MR", 1, 256, 1024, {"inner_len": 300, "block_size": 128, "group_size": 4}),
+    ("SE", 1, 128, 1024, {}),
+    ("LI", 1, 128, 4096, {"backend": "fft"}),
+])
+def test_operator_fused_projection_vs_oracle(variant, B, D, L, kw):
+    """HyenaOperator with the fused projection route (qkv_fused: hy_qkv_feat_gemm, then the
+    K-block / implicit conv gated by fq) against the fp64 oracle, and against the default route."""
+    cfg = _rounded_cfg(variant, D, L, 3, **kw)
+    x = _bf16(np.stack([hy.make_rng(4, stream=b).standard_normal((D, L)) for b in range(B)]))
+    op = hy.HyenaOperator(cfg, torch.bfloat16)
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    base = op.forward(xt).float().cpu().numpy()
+    op.qkv_fused = True
+    assert op.qkv_fused_eligible(L)
+    y = op.forward(xt).float().cpu().numpy()
+    ocfg = _oracle_cfg(cfg)
+    for b in range(B):
+        want = oracle.hyena_forward(x[b], ocfg)
+        assert oracle.rel_err(y[b], want) < 1e-2, b
+        assert oracle.rel_err(y[b], base[b]) < 1e-2, b
