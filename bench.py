@@ -40,6 +40,12 @@ WORKLOADS = {
     # sequence of N x 8192 tokens (weak scaling, 144-step p2p history between ranks)
     "mr": dict(kind="op", variant="MR", B=4, L=8192, D=4096, inner_len=128, block_size=128, dtype="bf16",
                desc="Hyena-MR operator fwd (filter len 128, blocked T0/T1), B=4, L=8192, D=4096, bf16"),
+    # the C2 operator through the fused projection route (hand-written tcgen05
+    # W_qkv GEMM with the featurizers and k * v in its epilogue, then the inner conv gated by fq)
+    "mr_fused": dict(kind="op", variant="MR", B=4, L=8192, D=4096, inner_len=128, block_size=128, dtype="bf16",
+                     qkv_fused=True,
+                     desc="Hyena-MR operator fwd, fused projection route (featurizers in the W_qkv GEMM "
+                          "epilogue), B=4, L=8192, D=4096, bf16"),
     "se": dict(kind="op", variant="SE", B=1, L=4096, D=4096, inner_len=7, block_size=16, dtype="f32",
                desc="Hyena-SE operator fwd (filter len 7), B=1, L=4096, D=4096, fp32"),
     "li": dict(kind="op", variant="LI", B=1, L=131072, D=4096, inner_len=None, block_size=128, dtype="bf16",
@@ -308,7 +314,36 @@ class Runner:
         B, D, L = wl["B"], wl["D"], wl["L"]
         kind = wl["kind"]
         self.kernels = []  # (label, variant, algorithmic bytes per launch)
-        if kind == "op" and ws == 1:
+        if kind == "op" and ws == 1 and wl.get("qkv_fused"):
+            op = hy.HyenaOperator(build_config(wl), dt)
+            op.qkv_fused = True
+            if not op.qkv_fused_eligible(L):
+                raise SystemExit("fused projection route not eligible for this workload")
+            self.m = L
+
+            def fused(x, ev=None):
+                if ev is not None:
+                    ev[0][0].record()
+                fq, u = op.project_featurized(x)
+                if ev is not None:
+                    ev[0][1].record()
+                    ev[1][0].record()
+                mixed = op.inner_gated(u, fq)
+                if ev is not None:
+                    ev[1][1].record()
+                return op.out_project(mixed)
+
+            self.fwd = fused
+            n = B * D * L
+            self.kernels = [
+                dict(label="QKV", kernel="qkv_feat_gemm_kernel<2> (hy_qkv_feat_gemm: tcgen05 cta_group::2 W_qkv GEMM, "
+                     "featurizer FIRs and k * v in the epilogue)", bound="tensor_bf16", work=6 * D * n,
+                     unit="TFLOP/s"),
+                dict(label="MR inner", kernel="two_stage_kernel (hy_two_stage_fwd: tcgen05 T0/T1 conv of u gated by "
+                     "fq; 2 rows in, 1 out)", bound="hbm", work=3 * self.esize * n, unit="GB/s")]
+            self.parallelism = "single"
+            self.l_global = L
+        elif kind == "op" and ws == 1:
             op = hy.HyenaOperator(build_config(wl), dt)
             self.m = L
             self.fwd = lambda x, ev=None: op.forward(x, events=None if ev is None else ev[0])
@@ -395,12 +430,16 @@ def kernel_info(run, kern_ms, peaks, wl, ws) -> list:
             if kd["bound"] == "hbm":
                 ach, peak = kd["work"] / (ms * 1e-3) / 1e9, peaks["hbm_gbs"]
                 extra = {"algorithmic_bytes_per_launch": kd["work"]}
+            elif kd["bound"] == "tensor_bf16":
+                ach, peak = kd["work"] / (ms * 1e-3) / 1e12, peaks["bf16_tflops"]
+                extra = {"algorithmic_flops_per_launch": kd["work"], "peak_source_note": "measured cuBLAS bf16 burst"}
             else:
                 ach = kd["work"] / (ms * 1e-3) / 1e12
                 peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
                 extra = {"algorithmic_flops_per_launch": kd["work"],
                          "peak_source_note": "derived FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 x sm_max_mhz"}
-            kinfo.append({"kernel": kd["kernel"], "label": kd["label"], "bound": kd["bound"], "achieved": ach,
+            kinfo.append({"kernel": kd["kernel"], "label": kd["label"], "bound": kd["bound"].split("_")[0],
+                          "achieved": ach,
                           "peak": peak, "unit": kd["unit"], "frac": ach / peak, **extra, "launch_ms": ms})
             continue
         label, variant, nbytes = kd
@@ -416,7 +455,7 @@ def kernel_info(run, kern_ms, peaks, wl, ws) -> list:
 # The other BASELINE configs, measured device-side in the same run as the headline line (the
 # driver runs only the default workload): N = 1 -> C1, C3 (bf16 and the reference's fp32), C4 and
 # C5's single-GPU operator at L = 1M; N > 1 -> the C5 context-parallel LI layer at L = 1M.
-EXTRA_N1 = ("se", "li", "li_f32", "stripe", "li_cp")
+EXTRA_N1 = ("se", "li", "li_f32", "stripe", "li_cp", "mr_fused")
 EXTRA_NN = ("li_cp",)
 
 
@@ -468,6 +507,8 @@ def measure_extra(names, args, ws, rank, local) -> dict:
                          "scaling": "strong" if wl["kind"] == "cp" else "weak", "parallelism": run.parallelism,
                          "roofline": None if dom is None else {k: dom[k] for k in ("kernel", "label", "bound", "achieved",
                                                                                    "peak", "unit", "frac", "launch_ms")},
+                         "roofline_kernels": [{k: d[k] for k in ("label", "bound", "achieved", "unit", "frac",
+                                                                 "launch_ms")} for d in kinfo] if len(kinfo) > 1 else None,
                          "roofline_operator_frac": operator_roofline(run.op_flops / ws / (ms * 1e-3) / 1e12, peaks,
                                                                      wl["dtype"], run.op_flops // ws)["frac"],
                          "clocks": clocks}
