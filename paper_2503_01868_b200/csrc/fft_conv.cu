@@ -34,6 +34,12 @@ constexpr int MAX_N2 = 4096;   // row transform length (shared memory: 32 KB dat
 constexpr int MAX_N1 = 512;    // column transform length
 constexpr int COL_POINTS = 8192;  // points per column-pass CTA: N1 x CC columns (64 KB)
 constexpr int ROW_BLOCK = 256; // channels per block (spectra + transforms held in the workspace)
+// channels per launch of the fast path (HY_FFT_ROW_BLOCK overrides; probe)
+inline int fast_row_block() {
+  const char* e = getenv("HY_FFT_ROW_BLOCK");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 && v <= ROW_BLOCK ? v : ROW_BLOCK;
+}
 constexpr int THREADS = 256;
 
 struct Plan {
@@ -327,7 +333,7 @@ int run(const void* q, const void* k, const void* v, void* y, const float* taps,
   float2* X = reinterpret_cast<float2*>(base + ly.x);
   if (fft_fast_supported(pl.N) && !getenv("HY_FFT_RADIX4")) {
     const int dt = sizeof(T) == 4 ? HY_F32 : HY_BF16;
-    return fft_fast_run(q, k, v, y, taps, B, C, L, lh, gs, dt, pl.N, ROW_BLOCK, tw, Hf, X, st);
+    return fft_fast_run(q, k, v, y, taps, B, C, L, lh, gs, dt, pl.N, fast_row_block(), tw, Hf, X, st);
   }
   twiddle_kernel<<<(pl.N + 255) / 256, 256, 0, st>>>(tw, pl.N);
   // widest column block that fits: N1 x COLS <= 8192 points, COLS <= N2
@@ -410,6 +416,6 @@ extern "C" HY_API int hy_fft_conv_spec_fwd(const void* q, const void* k, const v
   const fft::Layout ly = fft::ws_layout(pl, C, gs);
   if (!ws || ws_bytes < ly.total) return fail(HY_ERR_INVALID, "workspace %zu bytes, need %zu", ws_bytes, ly.total);
   unsigned char* base = static_cast<unsigned char*>(ws);
-  return fft_fast_conv_spec(q, k, v, y, spec, B, C, L, gs, dtype, pl.N, fft::ROW_BLOCK, base + ly.tw, base + ly.x,
+  return fft_fast_conv_spec(q, k, v, y, spec, B, C, L, gs, dtype, pl.N, fft::fast_row_block(), base + ly.tw, base + ly.x,
                             stream);
 }
