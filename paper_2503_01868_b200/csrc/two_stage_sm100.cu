@@ -171,6 +171,16 @@ __device__ __forceinline__ size_t elem_off(const Params& p, int row, int t) {
 // Optional timeline trace (debug/tuning): CTA 0 records clock64 per tile and event.
 constexpr int TRACE_TILES = 256, TRACE_EV = 24;
 __device__ unsigned long long g_trace[TRACE_TILES * TRACE_EV];
+// per-CTA start / end (globaltimer, ns) of a traced launch: load balance across SMs
+constexpr int TRACE_CTAS = 256;
+__device__ unsigned long long g_cta_times[2 * TRACE_CTAS];
+__device__ __forceinline__ void trace_cta(const Params& p, int which) {
+  if (p.trace && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_cta_times[2 * blockIdx.x + which] = t;
+  }
+}
 __device__ __forceinline__ void trace(const Params& p, int it, int ev) {
   if (p.trace && blockIdx.x == 0 && it < TRACE_TILES) g_trace[it * TRACE_EV + ev] = clock64();
 }
@@ -277,6 +287,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
   bf16* hpad = reinterpret_cast<bf16*>(smem + LY::OFF_HP);  // hpad[i + 128] = h[i], i in [-128, 384)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  trace_cta(p, 0);
   // IMPL carries the recurrence state from tile to tile, so a CTA owns whole sequences
   const int units = IMPL ? p.total_tiles / p.tiles_per_seq : p.total_tiles;
   const int per = IMPL ? p.tiles_per_seq : 1;
@@ -891,6 +902,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
   __syncthreads();
   tc_fence_after();
   if (warp == W_MMA) tmem_dealloc<512>(tmem_base);
+  trace_cta(p, 1);
 }
 
 template <bool FEAT, bool GK, bool GQ, int KS, bool IMPL = false>
@@ -1093,10 +1105,13 @@ extern "C" HY_API int hy_li_conv_segmented_fwd(const void* v, void* y, const flo
   return ts::launch<false, false, false, true>(p, static_cast<cudaStream_t>(stream));
 }
 
-// Debug: copy the CTA-0 timeline of the last traced two-stage launch (HY_TS_TRACE=1).
+// Debug: copy the CTA-0 timeline of the last traced two-stage launch (HY_TS_TRACE=1); with
+// n >= TRACE_TILES * TRACE_EV + 2 * TRACE_CTAS also every CTA's start / end globaltimer.
 extern "C" HY_API int hy_debug_two_stage_trace(unsigned long long* host_out, int n) {
-  if (n > ts::TRACE_TILES * ts::TRACE_EV) n = ts::TRACE_TILES * ts::TRACE_EV;
-  cudaError_t e = cudaMemcpyFromSymbol(host_out, ts::g_trace, n * sizeof(unsigned long long));
+  const int nt = ts::TRACE_TILES * ts::TRACE_EV;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, ts::g_trace, (n < nt ? n : nt) * sizeof(unsigned long long));
+  if (e == cudaSuccess && n >= nt + 2 * ts::TRACE_CTAS)
+    e = cudaMemcpyFromSymbol(host_out + nt, ts::g_cta_times, 2 * ts::TRACE_CTAS * sizeof(unsigned long long));
   return e == cudaSuccess ? HY_OK : fail(HY_ERR_CUDA, "trace copy: %s", cudaGetErrorString(e));
 }
 

@@ -10,7 +10,7 @@ os.environ["HY_TS_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_01868_b200 import _lib, ops  # noqa: E402
 
-D, L = 4096, 131072
+D, L = 4096, int(os.environ.get("TRACE_L", 131072))
 g = torch.Generator(device="cuda").manual_seed(0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "conv"
 res = torch.randn((D, 8), device="cuda", generator=g) / 8
