@@ -154,6 +154,7 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
   using A = typename Cfg<T>::A;
   constexpr int S = Cfg<T>::S;
   constexpr int TILE = THREADS * S;
+  constexpr bool PAIR = sizeof(A) == 4;  // fp32 states: FIRs and recurrences as packed FFMA2
   __shared__ A s_lam[MAXP], s_r[MAXP];
   __shared__ A s_pk[MAXP][5];           // lam^(S 2^k): the scan multipliers
   __shared__ A s_pl[MAXP][32];          // lam^(S l): a lane's offset in its warp
@@ -199,13 +200,30 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
     for (int t0 = 0; t0 < L; t0 += TILE) {
       const int ts = t0 + threadIdx.x * S;
       const int nv = max(0, min(S, L - ts));
+      if (VEC && threadIdx.x < 3 && t0 + TILE < L) {
+        // the next tile's rows into L2 while this one computes (the loads below are
+        // latency-bound at 16 warps per SM; no registers or shared memory are spent on it)
+        const T* pr = FEAT ? (threadIdx.x == 0 ? rq : threadIdx.x == 1 ? rk : rv)
+                           : (threadIdx.x == 0 ? q : threadIdx.x == 1 ? k : v);
+        if (pr != nullptr) {
+          if (!FEAT) pr += base;
+          const int n = min(TILE, L - t0 - TILE);
+          const unsigned bytes = static_cast<unsigned>(n * sizeof(T)) & ~15u;
+          if (bytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + t0 + TILE), "r"(bytes) : "memory");
+        }
+      }
       A u[S], yv[S];
+      auto fir = [&](const A* r, const A* h, A* o) {
+        if constexpr (PAIR) fir8_pairs<S>(r, h, o);
+        else fir8<A, S>(r, h, o);
+      };
       if constexpr (FEAT) {
         A raw[S + 8], fk[S];
         load_halo_seg<T, S, VEC>(rv, ts, L, raw);
-        fir8<A, S>(raw, fh[2], u);
+        fir(raw, fh[2], u);
         load_halo_seg<T, S, VEC>(rk, ts, L, raw);
-        fir8<A, S>(raw, fh[1], fk);
+        fir(raw, fh[1], fk);
 #pragma unroll
         for (int j = 0; j < S; ++j) u[j] *= fk[j];
       } else {
@@ -219,18 +237,35 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
       }
 #pragma unroll
       for (int j = 0; j < S; ++j) yv[j] = A(0);
+      float2 uu[PAIR ? S : 1];  // (u, u): the packed FFMA2 addend, built once per tile
+      if constexpr (PAIR) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) uu[j] = make_float2(u[j], u[j]);
+      }
       for (int b = 0; b < nb; ++b, ++it) {
         const int buf = it & 1;
         A lam[MB], st[MB];
 #pragma unroll
         for (int n = 0; n < MB; ++n) lam[n] = s_lam[b * MB + n];
         // 1. segment end state from zero
+        if constexpr (PAIR) {
 #pragma unroll
-        for (int n = 0; n < MB; ++n) {
-          A s = A(0);
+          for (int n = 0; n < MB; n += 2) {
+            const float2 l2 = make_float2(lam[n], lam[n + 1]);
+            float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < S; ++j) s = fma(lam[n], s, u[j]);
-          st[n] = s;
+            for (int j = 0; j < S; ++j) s2 = __ffma2_rn(l2, s2, uu[j]);
+            st[n] = s2.x;
+            st[n + 1] = s2.y;
+          }
+        } else {
+#pragma unroll
+          for (int n = 0; n < MB; ++n) {
+            A s = A(0);
+#pragma unroll
+            for (int j = 0; j < S; ++j) s = fma(lam[n], s, u[j]);
+            st[n] = s;
+          }
         }
         // 2. inclusive scan over the warp's lanes
 #pragma unroll
@@ -270,21 +305,40 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
           for (int w = 0; w < WARPS; ++w) acc += s_pw[p][WARPS - 1 - w] * static_cast<double>(s_tot[buf][w][lane]);
           s_carry[p] = acc;
         }
+        if constexpr (PAIR) {
+          float2 y2[S];
 #pragma unroll
-        for (int n = 0; n < MB; ++n) {
-          const A r = s_r[b * MB + n];
-          A s = st[n];
+          for (int j = 0; j < S; ++j) y2[j] = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < S; ++j) {
-            s = fma(lam[n], s, u[j]);
-            yv[j] = fma(r, s, yv[j]);
+          for (int n = 0; n < MB; n += 2) {
+            const float2 l2 = make_float2(lam[n], lam[n + 1]);
+            const float2 r2 = make_float2(s_r[b * MB + n], s_r[b * MB + n + 1]);
+            float2 s2 = make_float2(st[n], st[n + 1]);
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+              s2 = __ffma2_rn(l2, s2, uu[j]);
+              y2[j] = __ffma2_rn(r2, s2, y2[j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < S; ++j) yv[j] += y2[j].x + y2[j].y;
+        } else {
+#pragma unroll
+          for (int n = 0; n < MB; ++n) {
+            const A r = s_r[b * MB + n];
+            A s = st[n];
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+              s = fma(lam[n], s, u[j]);
+              yv[j] = fma(r, s, yv[j]);
+            }
           }
         }
       }
       if constexpr (FEAT) {
         A raw[S + 8], fq[S];
         load_halo_seg<T, S, VEC>(rq, ts, L, raw);
-        fir8<A, S>(raw, fh[0], fq);
+        fir(raw, fh[0], fq);
 #pragma unroll
         for (int j = 0; j < S; ++j) yv[j] *= fq[j];
       } else if (q != nullptr) {
