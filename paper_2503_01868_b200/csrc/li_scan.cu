@@ -30,6 +30,10 @@ namespace lis {
 
 constexpr int WARPS = 8, THREADS = WARPS * 32;
 constexpr int MB = 8;     // modes per register block
+#ifndef HY_LIS_LA
+#define HY_LIS_LA 1
+#endif
+constexpr int LA = HY_LIS_LA;  // one-shot kernel: tiles prefetched into L2 ahead of the loads
 constexpr int MAXP = 64;  // poles per group
 
 template <typename T> struct Cfg;
@@ -200,17 +204,20 @@ li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __rest
     for (int t0 = 0; t0 < L; t0 += TILE) {
       const int ts = t0 + threadIdx.x * S;
       const int nv = max(0, min(S, L - ts));
-      if (VEC && threadIdx.x < 3 && t0 + TILE < L) {
-        // the next tile's rows into L2 while this one computes (the loads below are
+      if (VEC && threadIdx.x < 3) {
+        // the rows LA tiles ahead into L2 while this one computes (the loads below are
         // latency-bound at 16 warps per SM; no registers or shared memory are spent on it)
         const T* pr = FEAT ? (threadIdx.x == 0 ? rq : threadIdx.x == 1 ? rk : rv)
                            : (threadIdx.x == 0 ? q : threadIdx.x == 1 ? k : v);
         if (pr != nullptr) {
           if (!FEAT) pr += base;
-          const int n = min(TILE, L - t0 - TILE);
-          const unsigned bytes = static_cast<unsigned>(n * sizeof(T)) & ~15u;
-          if (bytes)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + t0 + TILE), "r"(bytes) : "memory");
+          for (int a = t0 == 0 ? 1 : LA; a <= LA; ++a) {
+            const int tn = t0 + a * TILE;
+            const int n = min(TILE, L - tn);
+            const unsigned bytes = n > 0 ? static_cast<unsigned>(n * sizeof(T)) & ~15u : 0u;
+            if (bytes)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + tn), "r"(bytes) : "memory");
+          }
         }
       }
       A u[S], yv[S];
