@@ -577,7 +577,10 @@ def run_ours(args, wl):
     xh = torch.empty(tuple(run.x.shape), dtype=run.dt, pin_memory=True)
     xh.copy_(run.x.cpu())
     yh = torch.empty(tuple(run.x.shape), dtype=run.dt, pin_memory=True)
-    pipe = HostPipeline(run.fwd, tuple(run.x.shape), run.dt)
+    # whole steps through the pipeline (HY_E2E_CHUNKS=B streams a step's batch as per-sequence
+    # chunks: measured no better on average and far noisier at C2, 2.9-5.8 M tokens/s)
+    nch = int(os.environ.get("HY_E2E_CHUNKS", 1))
+    pipe = HostPipeline(run.fwd, tuple(run.x.shape), run.dt, chunks=nch)
     pipe.run(xh, yh, max(2, args.warmup))
     torch.cuda.synchronize()
     if dist.is_initialized():
@@ -619,7 +622,8 @@ def run_ours(args, wl):
                          "host input, forward, backward, D2H of dx (copies of neighbouring steps overlap)")
                 if wl["kind"] == "train" else
                         "streaming.HostPipeline over the public forward: per step H2D of its pinned host "
-                        "input, forward, D2H of its result (copies of neighbouring steps overlap the forward)"},
+                        "input, forward, D2H of its result (copies of neighbouring steps overlap the forward)"
+                        + (f"; each step's batch streamed as {nch} per-sequence chunks" if nch > 1 else "")},
         "roofline": dom,
         "roofline_kernels": kinfo,
         "roofline_operator": operator_roofline(op_tf, peaks, wl["dtype"], run.op_flops // ws),

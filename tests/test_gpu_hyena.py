@@ -146,11 +146,14 @@ def test_host_pipeline_matches_forward():
     g = torch.Generator().manual_seed(5)
     xs = [torch.randn((2, 64, 4096), generator=g).to(torch.bfloat16).pin_memory() for _ in range(3)]
     ys = [torch.empty_like(x).pin_memory() for x in xs]
-    pipe = HostPipeline(op.forward, tuple(xs[0].shape), torch.bfloat16)
-    pipe.run(xs, ys, 3)
-    torch.cuda.synchronize()
-    for x, y in zip(xs, ys):
-        assert torch.equal(y, op.forward(x.cuda()).cpu())
+    for chunks in (1, 2):
+        pipe = HostPipeline(op.forward, tuple(xs[0].shape), torch.bfloat16, chunks=chunks)
+        for y in ys:
+            y.zero_()
+        pipe.run(xs, ys, 3)
+        torch.cuda.synchronize()
+        for x, y in zip(xs, ys):
+            assert torch.equal(y, op.forward(x.cuda()).cpu()), chunks
 
 
 def test_se_operator_fp32_full_width_parity():
