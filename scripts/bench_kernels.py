@@ -152,6 +152,26 @@ def main():
             ms = timeit(lambda: ops.block_conv(v, taps, 16))
             report(f"block_conv_tcgen05_lh{lh}_gs16", ms, 4 * D * B * L, B=B, D=D, L=L, lh=lh, gs=16)
         del v, q
+    if args.which in ("all", "qkv"):
+        # projection GEMM with the featurizers in its epilogue (tcgen05 CTA pairs) vs cuBLAS on the
+        # same W_qkv GEMM, C2 shapes; tensor-bound: reported as TFLOP/s against the measured peak
+        B, D, L = 4, 4096, 8192
+        x = torch.randn((B, D, L), device=dev, dtype=torch.bfloat16, generator=g)
+        w = (torch.randn((3 * D, D), device=dev, generator=g) / 64).to(torch.bfloat16)
+        feat = torch.randn((3, D, 7), device=dev, generator=g) / 3
+        wp = ops.qkv_weight_permute(w)
+        flops = 2.0 * 3 * D * D * B * L
+        try:
+            peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+        except OSError:
+            peak = 1648.3
+        for name, fn in (("qkv_feat_gemm", lambda: ops.qkv_feat_gemm(x, wp, feat)),
+                         ("cublas_w_qkv_gemm", lambda: torch.matmul(w, x))):
+            ms = timeit(fn, iters=10)
+            tf = flops / (ms * 1e-3) / 1e12
+            print(json.dumps({"kernel": name, "ms": round(ms, 4), "TFLOP/s": round(tf, 1),
+                              "frac_bf16_peak": round(tf / peak, 3), "B": B, "D": D, "L": L}), flush=True)
+        del x, w, wp
     if args.which in ("all", "fft"):
         D = 4096
         for L, dt in ((131072, torch.bfloat16), (16384, torch.float32)):
@@ -163,6 +183,15 @@ def main():
                 ms = timeit(lambda: ops.fft_conv(v, taps, 1, q=v, k=v), iters=3, warmup=1)
                 os.environ.pop("HY_FFT_RADIX4", None)
                 report("fft_conv_" + path, ms, 4 * D * L * v.element_size(), D=D, L=L, dtype=str(dt))
+            # cached filter spectra (the operator's path): compute-bound, so also as FP32 TFLOP/s of
+            # the two N-point transforms per channel (5 N log2 N each)
+            spec = ops.fft_spectrum(taps, L)
+            ms = timeit(lambda: ops.fft_conv(v, taps, 1, q=v, k=v, spectrum=spec), iters=3, warmup=1)
+            n = 2 * L
+            tf = 2 * 5 * n * (n.bit_length() - 1) * D / (ms * 1e-3) / 1e12
+            report("fft_conv_spectrum", ms, 4 * D * L * v.element_size(), D=D, L=L, dtype=str(dt),
+                   fp32_tflops=round(tf, 1))
+            del spec
             del v, taps
 
 
