@@ -440,6 +440,9 @@ extern "C" HY_API int hy_qkv_feat_gemm(const void* w_perm, const void* x, const 
     return fail(HY_ERR_INVALID, "hy_qkv_feat_gemm needs D %% 128 == 0 and L %% 256 == 0 (D=%d, L=%d)", D, L);
   if (lhf < 1 || lhf > qg::NTAP) return fail(HY_ERR_UNSUPPORTED, "featurizer length %d > %d", lhf, qg::NTAP);
   if (segments < 0) return fail(HY_ERR_INVALID, "segments must be >= 0");
+  if ((reinterpret_cast<uintptr_t>(w_perm) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(fq) |
+       reinterpret_cast<uintptr_t>(u)) & 15)
+    return fail(HY_ERR_INVALID, "hy_qkv_feat_gemm needs 16-byte aligned w_perm, x, fq and u");
   qg::Params p{};
   p.taps = feat_taps;
   p.fq = static_cast<__nv_bfloat16*>(fq);

@@ -102,6 +102,14 @@ def test_qkv_feat_gemm_rejects():
         ops.qkv_feat_gemm(x[..., :300].contiguous(), ops.qkv_weight_permute(w), taps)
     with pytest.raises(NotImplementedError):
         ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), torch.zeros((3, 128, 9), device="cuda"))
+    # the C-ABI checks TMA / vector-store alignment of its raw pointers
+    from paper_2503_01868_b200 import _lib
+    buf = torch.empty(2 * 128 * 512 + 8, device="cuda", dtype=torch.bfloat16)
+    wp = ops.qkv_weight_permute(w)
+    taps32 = taps.float().contiguous()
+    st = _lib.load().hy_qkv_feat_gemm(wp.data_ptr(), x.data_ptr(), taps32.data_ptr(), 7, buf.data_ptr() + 2,
+                                      buf.data_ptr() + 2 + 128 * 512 * 2, 1, 128, 512, 0, _lib.HY_BF16, 0)
+    assert st == _lib.HY_ERR_INVALID
 
 
 def _bf16(a):
