@@ -829,6 +829,12 @@ def run_reference(args, wl):
 
 
 def main():
+    # the contract is ONE JSON line on stdout: keep a private handle on the real stdout and point
+    # fd 1 at stderr, so whatever the libraries print during the run (NCCL's version banner under
+    # NCCL_DEBUG=WARN / VERSION, cuBLAS or driver notices) cannot interleave with it
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -858,7 +864,8 @@ def main():
                                    "device stores in bf16 rounded to bf16" if err is not None else
                                    "no oracle for this workload's composition (parity in tests/)"}
     if rank == 0 and res is not None:
-        print(json.dumps(res), flush=True)
+        out.write(json.dumps(res) + "\n")
+        out.flush()
 
 
 if __name__ == "__main__":
