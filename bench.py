@@ -298,6 +298,18 @@ def _max_over_ranks(ms: float, ws: int) -> float:
     return float(t.item())
 
 
+def _per_rank(ms: float, ws: int) -> list:
+    """Every rank's value (rank order), so a straggler GPU is visible in the line."""
+    import torch
+    import torch.distributed as dist
+    if ws == 1:
+        return [ms]
+    t = torch.zeros(ws, device="cuda")
+    t[dist.get_rank()] = ms
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
 class Runner:
     """One workload on this rank: device-resident input, a step with kernel events, the
     public-API forward used for e2e, and the accounting the JSON line needs."""
@@ -566,6 +578,7 @@ def run_ours(args, wl):
         parity_io = (run.x[0].double().cpu().numpy(), y[0].double().cpu().numpy())
         del y
     ms_step = _max_over_ranks(t0.elapsed_time(t1), ws) / args.steps
+    rank_ms = [v / args.steps for v in _per_rank(t0.elapsed_time(t1), ws)]
     kern_ms = [statistics.mean(evs[i][j][0].elapsed_time(evs[i][j][1]) for i in range(args.steps))
                for j in range(nk)]
     if dist.is_initialized():
@@ -631,6 +644,7 @@ def run_ours(args, wl):
                       "rest (cuBLAS GEMMs, comm, elementwise)": ms_step - sum(kern_ms)},
         "clocks": clocks,
         "gpu_launches": launches,
+        "ms_per_step_per_rank": rank_ms if ws > 1 else None,
     }
     if not args.no_extra_configs and args.workload == "mr":
         del run, pipe, xh, yh
