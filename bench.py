@@ -502,6 +502,9 @@ def measure_extra(names, args, ws, rank, local) -> dict:
             stream = torch.cuda.current_stream()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            if dist.is_initialized():  # after the sampler start-up, whose latency differs per rank
+                dist.barrier()
+                torch.cuda.synchronize()
             sampler.region(True)
             t0.record(stream)
             for i in range(steps):
@@ -560,6 +563,12 @@ def run_ours(args, wl):
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # the barrier goes after the clock sampler's start-up, whose latency differs per rank: with it
+    # before, a late rank's halo arrived late at its successor, whose timed region then included
+    # the skew (an N = 4 straggler of up to +3.8 ms per step in 10 steps)
+    if dist.is_initialized():
+        dist.barrier()
+        torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     sampler.region(True)
     t0.record(stream)
