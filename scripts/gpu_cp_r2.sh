@@ -5,5 +5,5 @@ nvidia-smi -L
 timeout 1200 python -m pytest tests/test_gpu_cp.py -q -rs > gpurun_out/pytest_cp_multi.log 2>&1
 echo "cp tests rc=$?"; tail -5 gpurun_out/pytest_cp_multi.log
 for W in li_cp mr; do
-  W=$W STEPS=${STEPS:-5} bash scripts/gpu_cp_scale.sh
+  W=$W STEPS=${STEPS:-10} bash scripts/gpu_cp_scale.sh
 done
