@@ -841,10 +841,14 @@ def run_reference(args, wl):
         "impl": "reference",
         "metric": wl.get("metric", "Hyena-SE/MR/LI fwd tokens/s at D=4096 (% HBM/TC roofline); CP scaling 1-8 GPU"),
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
+        "scaling": "strong" if wl["kind"] == "cp" else "weak",
         "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "f32" else "f64",
         "data": "synthetic N(0,1) inputs, random-init weights (make_hyena_config seed 0)",
-        "config": {"workload": wl["desc"], "global_batch": wl["B"], "seq_len": wl["L"], "width": wl["D"]},
+        # the same config as our arm at this N (the op workloads run weak-scaled CP at N > 1)
+        "config": {"workload": wl["desc"], "global_batch": wl["B"],
+                   "seq_len": wl["L"] * (ws if wl["kind"] == "op" else 1), "width": wl["D"],
+                   "parallelism": "host CPU (rank 0 only; other ranks exit without work)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": sample, "host": host_info()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
