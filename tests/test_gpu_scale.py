@@ -195,7 +195,8 @@ def test_mr_operator_full_width(gs):
     assert err < BF16_TOL, err
 
 
-@pytest.mark.parametrize("case", ["mr_mixer", "li_mixer", "two_stage", "li_conv", "block_conv", "taps_grad"])
+@pytest.mark.parametrize("case", ["mr_mixer", "li_mixer", "two_stage", "li_conv", "block_conv", "taps_grad",
+                                  "qkv_gemm"])
 def test_pipelines_bitwise_repeatable(case):
     """Order / race check of the mbarrier pipelines (compute-sanitizer racecheck / synccheck is
     closed on the GPU pool): each warp-specialised tcgen05 kernel runs 12 times at a multi-group
@@ -228,6 +229,12 @@ def test_pipelines_bitwise_repeatable(case):
         v, q, k = (torch.randn((2, C, L), device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
         taps = torch.randn((C, 385), device="cuda", generator=g) / 20
         run = lambda: ops.block_conv(v, taps, 1, q=q, k=k)  # noqa: E731
+    elif case == "qkv_gemm":  # CTA-pair GEMM: 12 pair tiles x 6 time segments, halo passes included
+        x = torch.randn((2, C, L), device="cuda", generator=g).to(torch.bfloat16)
+        w = (torch.randn((3 * C, C), device="cuda", generator=g) / 32).to(torch.bfloat16)
+        feat = torch.randn((3, C, 7), device="cuda", generator=g) / 2.65
+        wp = ops.qkv_weight_permute(w)
+        run = lambda: torch.cat(ops.qkv_feat_gemm(x, wp, feat), dim=1)  # noqa: E731
     else:
         dc, u = (torch.randn((2, C, L), device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
         run = lambda: ops.two_stage_taps_grad(dc, u, 128, 1)  # noqa: E731
