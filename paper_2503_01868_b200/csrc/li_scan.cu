@@ -35,6 +35,11 @@ constexpr int MB = 8;     // modes per register block
 #endif
 constexpr int LA = HY_LIS_LA;  // one-shot kernel: tiles prefetched into L2 ahead of the loads
 constexpr int MAXP = 64;  // poles per group
+// one-shot kernel: CTAs per SM it is compiled for (3: 24 warps at <= 80 registers, no spills;
+// the loads are latency-bound, so occupancy pays: the C3 fp32 mixer 2.40 -> 2.32 ms)
+#ifndef LIS_MINB
+#define LIS_MINB 3
+#endif
 
 template <typename T> struct Cfg;
 template <> struct Cfg<float> {
@@ -148,7 +153,7 @@ __device__ __forceinline__ void store_seg(T* __restrict__ p, int nv, const typen
 // with its 8-step history read from the row (L1 / L2 hits), so the fused mixer reads every
 // projected row once and writes y once.
 template <typename T, bool VEC, bool FEAT>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, LIS_MINB)
 li_scan_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ y,
                const double* __restrict__ res, const double* __restrict__ poles, int np, int gs, int C, int L,
                long long rows, const void* __restrict__ feat_raw, int lhf) {
