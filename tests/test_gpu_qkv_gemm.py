@@ -173,3 +173,16 @@ def test_operator_fused_projection_vs_oracle(variant, B, D, L, kw):
         want = oracle.hyena_forward(x[b], ocfg)
         assert oracle.rel_err(y[b], want) < 1e-2, b
         assert oracle.rel_err(y[b], base[b]) < 1e-2, b
+
+
+@pytest.mark.parametrize("B,D,L", [(3, 128, 256), (1, 640, 768), (2, 512, 2304), (1, 1024, 256)])
+def test_qkv_feat_gemm_shapes(B, D, L):
+    """Edge shapes: one time tile per sequence, an odd batch, odd 128-row tile counts (single-CTA
+    path: D = 128, 640), CTA pairs with a ragged time-tile count (L = 2304 = 9 tiles)."""
+    x, w, taps = _case(B, D, L, 7, 11 + D)
+    fq, u = ops.qkv_feat_gemm(x, ops.qkv_weight_permute(w), taps)
+    for b in {0, B - 1}:
+        for c in {0, D // 2 + 1, D - 1}:
+            wq, wu = _want(x, w, taps, b, c)
+            assert oracle.rel_err(fq[b, c].double().cpu().numpy(), wq) < 1e-2, (b, c)
+            assert oracle.rel_err(u[b, c].double().cpu().numpy(), wu) < 1e-2, (b, c)
