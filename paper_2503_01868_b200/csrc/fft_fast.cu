@@ -167,18 +167,25 @@ __device__ __forceinline__ float ldf(const T* p) { return Elem<T>::to_a(*p); }
 // The N1 x COL_THREADS input tile is staged through shared memory — with 16-byte streaming
 // loads when rows are 16-byte aligned (L a multiple of the vector width) — then every thread
 // transforms its column in registers and stores row k1 of r's N-point workspace row.
-template <typename T, int N1, bool FILTER>
+// PAIR (activations only, filter groups of even size): block row r carries the two channels
+// row0 + 2r and row0 + 2r + 1, which share a filter, as the real and imaginary parts of one
+// complex sequence: IFFT((A + iB) H) = A*h + i B*h for real a, b, h, so one complex transform
+// pair does the work of two (the reference's real-input FFT conv, two channels at a time).
+template <typename T, int N1, bool FILTER, bool PAIR = false>
 __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, const float2* __restrict__ hi,
                                                        const float2* __restrict__ lo, const T* __restrict__ k,
                                                        const T* __restrict__ v, const float* __restrict__ taps,
                                                        int row0, int g0, int L, int lh, int N) {
   constexpr int VEC = Elem<T>::VEC, VPR = COL_THREADS / VEC;
-  __shared__ __align__(16) float tile[N1 * COL_THREADS];
+  __shared__ __align__(16) float tile[(PAIR ? 2 : 1) * N1 * COL_THREADS];
   const int n2_0 = blockIdx.x * COL_THREADS, tid = threadIdx.x, n2 = n2_0 + tid;
   const int r = blockIdx.y;
   (void)lo;
+  for (int part = 0; part < (PAIR ? 2 : 1); ++part) {
+  float* tl = tile + part * N1 * COL_THREADS;
+  const int arow = PAIR ? row0 + 2 * r + part : row0 + r;
   if (!FILTER && L % VEC == 0) {
-    const size_t rowoff = static_cast<size_t>(row0 + r) * L;
+    const size_t rowoff = static_cast<size_t>(arow) * L;
     for (int i = tid; i < N1 * VPR; i += COL_THREADS) {
       const int n1 = i / VPR, jv = i % VPR;
       const int t = n1 * M + n2_0 + jv * VEC;
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, c
 #pragma unroll
         for (int e = 0; e < VEC; ++e) val[e] = 0.f;
       }
-      float4* dst = reinterpret_cast<float4*>(tile + n1 * COL_THREADS + jv * VEC);
+      float4* dst = reinterpret_cast<float4*>(tl + n1 * COL_THREADS + jv * VEC);
 #pragma unroll
       for (int e = 0; e < VEC / 4; ++e) dst[e] = make_float4(val[4 * e], val[4 * e + 1], val[4 * e + 2], val[4 * e + 3]);
     }
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, c
       const int t = n1 * M + n2_0 + jv * 4;
       float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
       if (t < lh) f = __ldg(reinterpret_cast<const float4*>(trow + t));
-      *reinterpret_cast<float4*>(tile + n1 * COL_THREADS + jv * 4) = f;
+      *reinterpret_cast<float4*>(tl + n1 * COL_THREADS + jv * 4) = f;
     }
   } else {
     for (int i = tid; i < N1 * COL_THREADS; i += COL_THREADS) {
@@ -215,17 +222,19 @@ __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, c
       if (FILTER) {
         if (t < lh) val = taps[static_cast<size_t>(g0 + r) * lh + t];
       } else if (t < L) {
-        const size_t off = static_cast<size_t>(row0 + r) * L + t;
+        const size_t off = static_cast<size_t>(arow) * L + t;
         val = ldf(v + off);
         if (k) val *= ldf(k + off);
       }
-      tile[i] = val;
+      tl[i] = val;
     }
+  }
   }
   __syncthreads();
   float2 x[N1];
 #pragma unroll
-  for (int n1 = 0; n1 < N1; ++n1) x[n1] = make_float2(tile[n1 * COL_THREADS + tid], 0.f);
+  for (int n1 = 0; n1 < N1; ++n1)
+    x[n1] = make_float2(tile[n1 * COL_THREADS + tid], PAIR ? tile[(N1 + n1) * COL_THREADS + tid] : 0.f);
   dft<N1, false>(x);
   const float step_n = 6.283185307179586f / static_cast<float>(N);
   float2* out = X + static_cast<size_t>(r) * N + n2;
@@ -236,11 +245,11 @@ __global__ void __launch_bounds__(COL_THREADS) col_fwd(float2* __restrict__ X, c
 
 // Inverse column pass: inverse DFT over k1, then y = q * Re(x) / N for t < L, the output tile
 // staged through shared memory for 16-byte stores (and gate loads) where rows are aligned.
-template <typename T, int N1>
+template <typename T, int N1, bool PAIR = false>
 __global__ void __launch_bounds__(COL_THREADS) col_inv(const float2* __restrict__ X, const T* __restrict__ q,
                                                        T* __restrict__ y, int row0, int L, int N) {
   constexpr int VEC = Elem<T>::VEC, VPR = COL_THREADS / VEC;
-  __shared__ __align__(16) float tile[N1 * COL_THREADS];
+  __shared__ __align__(16) float tile[(PAIR ? 2 : 1) * N1 * COL_THREADS];
   const int n2_0 = blockIdx.x * COL_THREADS, tid = threadIdx.x, n2 = n2_0 + tid;
   const int r = blockIdx.y;
   const float2* in = X + static_cast<size_t>(r) * N + n2;
@@ -250,16 +259,21 @@ __global__ void __launch_bounds__(COL_THREADS) col_inv(const float2* __restrict_
   dft<N1, true>(x);
   const float scale = 1.f / static_cast<float>(N);
 #pragma unroll
-  for (int n1 = 0; n1 < N1; ++n1) tile[n1 * COL_THREADS + tid] = x[n1].x * scale;
+  for (int n1 = 0; n1 < N1; ++n1) {
+    tile[n1 * COL_THREADS + tid] = x[n1].x * scale;
+    if (PAIR) tile[(N1 + n1) * COL_THREADS + tid] = x[n1].y * scale;  // the odd channel of the pair
+  }
   __syncthreads();
-  const size_t rowoff = static_cast<size_t>(row0 + r) * L;
+  for (int part = 0; part < (PAIR ? 2 : 1); ++part) {
+  const float* tl = tile + part * N1 * COL_THREADS;
+  const size_t rowoff = static_cast<size_t>(PAIR ? row0 + 2 * r + part : row0 + r) * L;
   if (L % VEC == 0) {
     for (int i = tid; i < N1 * VPR; i += COL_THREADS) {
       const int n1 = i / VPR, jv = i % VPR;
       const int t = n1 * M + n2_0 + jv * VEC;
       if (t >= L) continue;
       float val[VEC];
-      const float4* src = reinterpret_cast<const float4*>(tile + n1 * COL_THREADS + jv * VEC);
+      const float4* src = reinterpret_cast<const float4*>(tl + n1 * COL_THREADS + jv * VEC);
 #pragma unroll
       for (int e = 0; e < VEC / 4; ++e) {
         const float4 f = src[e];
@@ -280,10 +294,11 @@ __global__ void __launch_bounds__(COL_THREADS) col_inv(const float2* __restrict_
     for (int i = tid; i < N1 * COL_THREADS; i += COL_THREADS) {
       const int t = (i / COL_THREADS) * M + n2_0 + i % COL_THREADS;
       if (t >= L) continue;
-      float val = tile[i];
+      float val = tl[i];
       if (q) val *= ldf(q + rowoff + t);
       y[rowoff + t] = Elem<T>::from_a(val);
     }
+  }
   }
 }
 
@@ -407,6 +422,31 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
   }
 }
 
+// One block of `rows` activation rows (channels c0.., batch row offset row0): column pass, row
+// pass (times the group spectra Hf, relative to group g0), inverse column pass. Even group sizes
+// go two channels per complex transform (PAIR): the row pass then sees channel pairs, i.e. c0 / 2
+// and group size gs / 2 in its group arithmetic.
+template <typename T, int N1>
+void act_pass(float2* X, const float2* Hf, const float2* hi, const float2* lo, const void* q, const void* k,
+              const void* v, void* y, int row0, int c0, int g0, int gs, int rows, int L, int N, cudaStream_t st) {
+  const T* kk = static_cast<const T*>(k);
+  const T* vv = static_cast<const T*>(v);
+  if (gs % 2 == 0 && rows % 2 == 0 && c0 % 2 == 0) {
+    const int pr = rows / 2;
+    col_fwd<T, N1, false, true><<<dim3(M / COL_THREADS, pr), COL_THREADS, 0, st>>>(X, hi, lo, kk, vv, nullptr, row0,
+                                                                                  0, L, 0, N);
+    row_kernel<false><<<dim3(N1, pr), ROW_THREADS, ROW_SMEM, st>>>(X, Hf, hi, lo, N, c0 / 2, g0, gs / 2);
+    col_inv<T, N1, true><<<dim3(M / COL_THREADS, pr), COL_THREADS, 0, st>>>(X, static_cast<const T*>(q),
+                                                                            static_cast<T*>(y), row0, L, N);
+    return;
+  }
+  col_fwd<T, N1, false><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(X, hi, lo, kk, vv, nullptr, row0, 0, L, 0,
+                                                                            N);
+  row_kernel<false><<<dim3(N1, rows), ROW_THREADS, ROW_SMEM, st>>>(X, Hf, hi, lo, N, c0, g0, gs);
+  col_inv<T, N1><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(X, static_cast<const T*>(q), static_cast<T*>(y),
+                                                                      row0, L, N);
+}
+
 template <typename T, int N1>
 int run_n1(const void* q, const void* k, const void* v, void* y, const float* taps, int B, int C, int L, int lh,
            int gs, int N, int row_block, float2* hi, float2* lo, float2* Hf, float2* X, cudaStream_t st) {
@@ -421,11 +461,7 @@ int run_n1(const void* q, const void* k, const void* v, void* y, const float* ta
     row_kernel<true><<<dim3(N1, ng), ROW_THREADS, ROW_SMEM, st>>>(Hf, nullptr, hi, lo, N, 0, 0, 1);
     for (int b = 0; b < B; ++b) {
       const int row0 = b * C + c0;
-      col_fwd<T, N1, false><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(
-          X, hi, lo, static_cast<const T*>(k), static_cast<const T*>(v), nullptr, row0, 0, L, lh, N);
-      row_kernel<false><<<dim3(N1, rows), ROW_THREADS, ROW_SMEM, st>>>(X, Hf, hi, lo, N, c0, g0, gs);
-      col_inv<T, N1><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(X, static_cast<const T*>(q),
-                                                                          static_cast<T*>(y), row0, L, N);
+      act_pass<T, N1>(X, Hf, hi, lo, q, k, v, y, row0, c0, g0, gs, rows, L, N, st);
     }
   }
   (void)cgrid_x;
@@ -455,12 +491,7 @@ int conv_spec_n1(const void* q, const void* k, const void* v, void* y, const flo
     const int g0 = c0 / gs;
     for (int b = 0; b < B; ++b) {
       const int row0 = b * C + c0;
-      col_fwd<T, N1, false><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(
-          X, hi, lo, static_cast<const T*>(k), static_cast<const T*>(v), nullptr, row0, 0, L, 0, N);
-      row_kernel<false><<<dim3(N1, rows), ROW_THREADS, ROW_SMEM, st>>>(X, spec + static_cast<size_t>(g0) * N, hi, lo,
-                                                                       N, c0, g0, gs);
-      col_inv<T, N1><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(X, static_cast<const T*>(q),
-                                                                          static_cast<T*>(y), row0, L, N);
+      act_pass<T, N1>(X, spec + static_cast<size_t>(g0) * N, hi, lo, q, k, v, y, row0, c0, g0, gs, rows, L, N, st);
     }
   }
   return check_launch("fft_conv (cached spectrum)");

@@ -336,6 +336,9 @@ def test_li_conv_segmented_equals_natural(m):
     ("f32", 2, 4, 9000, 100, 2, True),          # N = 16384, N1 = 2, groups, batch
     ("bf16", 1, 2, 70000, 5000, 1, True),       # N = 131072, N1 = 16, lh < L
     ("f32", 1, 2, 131072, 131072, 1, True),     # N = 262144, N1 = 32 (config C3 size)
+    # even group sizes: two channels per complex transform (real / imaginary parts)
+    ("bf16", 1, 8, 131072, 131072, 4, True),
+    ("f32", 2, 6, 16384, 16384, 2, False),
 ])
 def test_fft_conv_vs_oracle(dtype, B, C, L, lh, gs, gated):
     # fp32 complex FFT conv (fft.py:128-145 semantics: zero-padded, truncated to L) vs the
