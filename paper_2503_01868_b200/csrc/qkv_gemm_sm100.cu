@@ -9,18 +9,21 @@
 // rounded projections.
 //
 // GEMM: A = the permuted weight (3D, D) K-major, B = x (B*D, L) time-major ("MN-major"), both
-// TMA-loaded (128-byte swizzle) into a 4-stage ring; one elected thread issues
-// tcgen05.mma M = 128, N = 256, K = 16 into one of two 256-column TMEM accumulators while the
-// four epilogue warps drain the other. Weight rows are permuted so that an M tile holds either
-// the q rows of 128 channels or the k rows of 64 channels over the v rows of the same 64
-// (lanes 0..63 / 64..127): each epilogue thread owns one row, runs its FIR along the columns in
-// registers, and the v threads hand fv to the k threads through shared memory for u = fk fv.
+// TMA-loaded (128-byte swizzle) into a shared-memory ring; one elected thread issues the MMAs
+// into one of two 256-column TMEM accumulators while the four epilogue warps drain the other.
+// With an even number of 128-row tiles the kernel runs on CTA pairs (cluster of 2,
+// tcgen05.mma.cta_group::2, M = 256, N = 256, K = 16, 6-stage ring of 32 KB per CTA); otherwise
+// one CTA per 128 x 256 tile (4 stages of 48 KB). Weight rows are permuted so that a 128-row tile
+// holds either the q rows of 128 channels or the k rows of 64 channels over the v rows of the
+// same 64 (lanes 0..63 / 64..127): each epilogue thread owns one row, runs its FIR along the
+// columns in registers, and the v threads hand fv to the k threads through shared memory for
+// u = fk fv.
 //
 // Time order carries the FIR history: a CTA walks its tiles of one M tile in increasing time,
 // keeping each row's last 7 raw values in registers. Work units are (M tile, run of time tiles)
-// and a unit that starts mid-sequence first computes the 64 columns before it (an N = 64
-// "halo" accumulation) for that history. Units are ordered M-group -> time segment -> M tile,
-// so the CTAs running at the same time share a few x tiles and one group's weights in L2.
+// and a unit that starts mid-sequence first accumulates the 64 (128 on CTA pairs) columns before
+// it (a "halo" pass) for that history. Units are ordered M-group -> time segment -> M tile, so
+// the CTAs running at the same time share a few x tiles and one group's weights in L2.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
