@@ -1,3 +1,5 @@
+"""Times the C3 LI operator through the default route (cuBLAS W_qkv + fused LI mixer) and the fused
+projection route (hy_qkv_feat_gemm + li_conv gated by fq), and the two routes' parts; one JSON line."""
 import json, os, sys, time
 import torch
 sys.path.insert(0, os.getcwd())
