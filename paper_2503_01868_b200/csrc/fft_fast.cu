@@ -422,6 +422,161 @@ __global__ void __launch_bounds__(ROW_THREADS, 2) row_kernel(float2* X, const fl
   }
 }
 
+// Row pass for channel pairs with per-channel filters (gs = 1). Block row r carries channels
+// a = 2r, b = 2r + 1 (relative to the block) as Z = FFT(a + i b); with Zm(k) = conj(Z(-k)) the
+// Hermitian symmetry of the real transforms gives A = (Z + Zm) / 2, B = (Z - Zm) / (2i), so
+//     W(k) = A Ha + i B Hb = Z (Ha + Hb) / 2 + Zm (Ha - Hb) / 2,   IFFT(W) = a*ha + i (b*hb).
+// -k lives in row N1 - k1 (row 0 and row N1/2: themselves), so a CTA of 2 x 256 threads takes the
+// row pair (q, N1 - q): both forward transforms into shared memory, the mirror-bin product, both
+// inverse transforms. Position p of a row after the forward stages holds frequency
+// k2 = (p >> 8) + 32 ((p >> 4) & 15) + 512 (p & 15) (the DIF digit order of the 32 x 16 x 16 stages).
+constexpr int PAIR_THREADS = 2 * ROW_THREADS;
+constexpr int PAIR_SMEM = (2 * PHYS + 128 + 64) * 8;
+__device__ __forceinline__ int rowpos_to_k2(int p) { return (p >> 8) + 32 * ((p >> 4) & 15) + 512 * (p & 15); }
+__device__ __forceinline__ int k2_to_rowpos(int k) { return 256 * (k & 31) + 16 * ((k >> 5) & 15) + (k >> 9); }
+
+__global__ void __launch_bounds__(PAIR_THREADS, 1) row_pair_kernel(float2* X, const float2* __restrict__ Hf,
+                                                                  const float2* __restrict__ hi, int N, int N1) {
+  extern __shared__ float2 sm[];
+  const int q = blockIdx.x, r = blockIdx.y;
+  const int half = threadIdx.x / ROW_THREADS, tid = threadIdx.x % ROW_THREADS;
+  const bool self = (q == 0 || 2 * q == N1);
+  const int k1 = half == 0 ? q : N1 - q;  // this half's row
+  const bool active = half == 0 || !self;
+  float2* xs = sm + half * PHYS;
+  float2* rhi = sm + 2 * PHYS;
+  float2* rk1 = rhi + 128 + 32 * half;  // [32] W_N^(256 a k1) of this half's row
+  if (tid < 128) {
+    if (half == 0) {
+      double s, c;
+      sincospi(-2.0 * static_cast<double>(64 * tid) / static_cast<double>(M), &s, &c);
+      rhi[tid] = make_float2(static_cast<float>(c), static_cast<float>(s));
+    }
+  } else if (tid < 160) {
+    const long long e = (256LL * (tid - 128) * k1) % N;
+    double s, c;
+    sincospi(-2.0 * static_cast<double>(e) / static_cast<double>(N), &s, &c);
+    rk1[tid - 128] = make_float2(static_cast<float>(c), static_cast<float>(s));
+  }
+  float2* row = X + static_cast<size_t>(r) * N + static_cast<size_t>(k1) * M;
+  const float step_n = 6.283185307179586f / static_cast<float>(N);
+  const float2 w0 = tw_n(hi, (tid * k1) & (N - 1), step_n);
+  float2 v32[32];
+  // A: DIF radix 32 over span M from HBM
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < 32; ++a) v32[a] = row[tid + 256 * a];
+  }
+  __syncthreads();  // twiddle tables
+  if (active) {
+    dft<32, false>(v32);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) xs[phys(tid + 256 * c)] = c ? cmul(v32[c], tw_m(rhi, tid * c)) : v32[c];
+  }
+  __syncthreads();
+  // B: DIF radix 16 over span 256
+  if (active) {
+#pragma unroll 1
+    for (int gg = 0; gg < 2; ++gg) {
+      const int g = tid + gg * ROW_THREADS, j = g & 15, base = (g >> 4) * 256;
+      float2 v[16];
+#pragma unroll
+      for (int a = 0; a < 16; ++a) v[a] = xs[phys(base + j + 16 * a)];
+      dft<16, false>(v);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) xs[phys(base + j + 16 * c)] = c ? cmul(v[c], tw_m(rhi, 32 * j * c)) : v[c];
+    }
+  }
+  __syncthreads();
+  // C: DIF radix 16 over span 16: the forward spectra of both rows in shared memory
+  if (active) {
+#pragma unroll 1
+    for (int gg = 0; gg < 2; ++gg) {
+      const int g = tid + gg * ROW_THREADS;
+      float2 v[16];
+#pragma unroll
+      for (int a = 0; a < 16; ++a) v[a] = xs[phys(16 * g + a)];
+      dft<16, false>(v);
+#pragma unroll
+      for (int a = 0; a < 16; ++a) xs[phys(16 * g + a)] = v[a];
+    }
+  }
+  __syncthreads();
+  // mirror-bin product: every position of this half's row, W = Z S + conj(Z(-k)) T with
+  // S, T = (Ha +- Hb) / 2 read from the two channels' spectra at the same position
+  const float2* ha = Hf + static_cast<size_t>(2 * r) * N + static_cast<size_t>(k1) * M;
+  const float2* hb = ha + N;
+  const float2* xm = sm + (self ? 0 : (1 - half)) * PHYS;  // the mirror row
+  float2 w[32];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int p = tid + 256 * i;
+      const int k2 = rowpos_to_k2(p);
+      const int k2m = k1 == 0 ? (M - k2) & (M - 1) : M - 1 - k2;
+      const float2 z = xs[phys(p)];
+      const float2 zmv = xm[phys(k2_to_rowpos(k2m))];
+      const float2 zm = make_float2(zmv.x, -zmv.y);
+      const float2 a = __ldg(ha + p), b = __ldg(hb + p);
+      const float2 S = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
+      const float2 T = make_float2(0.5f * (a.x - b.x), 0.5f * (a.y - b.y));
+      const float2 zs = cmul(z, S), zt = cmul(zm, T);
+      w[i] = make_float2(zs.x + zt.x, zs.y + zt.y);
+    }
+  }
+  __syncthreads();  // every mirror read is done before the rows are overwritten
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) xs[phys(tid + 256 * i)] = w[i];
+  }
+  __syncthreads();
+  // C': inverse radix 16 over span 16
+  if (active) {
+#pragma unroll 1
+    for (int gg = 0; gg < 2; ++gg) {
+      const int g = tid + gg * ROW_THREADS;
+      float2 v[16];
+#pragma unroll
+      for (int a = 0; a < 16; ++a) v[a] = xs[phys(16 * g + a)];
+      dft<16, true>(v);
+#pragma unroll
+      for (int a = 0; a < 16; ++a) xs[phys(16 * g + a)] = v[a];
+    }
+  }
+  __syncthreads();
+  // D: DIT radix 16 over span 256: conj twiddle, inverse DFT
+  if (active) {
+#pragma unroll 1
+    for (int gg = 0; gg < 2; ++gg) {
+      const int g = tid + gg * ROW_THREADS, j = g & 15, base = (g >> 4) * 256;
+      float2 v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float2 x = xs[phys(base + j + 16 * c)];
+        v[c] = c ? cmulc(x, tw_m(rhi, 32 * j * c)) : x;
+      }
+      dft<16, true>(v);
+#pragma unroll
+      for (int a = 0; a < 16; ++a) xs[phys(base + j + 16 * a)] = v[a];
+    }
+  }
+  __syncthreads();
+  // E: DIT radix 32 over span M, times W_N^(-n2 k1), to HBM
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float2 x = xs[phys(tid + 256 * c)];
+      v32[c] = c ? cmulc(x, tw_m(rhi, tid * c)) : x;
+    }
+    dft<32, true>(v32);
+#pragma unroll
+    for (int a = 0; a < 32; ++a) {
+      const int n2 = tid + 256 * a;
+      row[n2] = k1 ? cmulc(v32[a], cmul(w0, rk1[a])) : v32[a];
+    }
+  }
+}
+
 // One block of `rows` activation rows (channels c0.., batch row offset row0): column pass, row
 // pass (times the group spectra Hf, relative to group g0), inverse column pass. Even group sizes
 // go two channels per complex transform (PAIR): the row pass then sees channel pairs, i.e. c0 / 2
@@ -440,6 +595,16 @@ void act_pass(float2* X, const float2* Hf, const float2* hi, const float2* lo, c
                                                                             static_cast<T*>(y), row0, L, N);
     return;
   }
+  if (gs == 1 && rows % 2 == 0) {  // per-channel filters: channel pairs with the mirror-bin product
+    const int pr = rows / 2;
+    col_fwd<T, N1, false, true><<<dim3(M / COL_THREADS, pr), COL_THREADS, 0, st>>>(X, hi, lo, kk, vv, nullptr, row0,
+                                                                                  0, L, 0, N);
+    row_pair_kernel<<<dim3(N1 / 2 + 1, pr), PAIR_THREADS, PAIR_SMEM, st>>>(X, Hf + static_cast<size_t>(c0 - g0) * N, hi,
+                                                                          N, N1);
+    col_inv<T, N1, true><<<dim3(M / COL_THREADS, pr), COL_THREADS, 0, st>>>(X, static_cast<const T*>(q),
+                                                                            static_cast<T*>(y), row0, L, N);
+    return;
+  }
   col_fwd<T, N1, false><<<dim3(M / COL_THREADS, rows), COL_THREADS, 0, st>>>(X, hi, lo, kk, vv, nullptr, row0, 0, L, 0,
                                                                             N);
   row_kernel<false><<<dim3(N1, rows), ROW_THREADS, ROW_SMEM, st>>>(X, Hf, hi, lo, N, c0, g0, gs);
@@ -452,6 +617,7 @@ int run_n1(const void* q, const void* k, const void* v, void* y, const float* ta
            int gs, int N, int row_block, float2* hi, float2* lo, float2* Hf, float2* X, cudaStream_t st) {
   ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<true>), ROW_SMEM);
   ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<false>), ROW_SMEM);
+  ensure_smem_attr(reinterpret_cast<const void*>(row_pair_kernel), PAIR_SMEM);
   const dim3 cgrid_x(M / COL_THREADS);
   for (int c0 = 0; c0 < C; c0 += row_block) {
     const int rows = C - c0 < row_block ? C - c0 : row_block;
@@ -486,6 +652,7 @@ template <typename T, int N1>
 int conv_spec_n1(const void* q, const void* k, const void* v, void* y, const float2* spec, int B, int C, int L,
                  int gs, int N, int row_block, float2* hi, float2* lo, float2* X, cudaStream_t st) {
   ensure_smem_attr(reinterpret_cast<const void*>(row_kernel<false>), ROW_SMEM);
+  ensure_smem_attr(reinterpret_cast<const void*>(row_pair_kernel), PAIR_SMEM);
   for (int c0 = 0; c0 < C; c0 += row_block) {
     const int rows = C - c0 < row_block ? C - c0 : row_block;
     const int g0 = c0 / gs;

@@ -339,6 +339,9 @@ def test_li_conv_segmented_equals_natural(m):
     # even group sizes: two channels per complex transform (real / imaginary parts)
     ("bf16", 1, 8, 131072, 131072, 4, True),
     ("f32", 2, 6, 16384, 16384, 2, False),
+    # per-channel filters in pairs: the mirror-bin product (rows k1 and N1 - k1 in one CTA)
+    ("f32", 2, 6, 9000, 9000, 1, True),          # N1 = 2: both rows self-paired
+    ("f32", 1, 4, 65536, 30000, 1, False),       # N1 = 16
 ])
 def test_fft_conv_vs_oracle(dtype, B, C, L, lh, gs, gated):
     # fp32 complex FFT conv (fft.py:128-145 semantics: zero-padded, truncated to L) vs the
