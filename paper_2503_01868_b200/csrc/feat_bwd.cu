@@ -207,18 +207,31 @@ feat_bwd_kernel(const T* __restrict__ proj, const T* __restrict__ gmix, const T*
     }
     if (++k == nch) k = 0, ++row;
     // featurizers and gate products
+    // (packed FFMA2 on output pairs (e, e + 1); each output keeps the scalar accumulation order)
     float dk[8], dv[8], dq[8];
+    {
+      float2 fk2[4], fv2[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float fk = 0.f, fv = 0.f;
+      for (int i = 0; i < 4; ++i) fk2[i] = fv2[i] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
-        fk = fmaf(Fk[j], wk[8 + e - j], fk);
-        fv = fmaf(Fv[j], wv[8 + e - j], fv);
+        const float2 tk = make_float2(Fk[j], Fk[j]), tv = make_float2(Fv[j], Fv[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int x0 = 8 + 2 * i - j;
+          fk2[i] = __ffma2_rn(tk, make_float2(wk[x0], wk[x0 + 1]), fk2[i]);
+          fv2[i] = __ffma2_rn(tv, make_float2(wv[x0], wv[x0 + 1]), fv2[i]);
+        }
       }
-      dk[e] = d[e] * fv;
-      dv[e] = d[e] * fk;
-      dq[e] = gq[e] * cq[e];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        dk[2 * i] = d[2 * i] * fv2[i].x;
+        dk[2 * i + 1] = d[2 * i + 1] * fv2[i].y;
+        dv[2 * i] = d[2 * i] * fk2[i].x;
+        dv[2 * i + 1] = d[2 * i + 1] * fk2[i].y;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dq[e] = gq[e] * cq[e];
     }
     // tap gradients (lane 31's steps belong to the next chunk)
     if (lane < 31) {
@@ -244,19 +257,33 @@ feat_bwd_kernel(const T* __restrict__ proj, const T* __restrict__ gmix, const T*
       }
     }
     float oq[8], ok_[8], ov[8];
+    {
+      float xq[16], xk[16], xv[16];  // this lane's d-features, then the next lane's first NF - 1
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float sq = 0.f, sk = 0.f, sv = 0.f;
+      for (int e = 0; e < 8; ++e) {
+        xq[e] = dq[e], xk[e] = dk[e], xv[e] = dv[e];
+        xq[8 + e] = nq[e], xk[8 + e] = nk[e], xv[8 + e] = nv[e];
+      }
+      float2 sq2[4], sk2[4], sv2[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sq2[i] = sk2[i] = sv2[i] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
-        const float xq = e + j < 8 ? dq[e + j] : nq[e + j - 8];
-        const float xk = e + j < 8 ? dk[e + j] : nk[e + j - 8];
-        const float xv = e + j < 8 ? dv[e + j] : nv[e + j - 8];
-        sq = fmaf(Fq[j], xq, sq);
-        sk = fmaf(Fk[j], xk, sk);
-        sv = fmaf(Fv[j], xv, sv);
+        const float2 tq = make_float2(Fq[j], Fq[j]), tk = make_float2(Fk[j], Fk[j]), tv = make_float2(Fv[j], Fv[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int x0 = 2 * i + j;
+          sq2[i] = __ffma2_rn(tq, make_float2(xq[x0], xq[x0 + 1]), sq2[i]);
+          sk2[i] = __ffma2_rn(tk, make_float2(xk[x0], xk[x0 + 1]), sk2[i]);
+          sv2[i] = __ffma2_rn(tv, make_float2(xv[x0], xv[x0 + 1]), sv2[i]);
+        }
       }
-      oq[e] = sq, ok_[e] = sk, ov[e] = sv;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        oq[2 * i] = sq2[i].x, oq[2 * i + 1] = sq2[i].y;
+        ok_[2 * i] = sk2[i].x, ok_[2 * i + 1] = sk2[i].y;
+        ov[2 * i] = sv2[i].x, ov[2 * i + 1] = sv2[i].y;
+      }
     }
     if (lane < 31 && tl < L) {
       const int b = cur_row / C, c = cur_row - b * C;
