@@ -80,7 +80,7 @@ struct Warps {
   static constexpr int THREADS = (PROD + N_PROD_WARPS) * 32;
 };
 constexpr int CONV_THREADS = N_CONV_WARPS * 32, TB_THREADS = N_TB_WARPS * 32;
-constexpr uint32_t BAR_CONV = 1, BAR_TB = 2;
+constexpr uint32_t BAR_CONV = 1, BAR_TB = 2, BAR_EPI = 3;
 
 // Ring depth of the per-tile buffers between converter, main MMA and epilogue
 // (U / U_prev / featurized q in SMEM, accumulators in TMEM).
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       mbar_init(&ufull[i], 1);
       mbar_init(&uempty[i], 1);
       mbar_init(&qfull[i], 1);
-      mbar_init(&qempty[i], N_EPI_WARPS);
+      mbar_init(&qempty[i], 1);  // the epilogue's store issuer, once its bulk store has read the buffer
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], N_EPI_WARPS);
     }
@@ -646,6 +646,13 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
     // ------------------------------------------------------------ epilogue
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int tout = quarter * 32 + lane;
+    const int etid = threadIdx.x - W_EPI0 * 32;
+    // y = q * acc goes into the tile's featurized-q buffer in place (each thread overwrites only
+    // the elements it read), then ONE 1-D bulk store writes the tile's contiguous y segment (the
+    // tile is 4096 consecutive steps of one row): one instruction instead of 32 2-byte stores per
+    // thread. The buffer returns to the converters (qempty) once a later store wait has seen the
+    // bulk store read it, one tile deferred so the issuer never stalls on its own store.
+    int prev_a = -1;
     Tile t;
     t.init(tb, p);
     for (int it = 0; it < ntiles; ++it, t.next(p)) {
@@ -660,19 +667,31 @@ __global__ void __launch_bounds__(Warps<IMPL>::THREADS, 1) two_stage_kernel(cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
       if (GQ) mbar_wait(&qfull[a], aph);
-      const bf16* fq = reinterpret_cast<const bf16*>(smem + LY::OFF_FQ + a * NCH * LB * 2);
+      bf16* stg = reinterpret_cast<bf16*>(smem + LY::OFF_FQ + a * NCH * LB * 2);
       bf16* yrow = p.y + elem_off(p, t.b * p.C + t.c, t.t0);
       const int nt = min(TILE_T, p.L - t.t0);
 #pragma unroll
       for (int n = 0; n < NCH; ++n) {
         const int tt = n * LB + tout;
         float val = acc[n];
-        if (GQ) val *= __bfloat162float(fq[tt]);
-        if (tt < nt) yrow[tt] = __float2bfloat16_rn(val);
+        if (GQ) val *= __bfloat162float(stg[tt]);
+        stg[tt] = __float2bfloat16_rn(val);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&qempty[a]);
+      fence_proxy_async();  // the generic writes above, before the async-proxy bulk read
+      named_bar_sync(BAR_EPI, N_EPI_WARPS * 32);
+      if (etid == 0) {
+        bulk_s2g(yrow, stg, static_cast<uint32_t>(nt) * 2);
+        bulk_commit();
+        bulk_wait_read<1>();  // every earlier tile's store has read its buffer
+        if (GQ && prev_a >= 0) mbar_arrive(&qempty[prev_a]);
+      }
+      prev_a = a;
       if (quarter == 0 && lane == 0) trace(p, it, 6);
+    }
+    if (etid == 0) {
+      bulk_wait_read<0>();
+      if (GQ && prev_a >= 0) mbar_arrive(&qempty[prev_a]);
+      bulk_wait<0>();
     }
   } else if (warp == W_SCAN) {
     // ------------------------------------------------------------ IMPL state scan
